@@ -1,0 +1,381 @@
+// api.cu — the C ABI (include/pipnn.h): validation, workspace sizing, stream plumbing, stage timing.
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace pipnn {
+
+static thread_local std::string g_last_error;
+static thread_local size_t g_required_ws = 0;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+pipnn_status fail(pipnn_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+bool sync_debug() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("PIPNN_SYNC_DEBUG");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+pipnn_status validate_points(const pipnn_points* X) {
+  if (!X) return fail(PIPNN_EINVAL, "X is NULL");
+  if (X->n < 1) return fail(PIPNN_EINVAL, "n must be >= 1");
+  if (X->n > 0xFFFFFFFEll) return fail(PIPNN_EUNSUPPORTED, "n must fit in 32-bit ids");
+  if (X->d < 1 || X->ld < X->d) return fail(PIPNN_EINVAL, "need d >= 1 and ld >= d");
+  if (!X->data) return fail(PIPNN_EINVAL, "X->data is NULL");
+  if (X->dtype != PIPNN_U8 && X->dtype != PIPNN_F32) return fail(PIPNN_EINVAL, "dtype must be PIPNN_U8 or PIPNN_F32");
+  if (X->metric != PIPNN_L2 && X->metric != PIPNN_MIPS) return fail(PIPNN_EINVAL, "metric must be L2 or MIPS");
+  if (X->dtype == PIPNN_U8 && X->metric == PIPNN_MIPS) return fail(PIPNN_EINVAL, "uint8 + MIPS is not supported (S:27)");
+  if (tiled_row_bytes(X) > 512)
+    return fail(PIPNN_EUNSUPPORTED, "d too large for this build (uint8 d <= 512, float32 d <= 240)");
+  return PIPNN_OK;
+}
+
+static pipnn_status validate_part(const pipnn_partition_params* p) {
+  if (!p) return fail(PIPNN_EINVAL, "partition params NULL");
+  if (p->c_max < 2 || p->c_max > 4096) return fail(PIPNN_EINVAL, "c_max must be in [2, 4096]");
+  if (p->c_min < 1 || 3ll * p->c_min >= p->c_max) return fail(PIPNN_EINVAL, "need 1 <= c_min and 3*c_min < c_max");
+  if (p->p_samp_num < 1 || p->p_samp_den < 1) return fail(PIPNN_EINVAL, "p_samp must be a positive rational");
+  if (p->leader_cap < 2 || p->leader_cap > 4096) return fail(PIPNN_EINVAL, "leader_cap must be in [2, 4096]");
+  if (p->n_fanout < 1 || p->n_fanout > 4) return fail(PIPNN_EINVAL, "n_fanout must be in [1, 4]");
+  for (int i = 0; i < p->n_fanout; ++i)
+    if (p->fanout[i] < 1 || p->fanout[i] > 16) return fail(PIPNN_EINVAL, "fanout[i] must be in [1, 16]");
+  if (p->replicas < 1 || p->replicas > 64) return fail(PIPNN_EINVAL, "replicas must be in [1, 64]");
+  return PIPNN_OK;
+}
+static pipnn_status validate_hp(const pipnn_hashprune_params* p) {
+  if (!p) return fail(PIPNN_EINVAL, "hashprune params NULL");
+  if (p->m < 1 || p->m > 16) return fail(PIPNN_EINVAL, "m must be in [1, 16] (2-byte hash, P:446)");
+  if (p->l_max < 1 || p->l_max > 1024) return fail(PIPNN_EINVAL, "l_max must be in [1, 1024]");
+  return PIPNN_OK;
+}
+static pipnn_status validate_prune(const pipnn_prune_params* p) {
+  if (!p) return fail(PIPNN_EINVAL, "prune params NULL");
+  if (p->R < 1 || p->R > 256) return fail(PIPNN_EINVAL, "R must be in [1, 256]");
+  if (p->alpha_num < 1 || p->alpha_den < 1) return fail(PIPNN_EINVAL, "alpha must be a positive rational");
+  return PIPNN_OK;
+}
+
+static int64_t prod_fanout(const pipnn_partition_params* p) {
+  int64_t f = 1;
+  for (int i = 0; i < p->n_fanout; ++i) f *= p->fanout[i];
+  return f * p->replicas;
+}
+
+// ws == NULL or too small -> PIPNN_EWORKSPACE with the requirement in pipnn_required_workspace()
+// (two-call size query).
+static pipnn_status check_ws(void* ws, size_t ws_bytes, size_t need) {
+  need += 4096;
+  g_required_ws = need;
+  if (!ws || ws_bytes < need)
+    return fail(PIPNN_EWORKSPACE, "workspace too small: need " + std::to_string(need) + " bytes");
+  if ((reinterpret_cast<uintptr_t>(ws) & 255) != 0) return fail(PIPNN_EINVAL, "workspace must be 256-B aligned");
+  return PIPNN_OK;
+}
+
+// The first 256 B of every workspace hold the device error flag.
+static int* err_slot(Arena& ar) { return ar.take<int>(64); }
+
+static pipnn_status pending_cuda() {
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(PIPNN_ECUDA, std::string("pending CUDA error: ") + cudaGetErrorString(e));
+  }
+  return PIPNN_OK;
+}
+
+static pipnn_status read_dev_error(int* err, cudaStream_t st) {
+  int h = 0;
+  PIPNN_CUDA(cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PIPNN_CUDA(cudaStreamSynchronize(st));
+  if (h == DERR_NONFINITE) return fail(PIPNN_EINVAL, "non-finite float input");
+  if (h != 0) return fail(PIPNN_ECUDA, "device error flag " + std::to_string(h) + " (bounded wait timeout / capacity)");
+  return PIPNN_OK;
+}
+
+// ------------------------------------------------------------------ build-level workspace plan
+struct BuildPlan {
+  int64_t leaf_ids_cap, leaf_off_cap;
+};
+static BuildPlan plan_of(const pipnn_points* X, const pipnn_build_params* p) {
+  BuildPlan b;
+  b.leaf_ids_cap = X->n * prod_fanout(&p->part);
+  b.leaf_off_cap = b.leaf_ids_cap + 1;
+  return b;
+}
+
+// Runs the whole build through an Arena; with a measuring Arena it only sizes the workspace.
+static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* p, Arena& ar, cudaStream_t st,
+                               uint64_t* row_ptr, uint32_t* col_idx, int64_t* n_edges_h, pipnn_stats* stats_h) {
+  const BuildPlan bp = plan_of(X, p);
+  int* err = err_slot(ar);
+  Ctx c{st, err};
+  int64_t* leaf_off = ar.take<int64_t>(bp.leaf_off_cap);
+  uint32_t* leaf_ids = ar.take<uint32_t>(bp.leaf_ids_cap);
+  const int k = p->pick.k;
+  uint32_t* nbr = ar.take<uint32_t>((size_t)bp.leaf_ids_cap * k);
+  float* dist = ar.take<float>((size_t)bp.leaf_ids_cap * k);
+  const bool sk_int = X->dtype == PIPNN_U8;
+  void* sketch = ar.take<int32_t>((size_t)X->n * p->hp.m);
+  uint64_t* slots = ar.take<uint64_t>((size_t)X->n * p->hp.l_max);
+  uint32_t* count = ar.take<uint32_t>(X->n);
+  int64_t* n_edges_dev = ar.take<int64_t>(1);
+  const size_t mark = ar.mark();
+
+  cudaEvent_t ev[7];
+  if (!ar.measuring()) {
+    if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small");
+    for (auto& e : ev) PIPNN_CUDA(cudaEventCreate(&e));
+    PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+    PIPNN_CUDA(cudaEventRecord(ev[0], st));
+  }
+  auto cleanup = [&]() {
+    if (!ar.measuring())
+      for (auto& e : ev) cudaEventDestroy(e);
+  };
+  // (a0) sketches
+  pipnn_status s = sketch_impl(X, p->hp.m, p->hp.seed, sketch, ar, c);
+  if (s != PIPNN_OK) { cleanup(); return s; }
+  ar.release(mark);
+  if (!ar.measuring()) cudaEventRecord(ev[1], st);
+  // (a1, a2) partition (Alg. 5)
+  int64_t n_leaves = 0, n_inst = 0;
+  int depth = 0;
+  s = partition_impl(X, &p->part, leaf_off, bp.leaf_off_cap, leaf_ids, bp.leaf_ids_cap, &n_leaves, &n_inst, &depth,
+                     ar, c);
+  if (s != PIPNN_OK) { cleanup(); return s; }
+  ar.release(mark);
+  if (ar.measuring()) n_inst = bp.leaf_ids_cap;  // size the later stages at their upper bounds
+  if (!ar.measuring()) cudaEventRecord(ev[2], st);
+  // (a3, a4) leaf distance tiles + fused pick, in waves of at most `budget` 128-row blocks so
+  // the tiled leaf buffer stays bounded (one wave at 1M points).
+  const int64_t budget = std::min<int64_t>(bp.leaf_ids_cap / 64 + 1024, (int64_t)1 << 16);
+  if (ar.measuring()) {
+    s = leaf_pick_impl(X, nullptr, nullptr, budget, budget * 128, k, nbr, dist, ar, c, budget);
+    if (s != PIPNN_OK) { cleanup(); return s; }
+  } else if (n_leaves > 0) {
+    std::vector<int64_t> off(n_leaves + 1);
+    PIPNN_CUDA(cudaMemcpyAsync(off.data(), leaf_off, (n_leaves + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    PIPNN_CUDA(cudaStreamSynchronize(st));
+    int64_t b0 = 0;
+    while (b0 < n_leaves) {
+      int64_t items = 0, b1 = b0;
+      while (b1 < n_leaves && items + ceil_div(off[b1 + 1] - off[b1], 128) <= budget) {
+        items += ceil_div(off[b1 + 1] - off[b1], 128);
+        ++b1;
+      }
+      if (b1 == b0) { cleanup(); return fail(PIPNN_EUNSUPPORTED, "leaf larger than the wave budget"); }
+      s = leaf_pick_impl(X, leaf_off + b0, leaf_ids, b1 - b0, off[b1] - off[b0], k, nbr, dist, ar, c, budget);
+      if (s != PIPNN_OK) { cleanup(); return s; }
+      ar.release(mark);
+      b0 = b1;
+    }
+  }
+  ar.release(mark);
+  if (!ar.measuring()) cudaEventRecord(ev[3], st);
+  // (a5, a6) bidirected edges -> HashPrune reservoirs (Alg. 3)
+  if (!ar.measuring()) {
+    PIPNN_CUDA(cudaMemsetAsync(slots, 0xFF, (size_t)X->n * p->hp.l_max * sizeof(uint64_t), st));
+    PIPNN_CUDA(cudaMemsetAsync(count, 0, (size_t)X->n * sizeof(uint32_t), st));
+  }
+  s = hashprune_from_lists(p->hp.m, p->hp.l_max, X->n, sketch, sk_int, slots, count, leaf_ids, n_inst, k, nbr, dist,
+                           n_edges_dev, ar, c);
+  if (s != PIPNN_OK) { cleanup(); return s; }
+  ar.release(mark);
+  if (!ar.measuring()) cudaEventRecord(ev[4], st);
+  // (a7, a8) final prune + CSR
+  s = final_prune_impl(X, p->hp.l_max, slots, count, &p->prune, row_ptr, col_idx, ar, c);
+  if (s != PIPNN_OK) { cleanup(); return s; }
+  if (ar.measuring()) return PIPNN_OK;
+  PIPNN_CUDA(cudaEventRecord(ev[5], st));
+  uint64_t ne = 0;
+  int64_t nstream = 0;
+  PIPNN_CUDA(cudaMemcpyAsync(&ne, row_ptr + X->n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  PIPNN_CUDA(cudaMemcpyAsync(&nstream, n_edges_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  s = read_dev_error(err, st);
+  if (s != PIPNN_OK) { cleanup(); return s; }
+  if (n_edges_h) *n_edges_h = (int64_t)ne;
+  if (stats_h) {
+    float t[6];
+    for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+    cudaEventElapsedTime(&t[5], ev[0], ev[5]);
+    stats_h->ms_prep = t[0];
+    stats_h->ms_partition = t[1];
+    stats_h->ms_leaf = t[2];
+    stats_h->ms_hashprune = t[3];
+    stats_h->ms_final = t[4];
+    stats_h->ms_total = t[5];
+    stats_h->n_leaves = n_leaves;
+    stats_h->n_instances = n_inst;
+    stats_h->n_edges = nstream;
+    stats_h->depth = depth;
+    int64_t mx = 0;
+    if (n_leaves > 0) {
+      std::vector<int64_t> off(n_leaves + 1);
+      cudaMemcpy(off.data(), leaf_off, (n_leaves + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost);
+      for (int64_t b = 0; b < n_leaves; ++b) mx = std::max(mx, off[b + 1] - off[b]);
+    }
+    stats_h->max_leaf = mx;
+  }
+  cleanup();
+  return PIPNN_OK;
+}
+
+}  // namespace pipnn
+
+using namespace pipnn;
+
+extern "C" {
+
+const char* pipnn_last_error(void) { return g_last_error.c_str(); }
+size_t pipnn_required_workspace(void) { return g_required_ws; }
+int32_t pipnn_abi_version(void) { return PIPNN_ABI_VERSION; }
+
+pipnn_status pipnn_workspace_size(const pipnn_points* X, const pipnn_build_params* p, size_t* bytes_h) {
+  PIPNN_TRY(validate_points(X));
+  if (!p || !bytes_h) return fail(PIPNN_EINVAL, "NULL argument");
+  PIPNN_TRY(validate_part(&p->part));
+  PIPNN_TRY(validate_hp(&p->hp));
+  PIPNN_TRY(validate_prune(&p->prune));
+  if (p->pick.k < 1 || p->pick.k > 15) return fail(PIPNN_EINVAL, "k must be in [1, 15]");
+  Arena ar;  // measuring
+  PIPNN_TRY(build_impl(X, p, ar, nullptr, nullptr, nullptr, nullptr, nullptr));
+  *bytes_h = ar.peak + 4096;
+  g_required_ws = *bytes_h;
+  return PIPNN_OK;
+}
+
+// Device error flag of the last call that used `ws` (synchronises `stream`). Test/diagnostic hook.
+pipnn_status pipnn_device_error(void* ws, void* stream) {
+  if (!ws) return fail(PIPNN_EINVAL, "ws NULL");
+  PIPNN_TRY(pending_cuda());
+  return read_dev_error((int*)ws, (cudaStream_t)stream);
+}
+
+pipnn_status pipnn_partition(const pipnn_points* X, const pipnn_partition_params* p, void* ws, size_t ws_bytes,
+                             int64_t* leaf_off, int64_t leaf_off_cap, uint32_t* leaf_ids, int64_t leaf_ids_cap,
+                             int64_t* n_leaves_h, int64_t* n_instances_h, void* stream) {
+  PIPNN_TRY(validate_points(X));
+  PIPNN_TRY(validate_part(p));
+  if (!leaf_off || !leaf_ids || !n_leaves_h || !n_instances_h) return fail(PIPNN_EINVAL, "NULL output");
+  const int64_t need_ids = X->n * prod_fanout(p);
+  if (leaf_ids_cap < need_ids)
+    return fail(PIPNN_ECAPACITY, "leaf_ids_cap must be >= n*prod(fanout)*replicas = " + std::to_string(need_ids));
+  if (leaf_off_cap < need_ids + 1)
+    return fail(PIPNN_ECAPACITY, "leaf_off_cap must be >= " + std::to_string(need_ids + 1));
+  cudaStream_t st = (cudaStream_t)stream;
+  Arena m;
+  m.take<int>(64);
+  int dummy_depth = 0;
+  int64_t a = 0, b = 0;
+  PIPNN_TRY(partition_impl(X, p, nullptr, leaf_off_cap, nullptr, leaf_ids_cap, &a, &b, &dummy_depth, m, Ctx{st, nullptr}));
+  PIPNN_TRY(check_ws(ws, ws_bytes, m.peak));
+  PIPNN_TRY(pending_cuda());
+  Arena ar(ws, ws_bytes);
+  int* err = err_slot(ar);
+  PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+  int depth = 0;
+  PIPNN_TRY(partition_impl(X, p, leaf_off, leaf_off_cap, leaf_ids, leaf_ids_cap, n_leaves_h, n_instances_h, &depth, ar,
+                           Ctx{st, err}));
+  return read_dev_error(err, st);
+}
+
+pipnn_status pipnn_leaf_pick(const pipnn_points* X, const int64_t* leaf_off, const uint32_t* leaf_ids,
+                             int64_t n_leaves, int64_t n_instances, const pipnn_pick_params* p, uint32_t* nbr,
+                             float* dist, void* ws, size_t ws_bytes, void* stream) {
+  PIPNN_TRY(validate_points(X));
+  if (!p || p->k < 1 || p->k > 15) return fail(PIPNN_EINVAL, "k must be in [1, 15]");
+  if (n_leaves < 0 || n_instances < 0) return fail(PIPNN_EINVAL, "negative sizes");
+  if (n_leaves > 0 && (!leaf_off || !leaf_ids || !nbr)) return fail(PIPNN_EINVAL, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  Arena m;
+  m.take<int>(64);
+  PIPNN_TRY(leaf_pick_impl(X, leaf_off, leaf_ids, n_leaves, n_instances, p->k, nbr, dist, m, Ctx{st, nullptr}));
+  PIPNN_TRY(check_ws(ws, ws_bytes, m.peak));
+  PIPNN_TRY(pending_cuda());
+  Arena ar(ws, ws_bytes);
+  int* err = err_slot(ar);
+  PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+  return leaf_pick_impl(X, leaf_off, leaf_ids, n_leaves, n_instances, p->k, nbr, dist, ar, Ctx{st, err});
+}
+
+pipnn_status pipnn_sketch(const pipnn_points* X, const pipnn_hashprune_params* p, void* sketch, void* ws,
+                          size_t ws_bytes, void* stream) {
+  PIPNN_TRY(validate_points(X));
+  PIPNN_TRY(validate_hp(p));
+  if (!sketch) return fail(PIPNN_EINVAL, "sketch NULL");
+  cudaStream_t st = (cudaStream_t)stream;
+  Arena m;
+  m.take<int>(64);
+  PIPNN_TRY(sketch_impl(X, p->m, p->seed, sketch, m, Ctx{st, nullptr}));
+  PIPNN_TRY(check_ws(ws, ws_bytes, m.peak));
+  PIPNN_TRY(pending_cuda());
+  Arena ar(ws, ws_bytes);
+  int* err = err_slot(ar);
+  PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+  return sketch_impl(X, p->m, p->seed, sketch, ar, Ctx{st, err});
+}
+
+pipnn_status hashprune_insert(const pipnn_hashprune_params* p, int64_t n, const void* sketch, int32_t sk_dtype,
+                              uint64_t* slots, uint32_t* count, const uint32_t* owner, const uint32_t* cand,
+                              const float* dist, int64_t n_edges, void* ws, size_t ws_bytes, void* stream) {
+  PIPNN_TRY(validate_hp(p));
+  if (n < 1 || n > 0xFFFFFFFEll) return fail(PIPNN_EINVAL, "n out of range");
+  if (n_edges < 0) return fail(PIPNN_EINVAL, "n_edges < 0");
+  if (!sketch || !slots || !count) return fail(PIPNN_EINVAL, "NULL argument");
+  if (n_edges > 0 && (!owner || !cand || !dist)) return fail(PIPNN_EINVAL, "NULL edge arrays");
+  if (sk_dtype != PIPNN_U8 && sk_dtype != PIPNN_F32) return fail(PIPNN_EINVAL, "sk_dtype");
+  cudaStream_t st = (cudaStream_t)stream;
+  Arena m;
+  m.take<int>(64);
+  PIPNN_TRY(hashprune_impl(p->m, p->l_max, n, sketch, sk_dtype == PIPNN_U8, slots, count, owner, cand, dist, n_edges, m,
+                           Ctx{st, nullptr}));
+  PIPNN_TRY(check_ws(ws, ws_bytes, m.peak));
+  PIPNN_TRY(pending_cuda());
+  Arena ar(ws, ws_bytes);
+  int* err = err_slot(ar);
+  PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+  return hashprune_impl(p->m, p->l_max, n, sketch, sk_dtype == PIPNN_U8, slots, count, owner, cand, dist, n_edges, ar,
+                        Ctx{st, err});
+}
+
+pipnn_status pipnn_final_prune(const pipnn_points* X, const pipnn_hashprune_params* hp, const uint64_t* slots,
+                               const uint32_t* count, const pipnn_prune_params* p, uint64_t* row_ptr,
+                               uint32_t* col_idx, void* ws, size_t ws_bytes, void* stream) {
+  PIPNN_TRY(validate_points(X));
+  PIPNN_TRY(validate_hp(hp));
+  PIPNN_TRY(validate_prune(p));
+  if (!slots || !count || !row_ptr || !col_idx) return fail(PIPNN_EINVAL, "NULL argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  Arena m;
+  m.take<int>(64);
+  PIPNN_TRY(final_prune_impl(X, hp->l_max, slots, count, p, row_ptr, col_idx, m, Ctx{st, nullptr}));
+  PIPNN_TRY(check_ws(ws, ws_bytes, m.peak));
+  PIPNN_TRY(pending_cuda());
+  Arena ar(ws, ws_bytes);
+  int* err = err_slot(ar);
+  PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+  return final_prune_impl(X, hp->l_max, slots, count, p, row_ptr, col_idx, ar, Ctx{st, err});
+}
+
+pipnn_status pipnn_build(const pipnn_points* X, const pipnn_build_params* p, void* ws, size_t ws_bytes,
+                         uint64_t* row_ptr, uint32_t* col_idx, int64_t* n_edges_h, pipnn_stats* stats_h, void* stream) {
+  size_t need = 0;
+  PIPNN_TRY(pipnn_workspace_size(X, p, &need));
+  if (!row_ptr || !col_idx) return fail(PIPNN_EINVAL, "NULL output");
+  PIPNN_TRY(check_ws(ws, ws_bytes, need - 4096));
+  PIPNN_TRY(pending_cuda());
+  Arena ar(ws, ws_bytes);
+  return build_impl(X, p, ar, (cudaStream_t)stream, row_ptr, col_idx, n_edges_h, stats_h);
+}
+
+}  // extern "C"

@@ -1,0 +1,27 @@
+// dist_topk.cu — instantiations + launcher of the distance-tile / top-k kernel (dist_topk.cuh).
+#include "dist_topk.cuh"
+
+namespace pipnn {
+
+template <bool U8, bool MIPS>
+static pipnn_status launch_one(const DistTopkArgs& a, cudaStream_t st) {
+  const int smem = dt_smem_bytes(a.Kb);
+  auto* fn = dist_topk_kernel<U8, MIPS>;
+  PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  fn<<<num_sms(), kDtThreads, smem, st>>>(a);
+  PIPNN_LAUNCHED("dist_topk_kernel", st);
+  return PIPNN_OK;
+}
+
+// kmax: the largest running-list length any segment needs (k + 1 with self exclusion).
+pipnn_status launch_dist_topk(const DistTopkArgs& a, bool u8, bool mips, int kmax, cudaStream_t st) {
+  if (a.Kb <= 0 || a.Kb % 32 != 0 || a.Kb > 512)
+    return fail(PIPNN_EUNSUPPORTED, "dist_topk: row bytes must be a multiple of 32 and <= 512");
+  if (kmax > kTopkMax) return fail(PIPNN_EUNSUPPORTED, "dist_topk: k too large (k+1 <= 16 with self exclusion)");
+  if (u8 && mips) return fail(PIPNN_EINVAL, "uint8 + MIPS unsupported");
+  if (u8) return launch_one<true, false>(a, st);
+  if (mips) return launch_one<false, true>(a, st);
+  return launch_one<false, false>(a, st);
+}
+
+}  // namespace pipnn

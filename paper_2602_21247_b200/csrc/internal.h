@@ -1,0 +1,59 @@
+// internal.h — host-side declarations shared by the libpipnn translation units (not the ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "common.cuh"
+#include "dist_topk.cuh"
+
+namespace pipnn {
+
+struct Ctx {
+  cudaStream_t st;
+  int* err;  // device error flag (DevErr)
+};
+
+// Bytes per row of the tiled (K-major, SWIZZLE_NONE) layout: uint8 -> round_up(d, 32);
+// float -> bf16 with round_up(d, 16) elements (so the row is a multiple of 32 B = one MMA K-step).
+int tiled_row_bytes(const pipnn_points* X);
+pipnn_status validate_points(const pipnn_points* X);
+
+// Gather rows ids[seg.id_off + i] (ids == nullptr: identity) of X into the tiled layout of `T` and their
+// squared norms into `nrm` (int32 for uint8, float for bf16-rounded float), one CTA per (segment,
+// 128-row block) work item; padding rows are zero. max_items bounds the grid.
+pipnn_status gather_tiled(const pipnn_points* X, const uint32_t* ids, const TileSeg* segs, const WorkItem* items,
+                          const int64_t* n_items, int64_t max_items, uint8_t* T, void* nrm, const Ctx& c);
+
+// Build TileSegs/items for CSR segments (off[0..ns]) with pad = round_up(rows, 128): writes segs
+// (DistSeg with a == b, self = 1, out_row = off[s], k) and the (segment, row-block) items.
+pipnn_status csr_dist_segs(const int64_t* off, int64_t ns, int k, int self, DistSeg* segs, WorkItem* items,
+                           int64_t* n_items, Arena& ar, const Ctx& c);
+
+// max_items: capacity in 128-row work items (0 = exact bound for these leaves); with an explicit capacity
+// the caller guarantees sum_b ceil(|b|/128) <= max_items (pipnn_build forms waves of leaves that fit).
+int64_t leaf_items_bound(int64_t n_leaves, int64_t n_inst);
+pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, const uint32_t* leaf_ids, int64_t n_leaves,
+                            int64_t n_inst, int k, uint32_t* nbr, float* dist, Arena& ar, const Ctx& c,
+                            int64_t max_items = 0);
+
+pipnn_status sketch_impl(const pipnn_points* X, int m, uint64_t seed, void* sketch, Arena& ar, const Ctx& c);
+
+pipnn_status hashprune_impl(int m, int l_max, int64_t n, const void* sketch, bool sk_int, uint64_t* slots,
+                            uint32_t* count, const uint32_t* owner, const uint32_t* cand, const float* dist,
+                            int64_t n_edges, Arena& ar, const Ctx& c);
+
+// Fused edge emission for pipnn_build: the bidirected edges of the candidate lists nbr/dist ([I, k])
+// grouped by owner and merged into the reservoirs.
+pipnn_status hashprune_from_lists(int m, int l_max, int64_t n, const void* sketch, bool sk_int, uint64_t* slots,
+                                  uint32_t* count, const uint32_t* leaf_ids, int64_t n_inst, int k,
+                                  const uint32_t* nbr, const float* dist, int64_t* n_edges_dev, Arena& ar,
+                                  const Ctx& c);
+
+pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* slots, const uint32_t* count,
+                              const pipnn_prune_params* p, uint64_t* row_ptr, uint32_t* col_idx, Arena& ar,
+                              const Ctx& c);
+
+pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params* p, int64_t* leaf_off,
+                            int64_t leaf_off_cap, uint32_t* leaf_ids, int64_t leaf_ids_cap, int64_t* n_leaves_h,
+                            int64_t* n_inst_h, int* depth_h, Arena& ar, const Ctx& c);
+
+}  // namespace pipnn

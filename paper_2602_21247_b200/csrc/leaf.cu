@@ -1,0 +1,213 @@
+// leaf.cu — leaf gather into the tiled MMA layout (+ squared norms) and the leaf-pick driver
+// (§4.2: all-pairs distances inside each leaf, then the bidirected k-NN pick).
+#include <algorithm>
+#include <cub/cub.cuh>
+
+#include "internal.h"
+
+namespace pipnn {
+
+int tiled_row_bytes(const pipnn_points* X) {
+  if (X->dtype == PIPNN_U8) return (int)round_up(X->d, 32);
+  return (int)round_up(X->d, 16) * 2 + 32;  // bf16 coordinates + one augmented K-step (dist_topk.cuh)
+}
+
+// ------------------------------------------------------------------ gather
+// One CTA per (segment, 128-row block). Phase 1: warp-per-row coalesced loads of the source rows into a
+// row-major SMEM staging tile (fp32 -> bf16 RNE for float data) + the row's squared norm. Phase 2: the
+// tile is written as [K/16][pad][16 B] planes — each plane slice of the block is 2 KB contiguous.
+// Float rows end with the 16-element augment K-step of dist_topk.cuh: (t_hi, t_mid, t_lo, 0...) with
+// t = -||y||^2/2 (L2) or 0 (MIPS), split over three bf16 values; padding rows get t = -1e30 (u8 padding
+// rows get the norm kPadNormU8 instead), so padded columns never enter a top-k.
+template <bool U8>
+__global__ void __launch_bounds__(256) gather_tiled_kernel(const void* __restrict__ Xv, int64_t ld, int d, int Kb,
+                                                           int mips, const uint32_t* __restrict__ ids,
+                                                           const TileSeg* __restrict__ segs,
+                                                           const WorkItem* __restrict__ items,
+                                                           const int64_t* __restrict__ n_items, uint8_t* __restrict__ T,
+                                                           void* __restrict__ nrm, int* err) {
+  extern __shared__ __align__(16) uint8_t st[];
+  if ((int64_t)blockIdx.x >= *n_items) return;
+  const WorkItem w = items[blockIdx.x];
+  const TileSeg S = segs[w.seg];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pitch = Kb + 16;  // staging row pitch (bank-conflict-free 16-B column reads)
+  const int r0 = w.rb * 128;
+  const int ldm = U8 ? Kb : (Kb - 32) / 2;  // elements of the coordinate part
+  for (int r = warp; r < 128; r += 8) {
+    const int local = r0 + r;
+    uint8_t* srow = st + r * pitch;
+    float nf = 0.0f;
+    int ni = 0;
+    const bool valid = local < S.rows;
+    if (valid) {
+      const int64_t id = ids ? (int64_t)ids[S.id_off + local] : (S.id_off + local);
+      if (U8) {
+        const uint8_t* src = (const uint8_t*)Xv + id * ld;
+        for (int j = lane; j < Kb; j += 32) {
+          const int v = j < d ? src[j] : 0;
+          srow[j] = (uint8_t)v;
+          ni += v * v;
+        }
+      } else {
+        const float* src = (const float*)Xv + id * ld;
+        uint16_t* drow = (uint16_t*)srow;
+        bool bad = false;
+        for (int j = lane; j < ldm; j += 32) {
+          const float x = j < d ? src[j] : 0.0f;
+          bad |= !isfinite(x);
+          const uint16_t b = f32_to_bf16_rne(x);
+          drow[j] = b;
+          const float xb = __uint_as_float((uint32_t)b << 16);
+          nf = fmaf(xb, xb, nf);
+        }
+        if (bad) atomicExch(err, DERR_NONFINITE);
+      }
+    } else {
+      for (int j = lane * 4; j < Kb; j += 128) *(uint32_t*)(srow + j) = 0u;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ni += __shfl_xor_sync(0xffffffffu, ni, o);
+      nf += __shfl_xor_sync(0xffffffffu, nf, o);
+    }
+    if (lane == 0) {
+      if (U8) {
+        ((int32_t*)nrm)[S.pos + local] = valid ? ni : kPadNormU8;
+      } else {
+        ((float*)nrm)[S.pos + local] = nf;
+        const float t = valid ? (mips ? 0.0f : -0.5f * nf) : -kPadKey;
+        const uint16_t hi = f32_to_bf16_rne(t);
+        const float r1 = t - __uint_as_float((uint32_t)hi << 16);
+        const uint16_t mid = f32_to_bf16_rne(r1);
+        const float r2 = r1 - __uint_as_float((uint32_t)mid << 16);
+        const uint16_t lo = f32_to_bf16_rne(r2);
+        uint32_t* aug = (uint32_t*)(srow + 2 * ldm);
+        aug[0] = (uint32_t)hi | ((uint32_t)mid << 16);
+        aug[1] = (uint32_t)lo;
+        aug[2] = aug[3] = aug[4] = aug[5] = aug[6] = aug[7] = 0u;
+      }
+    }
+  }
+  __syncthreads();
+  const int KC = Kb >> 4;
+  uint8_t* dst = T + S.pos * (int64_t)Kb;
+  for (int p = threadIdx.x; p < 128 * KC; p += 256) {
+    const int kc = p >> 7, r = p & 127;
+    const uint4 v = *(const uint4*)(st + r * pitch + kc * 16);
+    *(uint4*)(dst + ((int64_t)kc * S.pad + r0 + r) * 16) = v;
+  }
+}
+
+pipnn_status gather_tiled(const pipnn_points* X, const uint32_t* ids, const TileSeg* segs, const WorkItem* items,
+                          const int64_t* n_items, int64_t max_items, uint8_t* T, void* nrm, const Ctx& c) {
+  if (max_items <= 0) return PIPNN_OK;
+  const int Kb = tiled_row_bytes(X);
+  const int smem = 128 * (Kb + 16);
+  const int64_t ld = X->ld;
+  if (X->dtype == PIPNN_U8) {
+    PIPNN_CUDA(cudaFuncSetAttribute(gather_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    gather_tiled_kernel<true><<<(unsigned)max_items, 256, smem, c.st>>>(X->data, ld, X->d, Kb, 0, ids, segs, items,
+                                                                         n_items, T, nrm, c.err);
+  } else {
+    PIPNN_CUDA(cudaFuncSetAttribute(gather_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    gather_tiled_kernel<false><<<(unsigned)max_items, 256, smem, c.st>>>(X->data, ld, X->d, Kb,
+                                                                          X->metric == PIPNN_MIPS, ids, segs, items,
+                                                                          n_items, T, nrm, c.err);
+  }
+  PIPNN_LAUNCHED("gather_tiled_kernel", c.st);
+  return PIPNN_OK;
+}
+
+// ------------------------------------------------------------------ CSR segments -> DistSegs + items
+__global__ void csr_pad_kernel(const int64_t* __restrict__ off, int64_t ns, int64_t* __restrict__ blocks) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s < ns) blocks[s] = (off[s + 1] - off[s] + 127) / 128;
+}
+
+__global__ void csr_fill_kernel(const int64_t* __restrict__ off, int64_t ns, const int64_t* __restrict__ blocks,
+                                const int64_t* __restrict__ bpos, int k, int self, DistSeg* __restrict__ segs,
+                                WorkItem* __restrict__ items, int64_t* __restrict__ n_items) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= ns) return;
+  const int64_t nb = blocks[s], p = bpos[s];
+  TileSeg t;
+  t.id_off = off[s];
+  t.pos = p * 128;
+  t.pad = (int32_t)(nb * 128);
+  t.rows = (int32_t)(off[s + 1] - off[s]);
+  DistSeg d;
+  d.a = t;
+  d.b = t;
+  d.out_off = off[s] * k;
+  d.k = k;
+  d.self = self;
+  d.ostride = k;
+  d.pad_ = 0;
+  segs[s] = d;
+  for (int64_t rb = 0; rb < nb; ++rb) items[p + rb] = WorkItem{(int32_t)s, (int32_t)rb};
+  if (s == ns - 1) *n_items = p + nb;
+}
+
+pipnn_status csr_dist_segs(const int64_t* off, int64_t ns, int k, int self, DistSeg* segs, WorkItem* items,
+                           int64_t* n_items, Arena& ar, const Ctx& c) {
+  int64_t* blocks = ar.take<int64_t>(ns);
+  int64_t* bpos = ar.take<int64_t>(ns);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, blocks, bpos, (int)ns, c.st);
+  void* tmpbuf = ar.take<uint8_t>(tmp);
+  if (ar.measuring()) return PIPNN_OK;
+  if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (csr_dist_segs)");
+  if (ns == 0) {
+    PIPNN_CUDA(cudaMemsetAsync(n_items, 0, sizeof(int64_t), c.st));
+    return PIPNN_OK;
+  }
+  const int tb = 256;
+  csr_pad_kernel<<<(unsigned)ceil_div(ns, tb), tb, 0, c.st>>>(off, ns, blocks);
+  PIPNN_LAUNCHED("csr_pad_kernel", c.st);
+  PIPNN_CUDA(cub::DeviceScan::ExclusiveSum(tmpbuf, tmp, blocks, bpos, (int)ns, c.st));
+  csr_fill_kernel<<<(unsigned)ceil_div(ns, tb), tb, 0, c.st>>>(off, ns, blocks, bpos, k, self, segs, items, n_items);
+  PIPNN_LAUNCHED("csr_fill_kernel", c.st);
+  return PIPNN_OK;
+}
+
+// ------------------------------------------------------------------ leaf pick
+int64_t leaf_items_bound(int64_t n_leaves, int64_t n_inst) { return n_inst / 128 + n_leaves + 1; }
+
+pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, const uint32_t* leaf_ids, int64_t n_leaves,
+                            int64_t n_inst, int k, uint32_t* nbr, float* dist, Arena& ar, const Ctx& c,
+                            int64_t max_items) {
+  const int Kb = tiled_row_bytes(X);
+  if (max_items <= 0) max_items = leaf_items_bound(n_leaves, n_inst);
+  const int64_t seg_cap = std::min<int64_t>(n_leaves, max_items);
+  const int64_t max_rows = max_items * 128;
+  uint8_t* T = ar.take<uint8_t>((size_t)max_rows * Kb);
+  void* nrm = ar.take<int32_t>(max_rows);
+  DistSeg* segs = ar.take<DistSeg>(seg_cap);
+  WorkItem* items = ar.take<WorkItem>(max_items);
+  int64_t* n_items = ar.take<int64_t>(1);
+  TileSeg* tsegs = ar.take<TileSeg>(seg_cap);  // compact TileSeg view (seg.a) for the gather kernel
+  PIPNN_TRY(csr_dist_segs(leaf_off, seg_cap, k, 1, segs, items, n_items, ar, c));
+  if (ar.measuring()) return PIPNN_OK;
+  if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (leaf_pick)");
+  if (n_leaves == 0 || n_inst == 0) return PIPNN_OK;
+  PIPNN_CUDA(cudaMemcpy2DAsync(tsegs, sizeof(TileSeg), segs, sizeof(DistSeg), sizeof(TileSeg), (size_t)n_leaves,
+                               cudaMemcpyDeviceToDevice, c.st));
+  PIPNN_TRY(gather_tiled(X, leaf_ids, tsegs, items, n_items, max_items, T, nrm, c));
+  DistTopkArgs a{};
+  a.Ta = T;
+  a.Tb = T;
+  a.na = nrm;
+  a.nb = nrm;
+  a.Kb = Kb;
+  a.segs = segs;
+  a.items = items;
+  a.n_items = n_items;
+  a.col_ids = leaf_ids;
+  a.out_idx = nbr;
+  a.out_dist = dist;
+  a.err = c.err;
+  return launch_dist_topk(a, X->dtype == PIPNN_U8, X->metric == PIPNN_MIPS, k + 1, c.st);
+}
+
+}  // namespace pipnn

@@ -1,0 +1,599 @@
+// partition.cu — Randomized Ball Carving with fanout and merging (§4.1, Alg. 5) as a
+// level-synchronous GPU loop. The recursion of Alg. 5 is breadth-first here: all open subproblems of one
+// depth are processed together, which is equivalent because every subproblem is carved independently
+// from its own key (docs/DETERMINISM.md). Per level:
+//   1. leaders: the l_g members with the smallest mix(K_g, id) (line 2, "SampleLeaders"): a threshold
+//      filter (count pass + scatter pass) keeps ~4 l_g + 64 candidates per subproblem, a segmented sort
+//      orders them, the first l_g are sorted by id. mix(K, .) is injective, so the selection is exact;
+//      a subproblem whose filter kept fewer than l_g candidates is redone with no filter.
+//   2. nearest leaders (lines 5-9): members and leaders are gathered into the tiled MMA layout and the
+//      dist_topk kernel (tcgen05, the same kernel as the leaf pick) returns each member's f_g nearest
+//      leaders by (D, leader id) — leaders are in ascending id order, so "smaller column" = "smaller id".
+//   3. group-by: (child, id) pairs in member order, stable radix sort by child -> every child ascending.
+//   4. one device->host copy of the child sizes and leader ids; the host applies the merge rule of small
+//      siblings (line 10, R15), the base case, the degenerate-input guard, and schedules
+//      (a) leaf jobs (plain copies, or sorted + deduplicated unions for merged groups) and
+//      (b) the next level's subproblems (children larger than C_max, key mix(K_g, l + 1)).
+// At the end, leaf sizes -> exclusive scan -> leaf_off, and the staged leaves are compacted into leaf_ids.
+#include <algorithm>
+#include <cub/cub.cuh>
+#include <vector>
+
+#include "internal.h"
+
+namespace pipnn {
+
+struct PGroup {       // device view of an open subproblem at the current level
+  uint64_t key;       // K_g
+  uint64_t thr;       // leader-priority filter threshold
+  int64_t off;        // members: mem[off .. off+size)
+  int64_t cbase;      // compacted member index of its first member
+  int64_t size;
+  int64_t cand_off;   // candidate buffer offset
+  int64_t lead_off;   // leader buffer offset (= child base)
+  int64_t pair_off;   // (member, slot) pair offset
+  int32_t l, f;
+};
+
+struct LeafPart {
+  int64_t src;  // offset into the level's child-id buffer
+  int32_t len;
+  int32_t pad_;
+};
+struct LeafJob {
+  int64_t dst;      // staging offset
+  int64_t leaf;     // leaf index
+  int32_t part0, nparts;
+};
+
+// ------------------------------------------------------------------ kernels
+__global__ void iota_reps_kernel(uint32_t* __restrict__ out, int64_t n, int reps) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * reps; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = (uint32_t)(e % n);
+}
+
+__device__ __forceinline__ int find_group(const int64_t* __restrict__ cbase, int G, int64_t e) {
+  int lo = 0, hi = G - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (cbase[mid] <= e) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <bool kScatter>
+__global__ void prio_kernel(const PGroup* __restrict__ gs, const int64_t* __restrict__ cbase, int G, int64_t M,
+                            const uint32_t* __restrict__ mem, uint32_t* __restrict__ cnt, uint64_t* __restrict__ ck,
+                            uint32_t* __restrict__ cv) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M; e += (int64_t)gridDim.x * blockDim.x) {
+    const int g = find_group(cbase, G, e);
+    const PGroup& p = gs[g];
+    const uint32_t id = mem[p.off + (e - p.cbase)];
+    const uint64_t pri = mix64(p.key, id);
+    if (pri < p.thr || p.thr == ~0ull) {
+      const uint32_t slot = atomicAdd(&cnt[g], 1u);
+      if (kScatter) {
+        ck[p.cand_off + slot] = pri;
+        cv[p.cand_off + slot] = id;
+      }
+    }
+  }
+}
+
+// first l_g sorted candidates -> leaders (then sorted by id with a segmented sort)
+__global__ void take_leaders_kernel(const PGroup* __restrict__ gs, int G, const uint32_t* __restrict__ cv_sorted,
+                                    uint32_t* __restrict__ lead) {
+  const int g = blockIdx.x;
+  if (g >= G) return;
+  const PGroup& p = gs[g];
+  for (int j = threadIdx.x; j < p.l; j += blockDim.x) lead[p.lead_off + j] = cv_sorted[p.cand_off + j];
+}
+
+// (child, id) pairs in member order from the assignment; child sizes by atomics
+__global__ void pairs_kernel(const PGroup* __restrict__ gs, const int64_t* __restrict__ cbase, int G, int64_t M,
+                             const uint32_t* __restrict__ mem, const uint32_t* __restrict__ assign,
+                             uint32_t* __restrict__ pk, uint32_t* __restrict__ pv, uint32_t* __restrict__ ccnt,
+                             int* err) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M; e += (int64_t)gridDim.x * blockDim.x) {
+    const int g = find_group(cbase, G, e);
+    const PGroup& p = gs[g];
+    const int64_t r = e - p.cbase;
+    const uint32_t id = mem[p.off + r];
+    for (int t = 0; t < p.f; ++t) {
+      const int64_t q = p.pair_off + r * p.f + t;
+      const uint32_t j = assign[q];
+      if (j >= (uint32_t)p.l) {  // cannot happen: every member has >= f leaders
+        atomicExch(err, DERR_CAPACITY);
+        continue;
+      }
+      const uint32_t child = (uint32_t)p.lead_off + j;
+      pk[q] = child;
+      pv[q] = id;
+      atomicAdd(&ccnt[child], 1u);
+    }
+  }
+}
+
+// One CTA per leaf job: a plain copy, or the sorted, deduplicated union of several sibling groups.
+__global__ void __launch_bounds__(256) leaf_job_kernel(const LeafJob* __restrict__ jobs, int nj,
+                                                       const LeafPart* __restrict__ parts,
+                                                       const uint32_t* __restrict__ src, uint32_t* __restrict__ staging,
+                                                       int64_t* __restrict__ leaf_size) {
+  __shared__ uint32_t a[4096];
+  __shared__ int total_sh;
+  const int j = blockIdx.x;
+  if (j >= nj) return;
+  const LeafJob J = jobs[j];
+  if (J.nparts == 1) {
+    const LeafPart P = parts[J.part0];
+    for (int i = threadIdx.x; i < P.len; i += blockDim.x) staging[J.dst + i] = src[P.src + i];
+    if (threadIdx.x == 0) leaf_size[J.leaf] = P.len;
+    return;
+  }
+  int total = 0;
+  for (int q = 0; q < J.nparts; ++q) {
+    const LeafPart P = parts[J.part0 + q];
+    for (int i = threadIdx.x; i < P.len; i += blockDim.x) a[total + i] = src[P.src + i];
+    total += P.len;
+  }
+  int Pn = 32;
+  while (Pn < total) Pn <<= 1;
+  for (int i = total + threadIdx.x; i < Pn; i += blockDim.x) a[i] = 0xFFFFFFFFu;
+  __syncthreads();
+  for (int k = 2; k <= Pn; k <<= 1)
+    for (int s = k >> 1; s > 0; s >>= 1) {
+      for (int i = threadIdx.x; i < Pn; i += blockDim.x) {
+        const int ixj = i ^ s;
+        if (ixj > i) {
+          const uint32_t x = a[i], y = a[ixj];
+          if ((x > y) == ((i & k) == 0)) {
+            a[i] = y;
+            a[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  if (threadIdx.x < 32) {  // warp 0: ordered compaction of first occurrences
+    const int lane = threadIdx.x;
+    int base = 0;
+    for (int i0 = 0; i0 < total; i0 += 32) {
+      const int i = i0 + lane;
+      const bool keep = i < total && (i == 0 || a[i] != a[i - 1]);
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) staging[J.dst + base + __popc(bal & ((1u << lane) - 1u))] = a[i];
+      base += __popc(bal);
+    }
+    if (lane == 0) total_sh = base;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) leaf_size[J.leaf] = total_sh;
+}
+
+__global__ void leaf_compact_kernel(int64_t nl, const int64_t* __restrict__ leaf_dst, const int64_t* __restrict__ off,
+                                    const uint32_t* __restrict__ staging, uint32_t* __restrict__ out) {
+  for (int64_t b = blockIdx.x; b < nl; b += gridDim.x) {
+    const int64_t s = off[b], len = off[b + 1] - s, d = leaf_dst[b];
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) out[s + i] = staging[d + i];
+  }
+}
+
+// ------------------------------------------------------------------ host helpers
+static int64_t leaders_of(int64_t sz, const pipnn_partition_params* p) {
+  int64_t l = ((int64_t)p->p_samp_num * sz + p->p_samp_den - 1) / p->p_samp_den;
+  l = std::max<int64_t>(l, 2);
+  l = std::min<int64_t>(l, p->leader_cap);
+  return std::min<int64_t>(l, sz);
+}
+
+static int64_t prod_fan(const pipnn_partition_params* p) {
+  int64_t f = 1;
+  for (int i = 0; i < p->n_fanout; ++i) f *= p->fanout[i];
+  return f * p->replicas;
+}
+
+struct HGroup {  // host view of an open subproblem
+  int64_t off, size;
+  uint64_t key;
+};
+
+// Merge plan of one parent's children (R15) — same rule as the oracle, re-implemented.
+struct HMerge {
+  std::vector<int> big;
+  std::vector<std::vector<int>> bins;
+  std::vector<int> leftover;
+  int absorb = -1;
+};
+static HMerge merge_plan(const std::vector<int64_t>& sz, const std::vector<std::pair<uint64_t, uint32_t>>& key,
+                         int64_t c_min, int64_t c_max) {
+  HMerge m;
+  std::vector<int> small;
+  for (int j = 0; j < (int)sz.size(); ++j) {
+    if (sz[j] == 0) continue;
+    if (sz[j] < c_min) small.push_back(j);
+    else m.big.push_back(j);
+  }
+  std::sort(small.begin(), small.end(), [&](int a, int b) { return key[a] < key[b]; });
+  std::vector<int> cur;
+  int64_t sum = 0;
+  for (int j : small) {
+    cur.push_back(j);
+    sum += sz[j];
+    if (sum >= c_min) {
+      m.bins.push_back(cur);
+      cur.clear();
+      sum = 0;
+    }
+  }
+  if (!cur.empty()) {
+    if (!m.bins.empty()) {
+      m.bins[0].insert(m.bins[0].end(), cur.begin(), cur.end());
+    } else {
+      for (int j : m.big) {
+        if (sz[j] + sum > c_max) continue;
+        if (m.absorb < 0 || sz[j] < sz[m.absorb] || (sz[j] == sz[m.absorb] && key[j] < key[m.absorb])) m.absorb = j;
+      }
+      if (m.absorb < 0) m.bins.push_back(cur);
+      else m.leftover = cur;
+    }
+  }
+  return m;
+}
+
+struct PartCaps {
+  int64_t L;        // instances bound n * prod(fanout) * replicas
+  int64_t G;        // open groups per level
+  int64_t C;        // children (leaders) per level
+  int64_t J;        // leaf jobs / parts per level
+  int64_t rowsA;    // tiled member rows
+  int64_t rowsB;    // tiled leader rows
+  int64_t leaves;   // total leaves
+};
+static PartCaps caps_of(const pipnn_points* X, const pipnn_partition_params* p) {
+  PartCaps c;
+  c.L = X->n * prod_fan(p);
+  c.G = c.L / (p->c_max + 1) + p->replicas + 1;
+  c.C = c.L * p->p_samp_num / p->p_samp_den + 2 * c.G + 16;
+  c.C = std::min<int64_t>(c.C, c.G * p->leader_cap + 16);
+  c.J = c.C + 2 * c.L / std::max(1, p->c_max) + c.G + 16;
+  c.rowsA = c.L + 128 * c.G;
+  c.rowsB = c.C + 128 * c.G;
+  c.leaves = c.L + 1;
+  return c;
+}
+
+static int bits_for(int64_t v) {
+  int b = 1;
+  while (((int64_t)1 << b) <= v) ++b;
+  return b;
+}
+
+pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params* p, int64_t* leaf_off,
+                            int64_t leaf_off_cap, uint32_t* leaf_ids, int64_t leaf_ids_cap, int64_t* n_leaves_h,
+                            int64_t* n_inst_h, int* depth_h, Arena& ar, const Ctx& c) {
+  const PartCaps cp = caps_of(X, p);
+  const int Kb = tiled_row_bytes(X);
+  int fmax = 1;
+  for (int i = 0; i < p->n_fanout; ++i) fmax = std::max(fmax, p->fanout[i]);
+  // ---- workspace
+  uint32_t* memA = ar.take<uint32_t>(cp.L);
+  uint32_t* memB = ar.take<uint32_t>(cp.L);
+  uint32_t* staging = ar.take<uint32_t>(cp.L);
+  int64_t* leaf_size = ar.take<int64_t>(cp.leaves + 1);
+  int64_t* leaf_dst = ar.take<int64_t>(cp.leaves);
+  PGroup* d_groups = ar.take<PGroup>(cp.G);
+  int64_t* d_cbase = ar.take<int64_t>(cp.G);
+  uint32_t* d_cnt = ar.take<uint32_t>(cp.G);
+  int64_t* d_cand_seg = ar.take<int64_t>(cp.G + 1);
+  int64_t* d_lead_seg = ar.take<int64_t>(cp.G + 1);
+  uint64_t* ck = ar.take<uint64_t>(cp.L);
+  uint32_t* cv = ar.take<uint32_t>(cp.L);
+  uint64_t* ck2 = ar.take<uint64_t>(cp.L);
+  uint32_t* cv2 = ar.take<uint32_t>(cp.L);
+  uint32_t* lead = ar.take<uint32_t>(cp.C);
+  uint32_t* lead_sorted = ar.take<uint32_t>(cp.C);
+  uint32_t* ccnt = ar.take<uint32_t>(cp.C);
+  uint8_t* TA = ar.take<uint8_t>((size_t)cp.rowsA * Kb);
+  int32_t* nA = ar.take<int32_t>(cp.rowsA);
+  uint8_t* TB = ar.take<uint8_t>((size_t)cp.rowsB * Kb);
+  int32_t* nB = ar.take<int32_t>(cp.rowsB);
+  TileSeg* tsA = ar.take<TileSeg>(cp.G);
+  TileSeg* tsB = ar.take<TileSeg>(cp.G);
+  DistSeg* dsegs = ar.take<DistSeg>(cp.G);
+  WorkItem* itA = ar.take<WorkItem>(cp.rowsA / 128 + 1);
+  WorkItem* itB = ar.take<WorkItem>(cp.rowsB / 128 + 1);
+  int64_t* n_it = ar.take<int64_t>(2);
+  uint32_t* assign = ar.take<uint32_t>(cp.L);
+  uint32_t* pk = ar.take<uint32_t>(cp.L);
+  uint32_t* pk2 = ar.take<uint32_t>(cp.L);
+  LeafJob* d_jobs = ar.take<LeafJob>(cp.J);
+  LeafPart* d_parts = ar.take<LeafPart>(cp.J);
+  size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+  cub::DeviceSegmentedSort::SortPairs(nullptr, t1, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                      (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)std::min<int64_t>(cp.L, INT32_MAX),
+                                      (int)cp.G, (const int64_t*)nullptr, (const int64_t*)nullptr);
+  cub::DeviceSegmentedSort::SortKeys(nullptr, t2, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)cp.C, (int)cp.G,
+                                     (const int64_t*)nullptr, (const int64_t*)nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, t3, (const uint32_t*)nullptr, (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (int)std::min<int64_t>(cp.L, INT32_MAX));
+  cub::DeviceScan::ExclusiveSum(nullptr, t4, (const int64_t*)nullptr, (int64_t*)nullptr, (int)cp.leaves);
+  void* cub_tmp = ar.take<uint8_t>(std::max(std::max(t1, t2), std::max(t3, t4)));
+  const size_t cub_bytes = std::max(std::max(t1, t2), std::max(t3, t4));
+  if (ar.measuring()) return PIPNN_OK;
+  if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (partition)");
+  if (leaf_ids_cap < cp.L || leaf_off_cap < cp.L + 1) return fail(PIPNN_ECAPACITY, "leaf capacities too small");
+
+  const int64_t n = X->n;
+  const int reps = p->replicas;
+  const cudaStream_t st = c.st;
+  // level 0: one subproblem per replica, members 0..n-1 each
+  iota_reps_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n * reps, 256), num_sms() * 64), 256, 0, st>>>(memA, n, reps);
+  PIPNN_LAUNCHED("iota_reps_kernel", st);
+  std::vector<HGroup> open;
+  uint32_t* mem = memA;
+  uint32_t* nxt = memB;
+  int64_t n_leaves = 0, staged = 0;
+  int depth = 0;
+  std::vector<LeafJob> jobs;
+  std::vector<LeafPart> parts;
+
+  auto flush_jobs = [&](const uint32_t* src) -> pipnn_status {
+    if (jobs.empty()) return PIPNN_OK;
+    if ((int64_t)jobs.size() > cp.J || (int64_t)parts.size() > cp.J) return fail(PIPNN_ECAPACITY, "partition: job capacity");
+    PIPNN_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(LeafJob), cudaMemcpyHostToDevice, st));
+    PIPNN_CUDA(cudaMemcpyAsync(d_parts, parts.data(), parts.size() * sizeof(LeafPart), cudaMemcpyHostToDevice, st));
+    leaf_job_kernel<<<(unsigned)jobs.size(), 256, 0, st>>>(d_jobs, (int)jobs.size(), d_parts, src, staging, leaf_size);
+    PIPNN_LAUNCHED("leaf_job_kernel", st);
+    // jobs/parts host vectors must stay valid until the copies complete
+    PIPNN_CUDA(cudaStreamSynchronize(st));
+    jobs.clear();
+    parts.clear();
+    return PIPNN_OK;
+  };
+  std::vector<int64_t> h_leaf_dst;
+  auto add_leaf = [&](std::initializer_list<LeafPart> ps, int64_t upper) {
+    LeafJob J;
+    J.dst = staged;
+    J.leaf = n_leaves;
+    J.part0 = (int32_t)parts.size();
+    J.nparts = (int32_t)ps.size();
+    for (const LeafPart& q : ps) parts.push_back(q);
+    jobs.push_back(J);
+    h_leaf_dst.push_back(staged);
+    staged += upper;
+    ++n_leaves;
+  };
+
+  for (int r = 0; r < reps; ++r) {
+    if (n <= p->c_max) add_leaf({LeafPart{(int64_t)r * n, (int32_t)n, 0}}, n);  // line 1: base case
+    else open.push_back(HGroup{(int64_t)r * n, n, mix64(mix64(p->seed, kDomPart), (uint64_t)r)});
+  }
+  PIPNN_TRY(flush_jobs(memA));
+
+  while (!open.empty()) {
+    const int G = (int)open.size();
+    if (G > cp.G) return fail(PIPNN_ECAPACITY, "partition: open-group capacity");
+    // ---- host plan of the level
+    std::vector<PGroup> hg(G);
+    std::vector<int64_t> cb(G);
+    int64_t M = 0, C = 0, Q = 0;
+    int fmax_l = 1;
+    for (int g = 0; g < G; ++g) {
+      PGroup& q = hg[g];
+      q.key = open[g].key;
+      q.off = open[g].off;
+      q.size = open[g].size;
+      q.cbase = M;
+      cb[g] = M;
+      q.l = (int32_t)leaders_of(q.size, p);
+      const int fan = depth < p->n_fanout ? p->fanout[depth] : 1;
+      q.f = std::min(fan, q.l);
+      fmax_l = std::max(fmax_l, q.f);
+      q.lead_off = C;
+      q.pair_off = Q;
+      // filter threshold: expected 4 l + 64 candidates; no filter when that is most of the group
+      const double want = 4.0 * q.l + 64.0;
+      if (want >= 0.5 * (double)q.size) q.thr = ~0ull;
+      else q.thr = (uint64_t)(want / (double)q.size * 18446744073709551615.0);
+      M += q.size;
+      C += q.l;
+      Q += q.size * q.f;
+    }
+    if (C > cp.C || Q > cp.L || M > cp.L) return fail(PIPNN_ECAPACITY, "partition: level capacity");
+    (void)fmax;
+    // ---- 1. leaders
+    std::vector<uint32_t> hcnt(G);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      PIPNN_CUDA(cudaMemcpyAsync(d_groups, hg.data(), G * sizeof(PGroup), cudaMemcpyHostToDevice, st));
+      PIPNN_CUDA(cudaMemcpyAsync(d_cbase, cb.data(), G * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+      PIPNN_CUDA(cudaMemsetAsync(d_cnt, 0, G * sizeof(uint32_t), st));
+      prio_kernel<false><<<(unsigned)std::min<int64_t>(ceil_div(M, 256), num_sms() * 64), 256, 0, st>>>(
+          d_groups, d_cbase, G, M, mem, d_cnt, nullptr, nullptr);
+      PIPNN_LAUNCHED("prio_kernel(count)", st);
+      PIPNN_CUDA(cudaMemcpyAsync(hcnt.data(), d_cnt, G * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+      PIPNN_CUDA(cudaStreamSynchronize(st));
+      bool redo = false;
+      for (int g = 0; g < G; ++g)
+        if ((int64_t)hcnt[g] < hg[g].l) {
+          hg[g].thr = ~0ull;  // exceedingly rare: keep every member as a candidate
+          redo = true;
+        }
+      if (!redo) break;
+    }
+    std::vector<int64_t> cand_seg(G + 1, 0), lead_seg(G + 1, 0);
+    for (int g = 0; g < G; ++g) {
+      hg[g].cand_off = cand_seg[g];
+      cand_seg[g + 1] = cand_seg[g] + hcnt[g];
+      lead_seg[g + 1] = lead_seg[g] + hg[g].l;
+    }
+    const int64_t NC = cand_seg[G];
+    PIPNN_CUDA(cudaMemcpyAsync(d_groups, hg.data(), G * sizeof(PGroup), cudaMemcpyHostToDevice, st));
+    PIPNN_CUDA(cudaMemcpyAsync(d_cand_seg, cand_seg.data(), (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    PIPNN_CUDA(cudaMemcpyAsync(d_lead_seg, lead_seg.data(), (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    PIPNN_CUDA(cudaMemsetAsync(d_cnt, 0, G * sizeof(uint32_t), st));
+    prio_kernel<true><<<(unsigned)std::min<int64_t>(ceil_div(M, 256), num_sms() * 64), 256, 0, st>>>(
+        d_groups, d_cbase, G, M, mem, d_cnt, ck, cv);
+    PIPNN_LAUNCHED("prio_kernel(scatter)", st);
+    size_t tb = cub_bytes;
+    PIPNN_CUDA(cub::DeviceSegmentedSort::SortPairs(cub_tmp, tb, ck, ck2, cv, cv2, (int)NC, G, d_cand_seg,
+                                                   d_cand_seg + 1, st));
+    take_leaders_kernel<<<G, 128, 0, st>>>(d_groups, G, cv2, lead);
+    PIPNN_LAUNCHED("take_leaders_kernel", st);
+    tb = cub_bytes;
+    PIPNN_CUDA(cub::DeviceSegmentedSort::SortKeys(cub_tmp, tb, lead, lead_sorted, (int)C, G, d_lead_seg,
+                                                  d_lead_seg + 1, st));
+    // ---- 2. nearest f_g leaders of every member (tcgen05 distance tiles + top-f)
+    std::vector<TileSeg> hA(G), hB(G);
+    std::vector<DistSeg> hD(G);
+    std::vector<WorkItem> hItA, hItB;
+    int64_t posA = 0, posB = 0;
+    for (int g = 0; g < G; ++g) {
+      const PGroup& q = hg[g];
+      TileSeg a{q.off, posA, (int32_t)round_up(q.size, 128), (int32_t)q.size};
+      TileSeg b{q.lead_off, posB, (int32_t)round_up(q.l, 128), q.l};
+      for (int32_t rb = 0; rb < a.pad / 128; ++rb) hItA.push_back(WorkItem{g, rb});
+      for (int32_t rb = 0; rb < b.pad / 128; ++rb) hItB.push_back(WorkItem{g, rb});
+      posA += a.pad;
+      posB += b.pad;
+      hA[g] = a;
+      hB[g] = b;
+      DistSeg d;
+      d.a = a;
+      d.b = b;
+      d.out_off = q.pair_off;
+      d.k = q.f;
+      d.self = 0;
+      d.ostride = q.f;
+      d.pad_ = 0;
+      hD[g] = d;
+    }
+    if (posA > cp.rowsA || posB > cp.rowsB) return fail(PIPNN_ECAPACITY, "partition: tiled capacity");
+    const int64_t nItA = (int64_t)hItA.size(), nItB = (int64_t)hItB.size();
+    const int64_t nits[2] = {nItA, nItB};
+    PIPNN_CUDA(cudaMemcpyAsync(tsA, hA.data(), G * sizeof(TileSeg), cudaMemcpyHostToDevice, st));
+    PIPNN_CUDA(cudaMemcpyAsync(tsB, hB.data(), G * sizeof(TileSeg), cudaMemcpyHostToDevice, st));
+    PIPNN_CUDA(cudaMemcpyAsync(dsegs, hD.data(), G * sizeof(DistSeg), cudaMemcpyHostToDevice, st));
+    PIPNN_CUDA(cudaMemcpyAsync(itA, hItA.data(), nItA * sizeof(WorkItem), cudaMemcpyHostToDevice, st));
+    PIPNN_CUDA(cudaMemcpyAsync(itB, hItB.data(), nItB * sizeof(WorkItem), cudaMemcpyHostToDevice, st));
+    PIPNN_CUDA(cudaMemcpyAsync(n_it, nits, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    PIPNN_TRY(gather_tiled(X, mem, tsA, itA, n_it, nItA, TA, nA, c));
+    PIPNN_TRY(gather_tiled(X, lead_sorted, tsB, itB, n_it + 1, nItB, TB, nB, c));
+    DistTopkArgs da{};
+    da.Ta = TA;
+    da.Tb = TB;
+    da.na = nA;
+    da.nb = nB;
+    da.Kb = Kb;
+    da.segs = dsegs;
+    da.items = itA;
+    da.n_items = n_it;
+    da.col_ids = nullptr;
+    da.out_idx = assign;
+    da.out_dist = nullptr;
+    da.err = c.err;
+    PIPNN_TRY(launch_dist_topk(da, X->dtype == PIPNN_U8, X->metric == PIPNN_MIPS, fmax_l, st));
+    // ---- 3. group-by (stable radix sort of (child, id) pairs in member order)
+    PIPNN_CUDA(cudaMemsetAsync(ccnt, 0, C * sizeof(uint32_t), st));
+    pairs_kernel<<<(unsigned)std::min<int64_t>(ceil_div(M, 256), num_sms() * 64), 256, 0, st>>>(
+        d_groups, d_cbase, G, M, mem, assign, pk, cv2 /*ids*/, ccnt, c.err);
+    PIPNN_LAUNCHED("pairs_kernel", st);
+    tb = cub_bytes;
+    PIPNN_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, pk, pk2, cv2, nxt, (int)Q, 0, bits_for(C), st));
+    // ---- 4. host merge plan
+    std::vector<uint32_t> hccnt(C), hlead(C);
+    PIPNN_CUDA(cudaMemcpyAsync(hccnt.data(), ccnt, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    PIPNN_CUDA(cudaMemcpyAsync(hlead.data(), lead_sorted, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    PIPNN_CUDA(cudaStreamSynchronize(st));
+    std::vector<int64_t> coff(C + 1, 0);
+    for (int64_t j = 0; j < C; ++j) coff[j + 1] = coff[j] + hccnt[j];
+    std::vector<HGroup> next;
+    for (int g = 0; g < G; ++g) {
+      const PGroup& q = hg[g];
+      const int l = q.l;
+      std::vector<int64_t> sz(l);
+      std::vector<std::pair<uint64_t, uint32_t>> mk(l);
+      const uint64_t KM = q.key ^ kDomMerge;
+      for (int j = 0; j < l; ++j) {
+        sz[j] = hccnt[q.lead_off + j];
+        const uint32_t lid = hlead[q.lead_off + j];
+        mk[j] = {mix64(KM, lid), lid};
+      }
+      HMerge mp = merge_plan(sz, mk, p->c_min, p->c_max);
+      auto part_of = [&](int j) { return LeafPart{coff[q.lead_off + j], (int32_t)sz[j], 0}; };
+      for (int j : mp.big) {
+        if (j == mp.absorb) {
+          int64_t upper = sz[j];
+          LeafJob J;
+          J.dst = staged;
+          J.leaf = n_leaves;
+          J.part0 = (int32_t)parts.size();
+          J.nparts = 1 + (int32_t)mp.leftover.size();
+          parts.push_back(part_of(j));
+          for (int s : mp.leftover) {
+            parts.push_back(part_of(s));
+            upper += sz[s];
+          }
+          jobs.push_back(J);
+          h_leaf_dst.push_back(staged);
+          staged += upper;
+          ++n_leaves;
+          continue;
+        }
+        if (sz[j] <= p->c_max) {
+          add_leaf({part_of(j)}, sz[j]);
+        } else if (sz[j] == q.size || depth + 1 >= 64) {
+          // degenerate-input guard: ceil(|g|/C_max) near-equal chunks by ascending id
+          const int64_t nc = ceil_div(sz[j], p->c_max);
+          for (int64_t t = 0; t < nc; ++t) {
+            const int64_t lo = t * sz[j] / nc, hi = (t + 1) * sz[j] / nc;
+            add_leaf({LeafPart{coff[q.lead_off + j] + lo, (int32_t)(hi - lo), 0}}, hi - lo);
+          }
+        } else {
+          next.push_back(HGroup{coff[q.lead_off + j], sz[j], mix64(q.key, (uint64_t)hlead[q.lead_off + j] + 1)});
+        }
+      }
+      for (auto& bin : mp.bins) {
+        LeafJob J;
+        J.dst = staged;
+        J.leaf = n_leaves;
+        J.part0 = (int32_t)parts.size();
+        J.nparts = (int32_t)bin.size();
+        int64_t upper = 0;
+        for (int s : bin) {
+          parts.push_back(part_of(s));
+          upper += sz[s];
+        }
+        jobs.push_back(J);
+        h_leaf_dst.push_back(staged);
+        staged += upper;
+        ++n_leaves;
+      }
+    }
+    if (staged > cp.L || n_leaves > cp.leaves - 1) return fail(PIPNN_ECAPACITY, "partition: leaf capacity");
+    PIPNN_TRY(flush_jobs(nxt));
+    // next level: subproblems live in `nxt`; ping-pong the member buffers
+    open.swap(next);
+    std::swap(mem, nxt);
+    ++depth;
+  }
+  // ---- leaf_off = exclusive scan of the leaf sizes; compact the staged leaves into leaf_ids
+  PIPNN_CUDA(cudaMemsetAsync(leaf_size + n_leaves, 0, sizeof(int64_t), st));
+  size_t tb = cub_bytes;
+  PIPNN_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, leaf_size, leaf_off, (int)(n_leaves + 1), st));
+  PIPNN_CUDA(cudaMemcpyAsync(leaf_dst, h_leaf_dst.data(), n_leaves * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  if (n_leaves > 0) {
+    leaf_compact_kernel<<<(unsigned)std::min<int64_t>(n_leaves, 65535), 256, 0, st>>>(n_leaves, leaf_dst, leaf_off,
+                                                                                         staging, leaf_ids);
+    PIPNN_LAUNCHED("leaf_compact_kernel", st);
+  }
+  int64_t ni = 0;
+  PIPNN_CUDA(cudaMemcpyAsync(&ni, leaf_off + n_leaves, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  PIPNN_CUDA(cudaStreamSynchronize(st));
+  *n_leaves_h = n_leaves;
+  *n_inst_h = ni;
+  *depth_h = depth;
+  return PIPNN_OK;
+}
+
+}  // namespace pipnn

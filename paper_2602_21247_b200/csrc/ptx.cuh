@@ -44,10 +44,13 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar_addr, uint32_t parity
 }
 // Bounded wait. ~2^22 try_wait rounds (each may suspend in hardware) ≈ seconds; on timeout the
 // caller-supplied flag gets `code` and false is returned.
+// Also gives up early (returns false) once another thread has raised the flag, so one failure does not
+// leave the rest of the grid spinning.
 __device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity, int* err_flag, int code) {
   const uint32_t a = smem_u32(bar);
   for (uint32_t it = 0; it < (1u << 22); ++it) {
     if (mbar_try_wait(a, parity)) return true;
+    if ((it & 1023u) == 1023u && err_flag && *(volatile int*)err_flag != 0) return false;
   }
   if (err_flag) atomicExch(err_flag, code);
   return false;

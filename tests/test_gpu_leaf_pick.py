@@ -1,0 +1,105 @@
+"""GPU parity of pipnn_leaf_pick (K5: tcgen05 distance tiles + fused top-k) against the CPU oracle, both fed
+the same (oracle) leaves. uint8: bit-exact ids and distances. float: SURVEY §8(c) tolerances."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from tests.helpers import UINT32_MAX, check_candidate_lists_float
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def P():
+    import paper_2602_21247_b200 as P
+
+    return P
+
+
+def run_gpu(X, metric, off, ids, k):
+    Xt = torch.from_numpy(X).cuda()
+    nbr, dist = P().pipnn_leaf_pick(Xt, torch.from_numpy(off).cuda(), torch.from_numpy(ids.view(np.int32)).cuda(), k,
+                                    metric)
+    torch.cuda.synchronize()
+    return nbr.cpu().numpy().view(np.uint32), dist.cpu().numpy()
+
+
+def random_leaves(n, sizes, seed=0):
+    rng = np.random.default_rng(seed)
+    leaves = [np.sort(rng.choice(n, size=s, replace=False)).astype(np.uint32) for s in sizes]
+    off = np.concatenate([[0], np.cumsum([len(l) for l in leaves])]).astype(np.int64)
+    return off, np.concatenate(leaves)
+
+
+EDGE_SIZES = [1, 2, 3, 8, 9, 16, 17, 31, 32, 33, 127, 128, 129, 255, 256, 257, 300, 511, 512, 1000, 1024, 1500,
+              2048, 4096]
+
+
+@pytest.mark.parametrize("k", [1, 8, 10, 15])
+def test_leaf_pick_u8_edge_sizes_bit_exact(k):
+    X = synth.gen_uniform(6000, 128, "u8", seed=3)
+    X = (X // 16).astype(np.uint8)  # coarse values -> many exact distance ties (id tie-break)
+    off, ids = random_leaves(len(X), EDGE_SIZES, seed=k)
+    nbr, dist = run_gpu(X, "l2", off, ids, k)
+    onbr, odist = O.leaf_pick(O.Dataset(X), off, ids, k)
+    assert np.array_equal(nbr, onbr)
+    ok = onbr != UINT32_MAX
+    assert np.array_equal(dist[ok].astype(np.float64), odist[ok])
+    assert np.isinf(dist[~ok]).all()
+
+
+@pytest.mark.parametrize("d", [100, 128, 200])
+def test_leaf_pick_u8_other_dims(d):
+    X = synth.gen_uniform(3000, d, "u8", seed=d)
+    off, ids = random_leaves(len(X), [5, 130, 700, 1024], seed=1)
+    nbr, dist = run_gpu(X, "l2", off, ids, 8)
+    onbr, odist = O.leaf_pick(O.Dataset(X), off, ids, 8)
+    assert np.array_equal(nbr, onbr)
+    ok = onbr != UINT32_MAX
+    assert np.array_equal(dist[ok].astype(np.float64), odist[ok])
+
+
+@pytest.mark.parametrize("name,n", [("C2", 20000)])
+def test_leaf_pick_u8_config_leaves(name, n):
+    cfg = synth.CONFIGS[name].scaled(n)
+    X = synth.gen_points(cfg)
+    ds = O.Dataset(X)
+    off, ids, _ = O.partition(ds, cfg.params())
+    nbr, dist = run_gpu(X, "l2", off, ids, cfg.k)
+    onbr, odist = O.leaf_pick(ds, off, ids, cfg.k)
+    assert np.array_equal(nbr, onbr)
+    ok = onbr != UINT32_MAX
+    assert np.array_equal(dist[ok].astype(np.float64), odist[ok])
+
+
+@pytest.mark.parametrize("name,n", [("C1", 10000), ("C3", 20000), ("C4", 20000)])
+def test_leaf_pick_float_config_leaves(name, n):
+    cfg = synth.CONFIGS[name]
+    if cfg.n != n:
+        cfg = cfg.scaled(n)
+    X = synth.gen_points(cfg)
+    ds = O.Dataset(X, metric=cfg.metric, mode="bf16")
+    off, ids, _ = O.partition(ds, cfg.params())
+    nbr, dist = run_gpu(X, cfg.metric, off, ids, cfg.k)
+    onbr, odist = O.leaf_pick(ds, off, ids, cfg.k)
+    ndiff, rows = check_candidate_lists_float(X, cfg.metric, ids, nbr, dist, onbr, odist, cfg.k)
+    assert ndiff <= 0.01 * rows, (ndiff, rows)
+
+
+@pytest.mark.parametrize("metric,d", [("l2", 96), ("mips", 200), ("l2", 240), ("l2", 7)])
+def test_leaf_pick_float_edge_sizes(metric, d):
+    X = synth.gen_uniform(6000, d, "f32", seed=d)
+    off, ids = random_leaves(len(X), EDGE_SIZES, seed=2)
+    nbr, dist = run_gpu(X, metric, off, ids, 8)
+    onbr, odist = O.leaf_pick(O.Dataset(X, metric=metric, mode="bf16"), off, ids, 8)
+    ndiff, rows = check_candidate_lists_float(X, metric, ids, nbr, dist, onbr, odist, 8)
+    assert ndiff <= 0.01 * rows, (ndiff, rows)
+
+
+def test_leaf_pick_rejects_k16():
+    X = torch.zeros((10, 8), dtype=torch.uint8, device="cuda")
+    off = torch.tensor([0, 10], dtype=torch.int64, device="cuda")
+    ids = torch.arange(10, dtype=torch.int32, device="cuda")
+    with pytest.raises(P().PipnnError):
+        P().pipnn_leaf_pick(X, off, ids, 16)

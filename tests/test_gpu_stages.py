@@ -1,0 +1,164 @@
+"""GPU stage parity through the C ABI: each stage is fed the ORACLE's input for that stage, so a difference
+cannot cascade (SURVEY §4 layer 2). uint8 and every integer/key artefact: bit-exact."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from tests.helpers import UINT32_MAX
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def P():
+    import paper_2602_21247_b200 as P
+
+    return P
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+# ---------------------------------------------------------------- a0 sketches
+@pytest.mark.parametrize("dtype,d", [("u8", 128), ("f32", 96), ("f32", 200), ("u8", 100)])
+def test_sketch_bit_exact(dtype, d):
+    X = synth.gen_uniform(5000, d, dtype, seed=d)
+    S = P().pipnn_sketch(cuda(X), m=12, seed=0x5EED).cpu().numpy()
+    ref = O.sketch(O.Dataset(X, mode="bf16"), O.hyperplanes(12, d, 0x5EED))
+    assert S.dtype == ref.dtype
+    assert np.array_equal(S.view(np.uint32), ref.view(np.uint32))
+
+
+# ---------------------------------------------------------------- a5/a6 HashPrune
+def oracle_edges(cfg, k=None, n=None):
+    X = synth.gen_points(cfg)
+    ds = O.Dataset(X, metric=cfg.metric, mode="bf16")
+    off, ids, _ = O.partition(ds, cfg.params())
+    nbr, dd = O.leaf_pick(ds, off, ids, k or cfg.k)
+    own, cand, dist = O.bidirected_edges(ids, nbr, dd)
+    S = O.sketch(ds, O.hyperplanes(cfg.m, cfg.d, cfg.seed))
+    return X, S, own, cand, dist.astype(np.float32)
+
+
+@pytest.mark.parametrize("name,l_max,k", [("C2", 128, 8), ("C2", 8, 15), ("C2", 16, 15), ("C1", 128, 8),
+                                          ("C4", 160, 10), ("C4", 8, 10)])
+def test_hashprune_insert_bit_exact_batched_shuffled(name, l_max, k):
+    cfg = synth.CONFIGS[name].scaled(6000)
+    X, S, own, cand, dist = oracle_edges(cfg, k=k)
+    n = len(X)
+    ref_slots, ref_count, ok = O.hashprune(n, S, l_max, own, cand, dist.astype(np.float64))
+    assert ok
+    perm = np.random.default_rng(7).permutation(len(own))
+    slots, count = P().new_reservoirs(n, l_max)
+    St = cuda(S)
+    for part in np.array_split(perm, 3):  # three batches: composition is exact (Supp. G lemma)
+        P().hashprune_insert(St, slots, count, cuda(own[part].view(np.int32)), cuda(cand[part].view(np.int32)),
+                             cuda(dist[part]), m=cfg.m)
+    assert np.array_equal(count.cpu().numpy().view(np.uint32), ref_count)
+    assert np.array_equal(slots.cpu().numpy().view(np.uint64), ref_slots)
+    if l_max <= 16:
+        assert (ref_count == l_max).mean() > 0.2  # the eviction branch of Alg. 3 is exercised
+
+
+def test_hashprune_hub_owner():
+    # one owner receiving 20k edges (CTA-scale segment, chunked merge) + many small owners
+    rng = np.random.default_rng(3)
+    n, m, l_max = 30000, 12, 128
+    S = rng.integers(-1000, 1000, size=(n, m)).astype(np.int32)
+    own = np.concatenate([np.zeros(20000, np.uint32), rng.integers(1, n, 50000).astype(np.uint32)])
+    cand = rng.integers(1, n, len(own)).astype(np.uint32)
+    dist = rng.integers(0, 5000, len(own)).astype(np.float32)  # integer distances: many bf16 ties
+    ref_slots, ref_count, ok = O.hashprune(n, S, l_max, own, cand, dist.astype(np.float64))
+    assert ok and ref_count[0] == l_max
+    slots, count = P().new_reservoirs(n, l_max)
+    P().hashprune_insert(cuda(S), slots, count, cuda(own.view(np.int32)), cuda(cand.view(np.int32)), cuda(dist), m=m)
+    assert np.array_equal(slots.cpu().numpy().view(np.uint64), ref_slots)
+    assert np.array_equal(count.cpu().numpy().view(np.uint32), ref_count)
+
+
+# ---------------------------------------------------------------- a7/a8 final prune + CSR
+@pytest.mark.parametrize("name,R,final", [("C2", 64, 1), ("C2", 8, 1), ("C2", 32, 0)])
+def test_final_prune_u8_bit_exact(name, R, final):
+    cfg = synth.CONFIGS[name].scaled(6000)
+    X, S, own, cand, dist = oracle_edges(cfg)
+    n = len(X)
+    slots, count, ok = O.hashprune(n, S, cfg.l_max, own, cand, dist.astype(np.float64))
+    rp, ci, ok2 = O.final_prune(O.Dataset(X), slots, count, R, (6, 5), final)
+    assert ok and ok2
+    grp, gci = P().pipnn_final_prune(cuda(X), cuda(slots.view(np.int64)), cuda(count.view(np.int32)), R=R,
+                                     final_prune=final)
+    grp = grp.cpu().numpy()
+    assert np.array_equal(grp, rp)
+    assert np.array_equal(u32(gci)[: grp[-1]], ci)
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
+def test_final_prune_float_close(name):
+    cfg = synth.CONFIGS[name].scaled(6000) if synth.CONFIGS[name].n != 6000 else synth.CONFIGS[name]
+    X, S, own, cand, dist = oracle_edges(cfg)
+    n = len(X)
+    slots, count, ok = O.hashprune(n, S, cfg.l_max, own, cand, dist.astype(np.float64))
+    ds = O.Dataset(X, metric=cfg.metric, mode="bf16")
+    rp, ci, _ = O.final_prune(ds, slots, count, cfg.R)
+    grp, gci = P().pipnn_final_prune(cuda(X), cuda(slots.view(np.int64)), cuda(count.view(np.int32)), R=cfg.R,
+                                     metric=cfg.metric)
+    grp = grp.cpu().numpy()
+    gci = u32(gci)
+    same = sum(set(ci[rp[u]:rp[u + 1]]) == set(gci[grp[u]:grp[u + 1]]) for u in range(n))
+    assert same >= 0.99 * n, same  # fp32-vs-fp64 alpha tests may flip at exact near-ties only
+    assert np.diff(grp).max() <= cfg.R
+
+
+# ---------------------------------------------------------------- a1/a2 partition
+def canon(off, ids):
+    return sorted(tuple(ids[off[i]:off[i + 1]].tolist()) for i in range(len(off) - 1))
+
+
+@pytest.mark.parametrize("n,c_max,c_min,fanout,reps", [(20000, 1024, 100, (2,), 1), (30000, 256, 40, (2,), 1),
+                                                       (20000, 256, 40, (4, 2), 2), (900, 1024, 100, (2,), 2),
+                                                       (5000, 128, 20, (3,), 1)])
+def test_partition_u8_bit_exact(n, c_max, c_min, fanout, reps):
+    cfg = synth.C2.scaled(n)
+    X = synth.gen_points(cfg)
+    p = cfg.params()
+    p.update(c_max=c_max, p_den=c_max, c_min=c_min, fanout=fanout, replicas=reps)
+    off, ids, depth = O.partition(O.Dataset(X), p)
+    pp = P().partition_params(c_max=c_max, c_min=c_min, p_samp=(2, c_max), fanout=fanout, replicas=reps,
+                              seed=p["seed"])
+    goff, gids = P().pipnn_partition(cuda(X), pp)
+    goff, gids = goff.cpu().numpy(), u32(gids)
+    assert canon(goff, gids) == canon(off, ids)
+
+
+def test_partition_duplicates_guard():
+    X = np.zeros((3000, 16), dtype=np.uint8)
+    pp = P().partition_params(c_max=256, c_min=40, fanout=(2,))
+    goff, gids = P().pipnn_partition(cuda(X), pp)
+    p = synth.C2.params()
+    p.update(c_max=256, p_den=256, c_min=40)
+    off, ids, _ = O.partition(O.Dataset(X), p)
+    assert canon(goff.cpu().numpy(), u32(gids)) == canon(off, ids)
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
+def test_partition_float_invariants_and_overlap(name):
+    cfg = synth.CONFIGS[name]
+    cfg = cfg.scaled(20000) if cfg.n != 10000 else cfg
+    X = synth.gen_points(cfg)
+    p = cfg.params()
+    off, ids, _ = O.partition(O.Dataset(X, metric=cfg.metric, mode="bf16"), p)
+    pp = P().partition_params(c_max=cfg.c_max, fanout=cfg.fanout, seed=cfg.seed)
+    goff, gids = P().pipnn_partition(cuda(X), pp, metric=cfg.metric)
+    goff, gids = goff.cpu().numpy(), u32(gids)
+    sizes = np.diff(goff)
+    assert sizes.max() <= cfg.c_max
+    mult = np.bincount(gids, minlength=len(X))
+    assert mult.min() >= 1 and mult.max() <= int(np.prod(cfg.fanout))
+    a, b = set(canon(goff, gids)), set(canon(off, ids))
+    assert len(a & b) >= 0.9 * max(len(a), len(b)), (len(a & b), len(a), len(b))  # near-tie assignments only
