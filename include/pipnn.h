@@ -107,8 +107,10 @@ typedef struct {
 /* Per-stage device times (CUDA events on `stream`) and counters of the last pipnn_build. */
 typedef struct {
   int64_t n_leaves, n_instances, n_edges, max_leaf;
+  int64_t leaf_pairs; /* sum over leaves of |b|^2: the leaf distance work is 2 * leaf_pairs * d ops */
   int32_t depth;
   float ms_prep, ms_partition, ms_leaf, ms_hashprune, ms_final, ms_total;
+  float ms_leaf_tiles; /* the distance-tile kernel(s) of the leaf stage alone (events around the launches) */
 } pipnn_stats;
 
 /* Reservoir slot layout (part of the ABI; "4-byte ID, 2-byte hash, bf16 norm"):
@@ -118,6 +120,9 @@ typedef struct {
 
 PIPNN_API const char* pipnn_last_error(void);
 PIPNN_API int32_t pipnn_abi_version(void);
+/* Number of kernels this library has launched in this process (diagnostic; CUB scans/sorts it runs
+ * internally are not counted). */
+PIPNN_API uint64_t pipnn_launch_count(void);
 /* After a call returned PIPNN_EWORKSPACE (e.g. a size query with ws == NULL): the bytes it needs. */
 PIPNN_API size_t pipnn_required_workspace(void);
 

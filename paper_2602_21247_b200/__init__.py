@@ -65,8 +65,9 @@ class BuildParams(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("n_leaves", C.c_int64), ("n_instances", C.c_int64), ("n_edges", C.c_int64), ("max_leaf", C.c_int64),
-                ("depth", C.c_int32), ("ms_prep", C.c_float), ("ms_partition", C.c_float), ("ms_leaf", C.c_float),
-                ("ms_hashprune", C.c_float), ("ms_final", C.c_float), ("ms_total", C.c_float)]
+                ("leaf_pairs", C.c_int64), ("depth", C.c_int32), ("ms_prep", C.c_float),
+                ("ms_partition", C.c_float), ("ms_leaf", C.c_float), ("ms_hashprune", C.c_float),
+                ("ms_final", C.c_float), ("ms_total", C.c_float), ("ms_leaf_tiles", C.c_float)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -77,6 +78,7 @@ _vp = C.c_void_p
 _lib.pipnn_last_error.restype = C.c_char_p
 _lib.pipnn_abi_version.restype = C.c_int32
 _lib.pipnn_required_workspace.restype = C.c_size_t
+_lib.pipnn_launch_count.restype = C.c_uint64
 _lib.pipnn_workspace_size.argtypes = [_P(Points), _P(BuildParams), _P(C.c_size_t)]
 _lib.pipnn_partition.argtypes = [_P(Points), _P(PartitionParams), _vp, C.c_size_t, _vp, C.c_int64, _vp, C.c_int64,
                                  _P(C.c_int64), _P(C.c_int64), _vp]
@@ -93,13 +95,17 @@ for _f in ("pipnn_workspace_size", "pipnn_partition", "pipnn_leaf_pick", "pipnn_
            "hashprune_insert", "pipnn_final_prune", "pipnn_build"):
     getattr(_lib, _f).restype = C.c_int
 
-EXPORTS = ("pipnn_last_error", "pipnn_abi_version", "pipnn_required_workspace", "pipnn_workspace_size",
+EXPORTS = ("pipnn_last_error", "pipnn_abi_version", "pipnn_required_workspace", "pipnn_launch_count", "pipnn_workspace_size",
            "pipnn_partition", "pipnn_leaf_pick", "pipnn_sketch", "pipnn_device_error", "hashprune_insert",
            "pipnn_final_prune", "pipnn_build")
 
 
 def lib():
     return _lib
+
+
+def pipnn_launch_count() -> int:
+    return _lib.pipnn_launch_count()
 
 
 def _check(rc: int):

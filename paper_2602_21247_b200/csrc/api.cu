@@ -1,5 +1,6 @@
 // api.cu — the C ABI (include/pipnn.h): validation, workspace sizing, stream plumbing, stage timing.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -9,6 +10,8 @@
 namespace pipnn {
 
 static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 static thread_local size_t g_required_ws = 0;
 
 void set_error(const std::string& msg) { g_last_error = msg; }
@@ -130,6 +133,8 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   uint32_t* count = ar.take<uint32_t>(X->n);
   int64_t* n_edges_dev = ar.take<int64_t>(1);
   const size_t mark = ar.mark();
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tile_ev;
+  int64_t leaf_pairs = 0;
 
   cudaEvent_t ev[7];
   if (!ar.measuring()) {
@@ -141,6 +146,11 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   auto cleanup = [&]() {
     if (!ar.measuring())
       for (auto& e : ev) cudaEventDestroy(e);
+    for (auto& pr : tile_ev) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    tile_ev.clear();
   };
   // (a0) sketches
   pipnn_status s = sketch_impl(X, p->hp.m, p->hp.seed, sketch, ar, c);
@@ -166,6 +176,8 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
     std::vector<int64_t> off(n_leaves + 1);
     PIPNN_CUDA(cudaMemcpyAsync(off.data(), leaf_off, (n_leaves + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     PIPNN_CUDA(cudaStreamSynchronize(st));
+    for (int64_t b = 0; b < n_leaves; ++b) leaf_pairs += (off[b + 1] - off[b]) * (off[b + 1] - off[b]);
+    if (stats_h) c.tile_events = &tile_ev;
     int64_t b0 = 0;
     while (b0 < n_leaves) {
       int64_t items = 0, b1 = b0;
@@ -179,6 +191,7 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
       ar.release(mark);
       b0 = b1;
     }
+    c.tile_events = nullptr;
   }
   ar.release(mark);
   if (!ar.measuring()) cudaEventRecord(ev[3], st);
@@ -225,6 +238,14 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
       for (int64_t b = 0; b < n_leaves; ++b) mx = std::max(mx, off[b + 1] - off[b]);
     }
     stats_h->max_leaf = mx;
+    stats_h->leaf_pairs = leaf_pairs;
+    float tt = 0.0f;
+    for (auto& pr : tile_ev) {
+      float x = 0.0f;
+      cudaEventElapsedTime(&x, pr.first, pr.second);
+      tt += x;
+    }
+    stats_h->ms_leaf_tiles = tt;
   }
   cleanup();
   return PIPNN_OK;
@@ -238,6 +259,7 @@ extern "C" {
 
 const char* pipnn_last_error(void) { return g_last_error.c_str(); }
 size_t pipnn_required_workspace(void) { return g_required_ws; }
+uint64_t pipnn_launch_count(void) { return g_launches.load(); }
 int32_t pipnn_abi_version(void) { return PIPNN_ABI_VERSION; }
 
 pipnn_status pipnn_workspace_size(const pipnn_points* X, const pipnn_build_params* p, size_t* bytes_h) {

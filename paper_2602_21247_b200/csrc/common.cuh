@@ -12,6 +12,7 @@ namespace pipnn {
 
 // ------------------------------------------------------------------ status / last error
 void set_error(const std::string& msg);
+void count_launch();  // kernels launched by this library (diagnostic counter, pipnn_launch_count)
 pipnn_status fail(pipnn_status s, const std::string& msg);
 bool sync_debug();  // PIPNN_SYNC_DEBUG=1
 
@@ -30,6 +31,7 @@ struct CudaError {
 // After a kernel launch: launch error, and in debug mode a synchronisation.
 #define PIPNN_LAUNCHED(name, stream)                                                                 \
   do {                                                                                               \
+    ::pipnn::count_launch();                                                                         \
     cudaError_t _e = cudaGetLastError();                                                             \
     if (_e == cudaSuccess && ::pipnn::sync_debug()) _e = cudaStreamSynchronize(stream);              \
     if (_e != cudaSuccess)                                                                           \

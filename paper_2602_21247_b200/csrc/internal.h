@@ -1,6 +1,8 @@
 // internal.h — host-side declarations shared by the libpipnn translation units (not the ABI).
 #pragma once
 #include <cstdint>
+#include <utility>
+#include <vector>
 #include <cuda_runtime.h>
 #include "common.cuh"
 #include "dist_topk.cuh"
@@ -10,6 +12,8 @@ namespace pipnn {
 struct Ctx {
   cudaStream_t st;
   int* err;  // device error flag (DevErr)
+  // optional: event pairs recorded around every distance-tile kernel of the leaf stage (stats)
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* tile_events = nullptr;
 };
 
 // Bytes per row of the tiled (K-major, SWIZZLE_NONE) layout: uint8 -> round_up(d, 32);
