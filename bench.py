@@ -1,0 +1,325 @@
+#!/usr/bin/env python3
+"""bench.py — PiPNN index build on B200 (BASELINE.json metric: build points/s, leaf distance TFLOP/s,
+% roofline, recall@10).
+
+A step = one pipnn_build (all §8(a) rows: sketches, partition, leaf distance tiles + pick, HashPrune,
+final prune, CSR) over one synthetic input resident in HBM. Default workload: BASELINE.json configs[1]
+(C2: n=1M, d=128 uint8, L2, BIGANN-shaped mixture). Multi-GPU: one process per GPU (torchrun), each rank
+builds its own independent replica of the workload (the build does not shard),
+value = all ranks' points / max-over-ranks time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+--impl reference times the CPU oracle (oracle/, the reference arm of this tier) on a bounded sample of the
+same workload on the host cores; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "index build points/s and leaf distance TFLOP/s on 1 B200; % roofline; recall@10"
+UNIT = "points/s"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def workload_desc(cfg: synth.Config) -> dict:
+    return {"workload": f"{cfg.name}: n={cfg.n:,} d={cfg.d} {cfg.dtype} {cfg.metric}, {cfg.n_centres:,}-cluster "
+                        f"synthetic mixture (BASELINE.json configs[{list(synth.CONFIGS).index(cfg.name.split('@')[0])}])",
+            "n": cfg.n, "d": cfg.d, "dtype": cfg.dtype, "metric": cfg.metric, "c_max": cfg.c_max,
+            "fanout": list(cfg.fanout), "k": cfg.k, "m": cfg.m, "l_max": cfg.l_max, "R": cfg.R,
+            "alpha": f"{cfg.alpha_num}/{cfg.alpha_den}", "c_min": cfg.c_min, "leader_cap": cfg.leader_cap}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [x.strip() for x in out.stdout.strip().split(",")]
+                if len(parts) >= 8:
+                    self.rows.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_reference(args, cfg):
+    """Reference arm: the CPU oracle, as it stands, on a bounded sample of the workload (rank 0 only)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+
+    n_s = args.ref_sample
+    sub = cfg.scaled(n_s) if n_s < cfg.n else cfg
+    X = synth.gen_points(sub)
+    ds = O.Dataset(X, metric=cfg.metric, mode="bf16")
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.build(ds, sub.params())
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    val = sub.n / t
+    cores = O.num_threads()
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if cfg.dtype != "u8" else "int64", "data": "synthetic",
+            "config": workload_desc(cfg),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"oracle build (partition, leaf pick, HashPrune, final prune) of the first "
+                                       f"{sub.n:,} points of the {cfg.name} generator with the same parameters"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, n_sample):
+    import oracle as O
+
+    sub = cfg.scaled(n_sample)
+    X = synth.gen_points(sub)
+    ds = O.Dataset(X, metric=cfg.metric, mode="bf16")
+    t0 = time.perf_counter()
+    O.build(ds, sub.params())
+    dt = time.perf_counter() - t0
+    return {"value": sub.n / dt, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
+            "sample": f"oracle build of the first {sub.n:,} points of the {cfg.name} generator, same parameters "
+                      f"({dt:.1f} s)"}
+
+
+def recall_eval(X, cfg, rp, ci, n_queries):
+    """recall@10 of the GPU graph: exact ground truth by a fp32 torch GEMM (exact for uint8 data), CPU beam
+    search of the oracle's evaluation harness (Alg. 1) from the mean-nearest entry point."""
+    import torch
+
+    import oracle as O
+
+    Q = synth.gen_queries(cfg, n_queries=n_queries)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    Xt = torch.from_numpy(X).cuda().float()
+    Qt = torch.from_numpy(Q).cuda().float()
+    if cfg.metric == "mips":
+        D = -(Qt @ Xt.T)
+    else:
+        D = (Qt * Qt).sum(1, keepdim=True) + (Xt * Xt).sum(1)[None] - 2 * (Qt @ Xt.T)
+    truth = torch.topk(D, 10, dim=1, largest=False).indices.cpu().numpy().astype(np.uint32)
+    ds = O.Dataset(X, metric=cfg.metric, mode="exact")
+    e = O.entry_point(ds)
+    out = {}
+    for L in (10, 32, 64, 128):
+        res, cmps = O.beam_search(ds, rp, ci, Q, e, L, 10)
+        out[str(L)] = round(float(O.recall_at(res, truth).mean()), 4)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-sample", type=int, default=100_000)
+    ap.add_argument("--cpu-sample", type=int, default=200_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--recall-queries", type=int, default=1000)
+    args = ap.parse_args()
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_21247_b200 as P
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    X = synth.gen_points(cfg, seed=rank)  # each rank: an independent replica of the workload
+    Xh = torch.from_numpy(X).pin_memory()
+    Xd = Xh.to(dev)
+    params = P.build_params_from(cfg.params())
+    builder = P.Builder(Xd, params, metric=cfg.metric)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        out = builder(Xd)
+    torch.cuda.synchronize()
+
+    # ---------------- device-timed region (inputs resident in HBM)
+    step_ms, stats = [], []
+    launches0 = P.pipnn_launch_count()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between timed iterations (outside the events)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            out = builder(Xd)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            stats.append(out.stats)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches = P.pipnn_launch_count() - launches0
+    ms = sum(step_ms) / len(step_ms)
+    ms_t = torch.tensor([ms], device=dev)
+    if ws > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = cfg.n * ws / (ms_max / 1e3)
+
+    # ---------------- end-to-end through the public API with host buffers (pinned), copies inside
+    n_rp = cfg.n + 1
+    rp_h = torch.empty(n_rp, dtype=torch.int64).pin_memory()
+    ci_h = torch.empty(cfg.n * cfg.R, dtype=torch.int32).pin_memory()
+    e2e_ms, d2h = [], 0
+    for _ in range(max(2, min(args.steps, 5))):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        Xd.copy_(Xh, non_blocking=True)
+        o = builder(Xd)
+        rp_h.copy_(o.row_ptr, non_blocking=True)
+        ci_h[: o.n_edges].copy_(o.col_idx, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+        d2h = n_rp * 8 + o.n_edges * 4
+    e2e_t = torch.tensor([sum(e2e_ms) / len(e2e_ms)], device=dev)
+    if ws > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_val = cfg.n * ws / (float(e2e_t.item()) / 1e3)
+
+    if rank == 0:
+        peaks, src = measured_peaks()
+        st = stats[-1]
+        tile_ms = statistics.mean(s["ms_leaf_tiles"] for s in stats)
+        leaf_ops = 2.0 * st["leaf_pairs"] * cfg.d  # algorithmic: 2 s^2 d per leaf
+        if cfg.dtype == "u8":
+            peak = 2.0 * peaks["bf16_tflops"]  # int8 dense = 2x bf16 (nominal ratio) x measured bf16 burst
+            peak_note = f"int8 = 2 x bf16 burst ({src} MEASURED_PEAKS.json), nominal ratio 4.5/2.25 PF"
+        else:
+            peak = peaks["bf16_tflops"]
+            peak_note = f"bf16 burst ({src} MEASURED_PEAKS.json)"
+        achieved = leaf_ops / (tile_ms / 1e3) / 1e12
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "leaf_tile_traffic.json")
+        if os.path.exists(tp):
+            try:
+                with open(tp) as f:
+                    traffic = json.load(f).get(cfg.name)
+            except Exception:
+                traffic = None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u8" if cfg.dtype == "u8" else "bf16", "data": "synthetic",
+            "config": {**workload_desc(cfg), "parallelism": f"replicas x{ws} (independent builds)",
+                       "l2": "flushed between timed steps (512 MB write)"},
+            "roofline": {"bound": "tensor", "kernel": "dist_topk_kernel (leaf distance tiles + fused pick)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s" if cfg.dtype != "u8" else "TOP/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_note,
+                         "algorithmic_ops_per_launch": leaf_ops, "ms_per_launch": tile_ms},
+            "stages_ms": {k: round(statistics.mean(s[k] for s in stats), 4) for k in
+                          ("ms_prep", "ms_partition", "ms_leaf", "ms_leaf_tiles", "ms_hashprune", "ms_final",
+                           "ms_total")},
+            "counts": {k: st[k] for k in ("n_leaves", "n_instances", "n_edges", "max_leaf", "depth")},
+            "leaf_tflops": achieved,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if args.recall_queries > 0:
+            try:
+                rp = out.row_ptr.cpu().numpy()
+                ci = out.col_idx.cpu().numpy().view(np.uint32)
+                line["recall_at_10"] = recall_eval(X, cfg, rp, ci, args.recall_queries)
+                line["recall_queries"] = args.recall_queries
+            except Exception as ex:  # evaluation is reported, never gates the timing
+                line["recall_at_10"] = f"failed: {ex}"
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

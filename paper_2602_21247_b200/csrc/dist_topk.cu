@@ -3,14 +3,21 @@
 
 namespace pipnn {
 
-template <bool U8, bool MIPS>
+template <bool U8, bool MIPS, int KMAX>
 static pipnn_status launch_one(const DistTopkArgs& a, cudaStream_t st) {
   const int smem = dt_smem_bytes(a.Kb);
-  auto* fn = dist_topk_kernel<U8, MIPS>;
+  auto* fn = dist_topk_kernel<U8, MIPS, KMAX>;
   PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   fn<<<num_sms(), kDtThreads, smem, st>>>(a);
   PIPNN_LAUNCHED("dist_topk_kernel", st);
   return PIPNN_OK;
+}
+
+template <bool U8, bool MIPS>
+static pipnn_status launch_k(const DistTopkArgs& a, int kmax, cudaStream_t st) {
+  if (kmax <= 4) return launch_one<U8, MIPS, 4>(a, st);
+  if (kmax <= 12) return launch_one<U8, MIPS, 12>(a, st);
+  return launch_one<U8, MIPS, 16>(a, st);
 }
 
 // kmax: the largest running-list length any segment needs (k + 1 with self exclusion).
@@ -19,9 +26,9 @@ pipnn_status launch_dist_topk(const DistTopkArgs& a, bool u8, bool mips, int kma
     return fail(PIPNN_EUNSUPPORTED, "dist_topk: row bytes must be a multiple of 32 and <= 512");
   if (kmax > kTopkMax) return fail(PIPNN_EUNSUPPORTED, "dist_topk: k too large (k+1 <= 16 with self exclusion)");
   if (u8 && mips) return fail(PIPNN_EINVAL, "uint8 + MIPS unsupported");
-  if (u8) return launch_one<true, false>(a, st);
-  if (mips) return launch_one<false, true>(a, st);
-  return launch_one<false, false>(a, st);
+  if (u8) return launch_k<true, false>(a, kmax, st);
+  if (mips) return launch_k<false, true>(a, kmax, st);
+  return launch_k<false, false>(a, kmax, st);
 }
 
 }  // namespace pipnn

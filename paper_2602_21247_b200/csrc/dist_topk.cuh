@@ -70,24 +70,66 @@ struct DistTopkArgs {
   int* err;
 };
 
-constexpr int kDtStages = 4;
+constexpr int kDtMaxStages = 4;
 constexpr int kDtStageBytes = 256 * 128;  // 256 rows x 128 B of K
 constexpr int kDtThreads = 192;
 constexpr int kTopkMax = 16;              // max entries of a row's running list (k+1 with self exclusion)
+constexpr int kQCap = 64;                 // per-row candidate queue (SMEM) between drains
 constexpr int32_t kPadNormU8 = 0x3FFFFFFF; // norm of a padding row: key far above any real key
 constexpr float kPadKey = 1e30f;           // float: column term of a padding row
 
-__host__ __device__ constexpr int dt_smem_bytes(int Kb) {
-  return 128 * Kb + kDtStages * kDtStageBytes + 4096 /*ones tile*/ + kTopkMax * 128 * 8 /*top-k state*/;
+__host__ __device__ constexpr int dt_fixed_smem(int Kb) { return 128 * Kb + 4096 /*ones*/ + kQCap * 128 * 8 /*queues*/; }
+__host__ __device__ constexpr int dt_stages(int Kb) {
+  return (227 * 1024 - 2048 - dt_fixed_smem(Kb)) / kDtStageBytes >= kDtMaxStages
+             ? kDtMaxStages
+             : (227 * 1024 - 2048 - dt_fixed_smem(Kb)) / kDtStageBytes;
+}
+__host__ __device__ constexpr int dt_smem_bytes(int Kb) { return dt_fixed_smem(Kb) + dt_stages(Kb) * kDtStageBytes; }
+
+// Register top-K list (sorted ascending by (key, col)); insert requires key < kk[K-1] for the runtime K.
+template <typename KT, int KMAX>
+__device__ __forceinline__ void topk_insert(KT (&kk)[KMAX], uint32_t (&ii)[KMAX], KT key, uint32_t col) {
+#pragma unroll
+  for (int t = KMAX - 1; t >= 0; --t) {
+    if (t > 0 && key < kk[t - 1]) {
+      kk[t] = kk[t - 1];
+      ii[t] = ii[t - 1];
+    } else if (key < kk[t]) {
+      kk[t] = key;
+      ii[t] = col;
+    }
+  }
+}
+template <typename KT, int KMAX>
+__device__ __forceinline__ KT topk_kth(const KT (&kk)[KMAX], int K) {
+  KT r = kk[0];
+#pragma unroll
+  for (int t = 1; t < KMAX; ++t)
+    if (t == K - 1) r = kk[t];
+  return r;
 }
 
-template <bool U8, bool MIPS>
+// Drain a row's SMEM candidate queue (stride 128 words) into its register list.
+template <typename KT, int KMAX>
+__device__ __forceinline__ void topk_drain(KT (&kk)[KMAX], uint32_t (&ii)[KMAX], KT& thr, int& qlen,
+                                           const KT* qk, const uint32_t* qc, int K) {
+  for (int e = 0; e < qlen; ++e) {
+    const KT key = qk[e * 128];
+    if (key < thr) {
+      topk_insert<KT, KMAX>(kk, ii, key, qc[e * 128]);
+      thr = topk_kth<KT, KMAX>(kk, K);
+    }
+  }
+  qlen = 0;
+}
+
+template <bool U8, bool MIPS, int KMAX>
 __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopkArgs args) {
   using KT = typename std::conditional<U8, int32_t, float>::type;
   constexpr bool kFold = !U8;  // float paths fold the column term into an augmented MMA K-step
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar_a_full, bar_a_empty;
-  __shared__ __align__(8) uint64_t bar_b_full[kDtStages], bar_b_empty[kDtStages];
+  __shared__ __align__(8) uint64_t bar_b_full[kDtMaxStages], bar_b_empty[kDtMaxStages];
   __shared__ __align__(8) uint64_t bar_acc_full[2], bar_acc_empty[2];
   __shared__ uint32_t tmem_base_sh;
 
@@ -96,11 +138,12 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
   const int KC = Kb >> 4;                   // 16-B K planes per row (incl. the 2 augment planes for float)
   const int KCm = kFold ? KC - 2 : KC;      // planes of the coordinates themselves
   const int nchunks = (KC + 7) >> 3;
+  const int NS = dt_stages(Kb);
   uint8_t* sA = smem;
-  uint8_t* sB = smem + 128 * Kb;
-  uint8_t* sOnes = sB + kDtStages * kDtStageBytes;
-  KT* tk_key = reinterpret_cast<KT*>(sOnes + 4096);            // [kTopkMax][128]
-  uint32_t* tk_col = reinterpret_cast<uint32_t*>(tk_key + kTopkMax * 128);
+  uint8_t* sOnes = smem + 128 * Kb;
+  KT* q_key = reinterpret_cast<KT*>(sOnes + 4096);                  // [kQCap][128]
+  uint32_t* q_col = reinterpret_cast<uint32_t*>(q_key + kQCap * 128);  // [kQCap][128]
+  uint8_t* sB = reinterpret_cast<uint8_t*>(q_col + kQCap * 128);    // NS stages of 32 KB
 
   if (kFold) {
     // constant A-side augment tile, [2 planes][128 rows][16 B]: row = (1, 1, 1, 0, ...) in bf16
@@ -114,7 +157,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar_a_full, 1);
     ptx::mbar_init(&bar_a_empty, 1);
-    for (int s = 0; s < kDtStages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       ptx::mbar_init(&bar_b_full[s], 1);
       ptx::mbar_init(&bar_b_empty[s], 1);
     }
@@ -150,8 +193,8 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
         for (int c0 = 0; c0 < ncols; c0 += 256) {
           const int Nt = min(256, (ncols - c0 + 31) & ~31);
           for (int ch = 0; ch < nchunks; ++ch, ++g) {
-            const int s = g % kDtStages;
-            const uint32_t ph = (g / kDtStages) & 1;
+            const int s = g % NS;
+            const uint32_t ph = (g / NS) & 1;
             if (!ptx::mbar_wait(&bar_b_empty[s], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
             const int kc0 = ch * 8, kc1 = min(KC, kc0 + 8);
             ptx::mbar_arrive_expect_tx(&bar_b_full[s], (uint32_t)((kc1 - kc0) * Nt * 16));
@@ -182,8 +225,8 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
           const uint32_t idesc = U8 ? ptx::idesc_u8_s32(128, Nt) : (ptx::idesc_bf16_f32(128, Nt) | (1u << 14));
           const uint32_t dtm = tmem + buf * 256;
           for (int ch = 0; ch < nchunks; ++ch, ++g) {
-            const int s = g % kDtStages;
-            const uint32_t ph = (g / kDtStages) & 1;
+            const int s = g % NS;
+            const uint32_t ph = (g / NS) & 1;
             if (!ptx::mbar_wait(&bar_b_full[s], ph, args.err, DERR_WAIT_TIMEOUT)) return;
             ptx::tc_fence_after();
             const int kc0 = ch * 8, kc1 = min(KC, kc0 + 8);
@@ -206,12 +249,17 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
     }();
   } else {
     // ------------------------------------------------------------ epilogue (4 warps, one row per thread)
+    // Per element: (u8) key = ||y||^2 - 2 acc, then append to the row's SMEM queue iff key < thr
+    // (predicated, no divergence). The queue is drained into the register top-K list — re-checking each
+    // entry against the (meanwhile tighter) threshold — whenever any lane of the warp might overflow it,
+    // while the list is not yet full, and at the end of the row. Appends happen in ascending column
+    // order and insertion is strict, so equal keys keep the smaller column (= smaller id), exactly.
     [&]() {
       const int q = warp & 3;
       const int tid = q * 32 + lane;  // = row within the 128-row block = TMEM lane
       const KT kInf = U8 ? (KT)0x7FFFFFFF : (KT)__int_as_float(0x7F800000);
-      KT* my_key = tk_key + tid;
-      uint32_t* my_col = tk_col + tid;
+      KT* my_qk = q_key + tid;
+      uint32_t* my_qc = q_col + tid;
       uint32_t tcount = 0;
       for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         const WorkItem w = args.items[it];
@@ -220,11 +268,15 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
         const int row = r0 + tid;
         const int K = S.k + (S.self ? 1 : 0);  // self exclusion: keep k+1, drop the row itself afterwards
         const int ncols = S.b.rows;
-        for (int t = 0; t < K; ++t) {
-          my_key[t * 128] = kInf;
-          my_col[t * 128] = 0xFFFFFFFFu;
+        KT kk[KMAX];
+        uint32_t ii[KMAX];
+#pragma unroll
+        for (int t = 0; t < KMAX; ++t) {
+          kk[t] = kInf;
+          ii[t] = 0xFFFFFFFFu;
         }
         KT thr = kInf;
+        int qlen = 0;
         const KT* nbp = U8 ? (const KT*)args.nb + S.b.pos : nullptr;
         for (int c0 = 0; c0 < ncols; c0 += 256, ++tcount) {
           const int Nt = min(256, (ncols - c0 + 31) & ~31);
@@ -255,42 +307,41 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
               if (U8) key = nbv[jj] - 2 * (int32_t)v[jj];
               else key = __uint_as_float(v[jj]);
               if (key < thr) {
-                // insertion into the sorted SMEM list (strict <: equal keys keep the smaller column)
-                int t = K - 1;
-                while (t > 0) {
-                  const KT prev = my_key[(t - 1) * 128];
-                  if (!(key < prev)) break;
-                  my_key[t * 128] = prev;
-                  my_col[t * 128] = my_col[(t - 1) * 128];
-                  --t;
-                }
-                my_key[t * 128] = key;
-                my_col[t * 128] = (uint32_t)(col0 + jj);
-                thr = my_key[(K - 1) * 128];
+                my_qk[qlen * 128] = key;
+                my_qc[qlen * 128] = (uint32_t)(col0 + jj);
+                ++qlen;
               }
             }
+            // warp-uniform drain decision: the queue could overflow on the next chunk, or the list is not
+            // full yet (then every chunk drains, which also makes the threshold finite quickly)
+            if (__any_sync(0xffffffffu, qlen > kQCap - 32 || (qlen > 0 && thr == kInf)))
+              topk_drain<KT, KMAX>(kk, ii, thr, qlen, my_qk, my_qc, K);
           }
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&bar_acc_empty[buf]);
         }
+        topk_drain<KT, KMAX>(kk, ii, thr, qlen, my_qk, my_qc, K);
         if (row < S.a.rows) {
           const int64_t obase = S.out_off + (int64_t)row * S.ostride;
           KT na = 0;
           if (!MIPS) na = ((const KT*)args.na)[S.a.pos + row];
           int o = 0;
-          for (int t = 0; t < K && o < S.k; ++t) {
-            const uint32_t col = my_col[t * 128];
-            if (S.self && col == (uint32_t)row) continue;
-            if (col == 0xFFFFFFFFu || col >= (uint32_t)ncols) break;
-            const KT key = my_key[t * 128];
-            float D;
-            if (MIPS) D = (float)key;
-            else if (U8) D = (float)(na + key);
-            else D = fmaxf(fmaf(2.0f, (float)key, (float)na), 0.0f);
-            args.out_idx[obase + o] = args.col_ids ? args.col_ids[S.b.id_off + col] : col;
-            if (args.out_dist) args.out_dist[obase + o] = D;
-            ++o;
+#pragma unroll
+          for (int t = 0; t < KMAX; ++t) {
+            const uint32_t col = ii[t];
+            const bool take = t < K && o < S.k && col != 0xFFFFFFFFu && col < (uint32_t)ncols &&
+                              !(S.self && col == (uint32_t)row);
+            if (take) {
+              const KT key = kk[t];
+              float D;
+              if (MIPS) D = (float)key;
+              else if (U8) D = (float)(na + key);
+              else D = fmaxf(fmaf(2.0f, (float)key, (float)na), 0.0f);
+              args.out_idx[obase + o] = args.col_ids ? args.col_ids[S.b.id_off + col] : col;
+              if (args.out_dist) args.out_dist[obase + o] = D;
+              ++o;
+            }
           }
           for (; o < S.ostride; ++o) {
             args.out_idx[obase + o] = 0xFFFFFFFFu;
