@@ -477,10 +477,11 @@ def test_beam_search_complete_graph_recall_one():
 
 @pytest.mark.slow
 def test_recall_quality_bar():
-    # S:537 scale-free quality bar (stand-in for Fig. 5): 100K x 64 clustered, defaults, 10@10 >= 0.95 at
-    # some L <= 100. Uses the SPEC defaults except k (bidirected k-NN with k=4 as the paper allows).
-    cfg = synth.Config("S537", n=100_000, d=64, dtype="f32", metric="l2", n_centres=1000, c_max=1024, k=4,
-                       n_queries=1000)
+    # S:537 scale-free quality bar (stand-in for Fig. 5): 100K x 64 clustered, default parameters, 10@10 >=
+    # 0.95 at some L <= 100. Defaults as SPEC states them: fanout [10, 3] ("10 on the top
+    # level, 3 on the second"), k = 2, l_max = 64, R = 64, alpha = 1.2.
+    cfg = synth.Config("S537", n=100_000, d=64, dtype="f32", metric="l2", n_centres=1000, c_max=1024,
+                       fanout=(10, 3), k=2, l_max=64, n_queries=1000)
     X = synth.gen_points(cfg)
     Q = synth.gen_queries(cfg)
     ds = O.Dataset(X, mode="exact")
@@ -489,3 +490,4 @@ def test_recall_quality_bar():
     e = O.entry_point(ds)
     res, _ = O.beam_search(ds, r.row_ptr, r.col_idx, Q, e, 100, 10)
     assert O.recall_at(res, truth).mean() >= 0.95
+    assert np.diff(r.row_ptr).max() <= 64  # degree cap
