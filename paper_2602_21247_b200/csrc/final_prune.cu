@@ -1,13 +1,14 @@
 // final_prune.cu — final RobustPrune of every reservoir and the CSR write-out (§4.3, P:568-570;
-// Alg. 2 P:227-248 in its lazy form P:938-942), one warp per point:
-//   1. candidates = the reservoir's ids; their vectors (and u's) are staged in shared memory with coalesced
-//      row loads (float rows as bf16, the path precision of DESIGN.md R19/R24), row stride padded by one
-//      word so lane-per-candidate reads are bank-conflict free;
-//   2. D(u, v) recomputed at path precision: exact integers for uint8 (|a-b| per byte + dp4a),
-//      fp32 on bf16 coordinates for float (direct form); bitonic sort by (D, v) (R4);
-//   3. the candidate Gram D(v_i, v_j) (lane per pair, from SMEM), then the lazy scan: admit c unless an
-//      admitted y has alpha_num*D(y,c) < alpha_den*D(u,c); stop at R (the lanes test the admitted set).
-//   Reservoirs with more than kFpStage candidates take a slow path (warp-cooperative distances from HBM).
+// Alg. 2 P:227-248 in its lazy form P:938-942), one warp per point u (fp_gram_kernel):
+//   1. rows = u and its c reservoir candidates, staged in shared memory (uint8 bytes, or the bf16 RNE
+//      coordinates of float rows: the path precision of DESIGN.md R19/R24);
+//   2. the (c+1)x(c+1) Gram on the tensor cores with warp-level MMAs (u8 x u8 -> s32, exact; bf16 -> f32),
+//      turned into D in place: D(r,s) = G_rr + G_ss - 2 G_rs (L2), -G_rs (MIPS);
+//   3. candidates sorted by (D(u,v), v) (R4); lazy scan: admit c unless an admitted y has
+//      alpha_num*D(y,c) < alpha_den*D(u,c); stop at R (lanes test the admitted set, one ballot per 32).
+//   Tiers by reservoir occupancy (<= 31, <= 63, <= 127 candidates; larger reservoirs take the generic
+//   final_prune_kernel), so the common case runs many warps per SM with small tiles.
+// final_prune = 0 (keep the R nearest reservoir entries) uses the generic kernel.
 // Then row_ptr = exclusive scan of the degrees and a coalesced copy into col_idx.
 #include <cub/cub.cuh>
 
@@ -329,6 +330,257 @@ __global__ void final_prune_kernel(const void* __restrict__ Xv, int64_t n, int d
   }
 }
 
+// ------------------------------------------------------------------ Gram path (tensor cores, warp per point)
+// Rows 0..c of a per-warp SMEM tile hold u (row 0) and its c reservoir candidates (rows 1..c), as u8 bytes or
+// bf16 coordinates, zero-padded to Kb bytes and to a multiple of 16 rows; the row pitch is Kb + 16 bytes so
+// the mma.sync fragment loads (8 rows x 4 consecutive words per instruction) are bank-conflict free. The
+// Gram G = V V^T comes from warp-level MMAs (m16n8k32 u8 x u8 -> s32, exact; m16n8k16 bf16 x bf16 -> f32),
+// then D(r, s) = G_rr + G_ss - 2 G_rs (L2; clamped at 0 for float) or -G_rs (MIPS) in place.
+// Both fragment layouts address the same bytes: one K-step = 32 bytes of every row.
+template <bool U8>
+__device__ __forceinline__ void mma_16x8(int32_t (&acc)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  if (U8) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+  } else {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(acc[0]), "+r"(acc[1]), "+r"(acc[2]), "+r"(acc[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+  }
+}
+
+struct GpLayout {
+  int Kb, pitch;  // bytes of a staged row (multiple of 32), SMEM row pitch (Kb + 16)
+  size_t rows_off, d_off, nrm_off, keys_off, perm_off, ids_off, adm_off, per_warp;
+};
+__host__ __device__ inline GpLayout gp_layout(int d, bool u8, int CP) {
+  GpLayout L;
+  L.Kb = u8 ? (d + 31) / 32 * 32 : (d + 15) / 16 * 32;
+  L.pitch = L.Kb + 16;
+  size_t o = 0;
+  L.rows_off = o;
+  o += (size_t)CP * L.pitch;
+  L.d_off = o;
+  o += (size_t)CP * (CP + 1) * 4;
+  L.nrm_off = o;
+  o += (size_t)CP * 4;
+  o = (o + 15) & ~(size_t)15;
+  L.keys_off = o;
+  o += (size_t)CP * 8;
+  L.perm_off = o;
+  o += (size_t)CP * 2;
+  L.ids_off = o;
+  o += (size_t)CP * 4;
+  L.adm_off = o;
+  o += (size_t)CP * 2;
+  L.per_warp = (o + 127) & ~(size_t)127;
+  return L;
+}
+
+// Stage rows ids[0..nr) into the tile as 16-B chunks (u8 bytes / bf16 RNE of the fp32 coordinates);
+// chunks beyond d are zero, rows nr..nrp-1 are zero. Up to 8 chunks in flight per lane.
+template <bool U8>
+__device__ __forceinline__ void gp_stage(const void* __restrict__ Xv, int64_t ld, int d, const uint32_t* ids, int nr,
+                                         int nrp, uint8_t* rows, const GpLayout& L, int lane) {
+  const int cpr = L.Kb >> 4;  // 16-B chunks per row
+  const int total = nrp * cpr;
+  const bool fast = U8 ? ((d & 15) == 0 && (ld & 15) == 0) : ((d & 7) == 0 && (ld & 3) == 0);
+  for (int e0 = 0; e0 < total; e0 += 256) {
+    uint4 v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = e0 + j * 32 + lane;
+      v[j] = make_uint4(0u, 0u, 0u, 0u);
+      if (e < total) {
+        const int r = e / cpr, ch = e - r * cpr;
+        if (r < nr) {
+          const int64_t id = ids[r];
+          if (U8) {
+            const uint8_t* src = (const uint8_t*)Xv + id * ld;
+            if (fast) {
+              if (ch * 16 < d) v[j] = __ldg((const uint4*)src + ch);
+            } else {
+              uint32_t w[4] = {0u, 0u, 0u, 0u};
+              for (int t = 0; t < 16; ++t)
+                if (ch * 16 + t < d) w[t >> 2] |= (uint32_t)src[ch * 16 + t] << (8 * (t & 3));
+              v[j] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          } else {
+            const float* src = (const float*)Xv + id * ld;
+            float f[8];
+            if (fast && ch * 8 < d) {
+              const float4 a = __ldg((const float4*)(src + ch * 8));
+              const float4 b = __ldg((const float4*)(src + ch * 8 + 4));
+              f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+            } else {
+#pragma unroll
+              for (int t = 0; t < 8; ++t) f[t] = (ch * 8 + t < d) ? __ldg(src + ch * 8 + t) : 0.0f;
+            }
+            uint32_t w[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              w[t] = (uint32_t)f32_to_bf16_rne(f[2 * t]) | ((uint32_t)f32_to_bf16_rne(f[2 * t + 1]) << 16);
+            v[j] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int e = e0 + j * 32 + lane;
+      if (e < total) {
+        const int r = e / cpr, ch = e - r * cpr;
+        *(uint4*)(rows + (size_t)r * L.pitch + ch * 16) = v[j];
+      }
+    }
+  }
+}
+
+// Pass over points (list == nullptr: all points) whose reservoir fits CP-1 candidates; larger ones are
+// appended to `defer` for the next tier. final_prune == 1 only (the R-nearest variant uses the generic kernel).
+template <bool U8, bool MIPS, int CP>
+__global__ void __launch_bounds__(256) fp_gram_kernel(const void* __restrict__ Xv, int64_t n, int d, int64_t ld,
+                                                      int l_max, const uint64_t* __restrict__ slots,
+                                                      const uint32_t* __restrict__ count, int R, int an, int ad,
+                                                      uint32_t* __restrict__ nbr_tmp, uint32_t* __restrict__ deg,
+                                                      const uint32_t* __restrict__ list,
+                                                      const uint32_t* __restrict__ list_n,
+                                                      uint32_t* __restrict__ defer, uint32_t* __restrict__ defer_n) {
+  using DT = typename std::conditional<U8, int32_t, float>::type;
+  extern __shared__ __align__(16) uint8_t gsm[];
+  const GpLayout L = gp_layout(d, U8, CP);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  uint8_t* base = gsm + (size_t)warp * L.per_warp;
+  uint8_t* rows = base + L.rows_off;
+  DT* Dm = (DT*)(base + L.d_off);  // [CP][CP + 1]
+  DT* nrm = (DT*)(base + L.nrm_off);
+  uint64_t* keys = (uint64_t*)(base + L.keys_off);
+  uint16_t* perm = (uint16_t*)(base + L.perm_off);
+  uint32_t* ids = (uint32_t*)(base + L.ids_off);
+  int16_t* adm = (int16_t*)(base + L.adm_off);
+  const int DS = CP + 1;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t n_iter = list ? (int64_t)*list_n : n;
+
+  for (int64_t it = (int64_t)blockIdx.x * wpb + warp; it < n_iter; it += (int64_t)gridDim.x * wpb) {
+    const int64_t u = list ? (int64_t)list[it] : it;
+    const int c = (int)count[u];
+    if (c > CP - 1) {
+      if (lane == 0) defer[atomicAdd(defer_n, 1u)] = (uint32_t)u;
+      continue;
+    }
+    uint32_t* out = nbr_tmp + u * (int64_t)R;
+    if (c == 0) {
+      if (lane == 0) deg[u] = 0;
+      continue;
+    }
+    const uint64_t* res = slots + u * (int64_t)l_max;
+    const int nr = c + 1, nrp = (nr + 15) & ~15;
+    for (int t = lane; t < nr; t += 32) ids[t] = t == 0 ? (uint32_t)u : (uint32_t)(res[t - 1] & 0xFFFFFFFFu);
+    __syncwarp();
+    gp_stage<U8>(Xv, ld, d, ids, nr, nrp, rows, L, lane);
+    __syncwarp();
+    // ---- Gram on tensor cores: 16-row blocks x 8-row blocks, K in 32-byte steps
+    const int nb16 = nrp >> 4, nb8 = nrp >> 3;
+    for (int bi = 0; bi < nb16; ++bi) {
+      int32_t acc[CP / 8][4];
+#pragma unroll
+      for (int bj = 0; bj < CP / 8; ++bj) acc[bj][0] = acc[bj][1] = acc[bj][2] = acc[bj][3] = 0;
+      const uint8_t* ra = rows + (size_t)(bi * 16 + g) * L.pitch + t4 * 4;
+      for (int kb = 0; kb < L.Kb; kb += 32) {
+        uint32_t a[4];
+        a[0] = *(const uint32_t*)(ra + kb);
+        a[1] = *(const uint32_t*)(ra + 8 * L.pitch + kb);
+        a[2] = *(const uint32_t*)(ra + kb + 16);
+        a[3] = *(const uint32_t*)(ra + 8 * L.pitch + kb + 16);
+#pragma unroll
+        for (int bj = 0; bj < CP / 8; ++bj) {
+          if (bj < nb8) {
+            const uint8_t* rb = rows + (size_t)(bj * 8 + g) * L.pitch + t4 * 4 + kb;
+            uint32_t b[2];
+            b[0] = *(const uint32_t*)rb;
+            b[1] = *(const uint32_t*)(rb + 16);
+            mma_16x8<U8>(acc[bj], a, b);
+          }
+        }
+      }
+#pragma unroll
+      for (int bj = 0; bj < CP / 8; ++bj) {
+        if (bj < nb8) {
+          const int r = bi * 16 + g, s = bj * 8 + 2 * t4;
+          DT* d0 = Dm + (size_t)r * DS + s;
+          DT* d1 = Dm + (size_t)(r + 8) * DS + s;
+          if (U8) {
+            d0[0] = acc[bj][0]; d0[1] = acc[bj][1]; d1[0] = acc[bj][2]; d1[1] = acc[bj][3];
+          } else {
+            d0[0] = __int_as_float(acc[bj][0]); d0[1] = __int_as_float(acc[bj][1]);
+            d1[0] = __int_as_float(acc[bj][2]); d1[1] = __int_as_float(acc[bj][3]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (!MIPS) {
+      for (int r = lane; r < nr; r += 32) nrm[r] = Dm[(size_t)r * DS + r];
+      __syncwarp();
+    }
+    for (int e = lane; e < nr * nr; e += 32) {
+      const int r = e / nr, s = e - r * nr;
+      DT* p = Dm + (size_t)r * DS + s;
+      if (MIPS) *p = -*p;
+      else if (U8) *p = nrm[r] + nrm[s] - 2 * *p;
+      else *p = fmaxf(nrm[r] + nrm[s] - 2.0f * *p, 0.0f);
+    }
+    // ---- candidates ascending by (D(u, v), v)
+    int P = 32;
+    while (P < c) P <<= 1;
+    __syncwarp();
+    for (int t = lane; t < P; t += 32) {
+      uint64_t key = ~0ull;
+      if (t < c) {
+        const DT Du = Dm[t + 1];
+        key = ((uint64_t)(U8 ? (uint32_t)Du : f_ord((float)Du)) << 32) | ids[t + 1];
+      }
+      keys[t] = key;
+      perm[t] = (uint16_t)(t + 1);
+    }
+    __syncwarp();
+    warp_sort_kv(keys, perm, P, lane);
+    // ---- lazy RobustPrune: admit c unless an admitted y has an*D(y,c) < ad*D(u,c); stop at R
+    int na = 0;
+    for (int i = 0; i < c && na < R; ++i) {
+      const int ri = perm[i];
+      const DT Dui = Dm[ri];
+      bool pr = false;
+      for (int a0 = 0; a0 < na && !pr; a0 += 32) {
+        bool mine = false;
+        if (a0 + lane < na) {
+          const DT Dyi = Dm[(size_t)adm[a0 + lane] * DS + ri];
+          if (U8) mine = (int64_t)an * (int64_t)Dyi < (int64_t)ad * (int64_t)Dui;
+          else mine = (float)an * (float)Dyi < (float)ad * (float)Dui;
+        }
+        pr = __any_sync(0xffffffffu, mine);
+      }
+      if (!pr) {
+        if (lane == 0) {
+          adm[na] = (int16_t)ri;
+          out[na] = ids[ri];
+        }
+        ++na;
+        __syncwarp();
+      }
+    }
+    if (lane == 0) deg[u] = (uint32_t)na;
+    __syncwarp();
+  }
+}
+
 __global__ void csr_copy_kernel(int64_t n, int R, const uint32_t* __restrict__ nbr_tmp, const uint32_t* __restrict__ deg,
                                 const uint64_t* __restrict__ row_ptr, uint32_t* __restrict__ col_idx) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -347,8 +599,8 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
   const int R = p->R;
   uint32_t* nbr_tmp = ar.take<uint32_t>((size_t)n * R);
   uint32_t* deg = ar.take<uint32_t>(n + 1);
-  uint32_t* defer = ar.take<uint32_t>(n);
-  uint32_t* defer_n = ar.take<uint32_t>(1);
+  uint32_t* defer = ar.take<uint32_t>((size_t)3 * n);
+  uint32_t* defer_n = ar.take<uint32_t>(4);
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const uint32_t*)nullptr, (uint64_t*)nullptr, (int)(n + 1));
   void* tmp = ar.take<uint8_t>(tmp_bytes);
@@ -356,36 +608,73 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
   if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (final_prune)");
   if (R > 256) return fail(PIPNN_EUNSUPPORTED, "R > 256");
   const bool u8 = X->dtype == PIPNN_U8, mips = X->metric == PIPNN_MIPS;
-  // pass 0: many warps, <= kFpStage staged candidates (Gram); pass 1: one warp per CTA, up to l_max rows
-  const FpLayout L0 = fp_layout(X->d, u8, l_max, kFpStage);
-  int wpb = 8;
-  while (wpb > 1 && (size_t)wpb * L0.per_warp > 96 * 1024) wpb >>= 1;
-  const size_t pair_bytes = (size_t)kFpStage * (kFpStage - 1) * 2;  // u16 (i, j) pairs
-  const int smem0 = (int)(wpb * L0.per_warp + pair_bytes);
+  PIPNN_CUDA(cudaMemsetAsync(deg + n, 0, sizeof(uint32_t), c.st));
+  PIPNN_CUDA(cudaMemsetAsync(defer_n, 0, 4 * sizeof(uint32_t), c.st));
+  const size_t pair_bytes = (size_t)kFpStage * (kFpStage - 1) * 2;  // u16 (i, j) pairs of the generic kernel
   int cap1 = l_max;
   FpLayout L1 = fp_layout(X->d, u8, l_max, cap1);
   while (cap1 > kFpStage && L1.per_warp + pair_bytes > 200 * 1024) L1 = fp_layout(X->d, u8, l_max, cap1 -= 16);
   const int smem1 = (int)(L1.per_warp + pair_bytes);
-  const int64_t blocks = std::min<int64_t>(ceil_div(n, wpb), (int64_t)num_sms() * 16);
-  PIPNN_CUDA(cudaMemsetAsync(deg + n, 0, sizeof(uint32_t), c.st));
-  PIPNN_CUDA(cudaMemsetAsync(defer_n, 0, sizeof(uint32_t), c.st));
+  if (p->final_prune) {
+    // tiers of the Gram path: <= 31, <= 63, <= 127 candidates; anything larger -> generic kernel
+    const uint32_t* in_list = nullptr;
+    const uint32_t* in_n = nullptr;
+#define GP_TIER(U, M, CPV, T)                                                                                      \
+  do {                                                                                                             \
+    const GpLayout GL = gp_layout(X->d, U, CPV);                                                                   \
+    int w = (int)std::min<size_t>(8, (200 * 1024) / GL.per_warp);                                                  \
+    if (w < 1) return fail(PIPNN_EUNSUPPORTED, "final prune: row too large for the Gram tile");                   \
+    const int sm = (int)(w * GL.per_warp);                                                                         \
+    auto* fn = fp_gram_kernel<U, M, CPV>;                                                                          \
+    PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));                         \
+    const int64_t blocks = in_list ? (int64_t)num_sms() * 4 : std::min<int64_t>(ceil_div(n, w), num_sms() * 32);   \
+    fn<<<(unsigned)blocks, 32 * w, sm, c.st>>>(X->data, n, X->d, X->ld, l_max, slots, count, R, p->alpha_num,      \
+                                               p->alpha_den, nbr_tmp, deg, in_list, in_n, defer + (T) * n,        \
+                                               defer_n + (T));                                                     \
+    PIPNN_LAUNCHED("fp_gram_kernel", c.st);                                                                        \
+    in_list = defer + (T) * n;                                                                                     \
+    in_n = defer_n + (T);                                                                                          \
+  } while (0)
+#define GP_ALL(U, M)                                                                                               \
+  do {                                                                                                             \
+    GP_TIER(U, M, 32, 0);                                                                                          \
+    if (l_max > 31) GP_TIER(U, M, 64, 1);                                                                          \
+    if (l_max > 63) GP_TIER(U, M, 128, 2);                                                                         \
+    if (l_max > 127) {                                                                                             \
+      auto* fn = final_prune_kernel<U, M>;                                                                         \
+      PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));                    \
+      fn<<<(unsigned)(num_sms() * 2), 32, smem1, c.st>>>(X->data, n, X->d, X->ld, l_max, slots, count, R,          \
+                                                        p->alpha_num, p->alpha_den, 1, nbr_tmp, deg, cap1, in_list, \
+                                                        in_n, nullptr, nullptr);                                    \
+      PIPNN_LAUNCHED("final_prune_kernel(generic)", c.st);                                                         \
+    }                                                                                                              \
+  } while (0)
+    if (u8) GP_ALL(true, false);
+    else if (mips) GP_ALL(false, true);
+    else GP_ALL(false, false);
+#undef GP_ALL
+#undef GP_TIER
+  } else {
+    // final_prune = 0: the R nearest reservoir entries, generic kernel
+    const FpLayout L0 = fp_layout(X->d, u8, l_max, kFpStage);
+    int wpb = 8;
+    while (wpb > 1 && (size_t)wpb * L0.per_warp > 96 * 1024) wpb >>= 1;
+    const int smem0 = (int)(wpb * L0.per_warp + pair_bytes);
+    const int64_t blocks = std::min<int64_t>(ceil_div(n, wpb), (int64_t)num_sms() * 16);
 #define FP_LAUNCH(U, M)                                                                                            \
   do {                                                                                                             \
     auto* fn = final_prune_kernel<U, M>;                                                                           \
     PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(smem0, smem1)));      \
     fn<<<(unsigned)blocks, 32 * wpb, smem0, c.st>>>(X->data, n, X->d, X->ld, l_max, slots, count, R, p->alpha_num,  \
-                                                    p->alpha_den, p->final_prune, nbr_tmp, deg, kFpStage, nullptr,  \
-                                                    nullptr, defer, defer_n);                                       \
+                                                    p->alpha_den, 0, nbr_tmp, deg, kFpStage, nullptr, nullptr,      \
+                                                    nullptr, nullptr);                                              \
     PIPNN_LAUNCHED("final_prune_kernel", c.st);                                                                    \
-    fn<<<(unsigned)(num_sms() * 2), 32, smem1, c.st>>>(X->data, n, X->d, X->ld, l_max, slots, count, R,            \
-                                                      p->alpha_num, p->alpha_den, p->final_prune, nbr_tmp, deg,     \
-                                                      cap1, defer, defer_n, nullptr, nullptr);                      \
-    PIPNN_LAUNCHED("final_prune_kernel(deferred)", c.st);                                                          \
   } while (0)
-  if (u8) FP_LAUNCH(true, false);
-  else if (mips) FP_LAUNCH(false, true);
-  else FP_LAUNCH(false, false);
+    if (u8) FP_LAUNCH(true, false);
+    else if (mips) FP_LAUNCH(false, true);
+    else FP_LAUNCH(false, false);
 #undef FP_LAUNCH
+  }
   PIPNN_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, deg, row_ptr, (int)(n + 1), c.st));
   csr_copy_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 8), num_sms() * 32), 256, 0, c.st>>>(n, R, nbr_tmp, deg,
                                                                                                  row_ptr, col_idx);

@@ -15,14 +15,25 @@ __global__ void hyperplane_kernel(int m, int d, uint64_t seed, int8_t* __restric
   H[e] = (int8_t)v;
 }
 
-// One thread per point; H in shared memory. uint8: exact int32. float: the bf16-rounded coordinates
-// accumulated in fp64 in ascending j order, then rounded to fp32 (so the value is deterministic and
-// reproducible by any in-order fp64 implementation; reading R8).
+// One thread per point; H in shared memory (uint8: packed as 32-bit words of 4 int8, read by broadcast).
+// uint8: exact int32 — 4 coordinates per dp4a (s8 x u8), the row read with 16-B loads when aligned.
+// float: the bf16-rounded coordinates accumulated in fp64 in ascending j order, then rounded to fp32 (so the
+// value is deterministic and reproducible by any in-order fp64 implementation; reading R8).
+__device__ __forceinline__ int32_t dp4a_su(uint32_t h_s8x4, uint32_t x_u8x4, int32_t acc) {
+  int32_t r;
+  asm("dp4a.s32.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(h_s8x4), "r"(x_u8x4), "r"(acc));
+  return r;
+}
+
 template <bool U8>
 __global__ void __launch_bounds__(128) sketch_kernel(const void* __restrict__ Xv, int64_t n, int d, int64_t ld, int m,
                                                      const int8_t* __restrict__ Hg, void* __restrict__ S) {
-  extern __shared__ int8_t Hs[];
-  for (int e = threadIdx.x; e < m * d; e += blockDim.x) Hs[e] = Hg[e];
+  extern __shared__ __align__(16) int8_t Hs[];  // [m][dp] with dp = round_up(d, 16), zero padded
+  const int dp = (d + 15) & ~15;
+  for (int e = threadIdx.x; e < m * dp; e += blockDim.x) {
+    const int i = e / dp, j = e - i * dp;
+    Hs[e] = j < d ? Hg[i * d + j] : (int8_t)0;
+  }
   __syncthreads();
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (x >= n) return;
@@ -31,11 +42,34 @@ __global__ void __launch_bounds__(128) sketch_kernel(const void* __restrict__ Xv
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i] = 0;
     const uint8_t* row = (const uint8_t*)Xv + x * ld;
-    for (int j = 0; j < d; ++j) {
-      const int v = row[j];
+    const bool vec = ((d & 15) == 0) && ((ld & 15) == 0);
+    for (int j0 = 0; j0 < dp; j0 += 16) {
+      uint32_t w[4];
+      if (vec) {
+        const uint4 q = __ldg((const uint4*)(row + j0));
+        w[0] = q.x; w[1] = q.y; w[2] = q.z; w[3] = q.w;
+      } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (i < m) acc[i] += (int)Hs[i * d + j] * v;
+        for (int t = 0; t < 4; ++t) {
+          uint32_t v = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int j = j0 + 4 * t + b;
+            if (j < d) v |= (uint32_t)row[j] << (8 * b);
+          }
+          w[t] = v;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i < m) {
+          const uint4 h = *(const uint4*)(Hs + i * dp + j0);
+          acc[i] = dp4a_su(h.x, w[0], acc[i]);
+          acc[i] = dp4a_su(h.y, w[1], acc[i]);
+          acc[i] = dp4a_su(h.z, w[2], acc[i]);
+          acc[i] = dp4a_su(h.w, w[3], acc[i]);
+        }
+      }
     }
     int32_t* out = (int32_t*)S + x * m;
     for (int i = 0; i < m; ++i) out[i] = acc[i];
@@ -44,11 +78,23 @@ __global__ void __launch_bounds__(128) sketch_kernel(const void* __restrict__ Xv
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i] = 0.0;
     const float* row = (const float*)Xv + x * ld;
-    for (int j = 0; j < d; ++j) {
-      const double v = (double)__uint_as_float((uint32_t)f32_to_bf16_rne(row[j]) << 16);
+    const bool vec = ((d & 3) == 0) && ((ld & 3) == 0);
+    for (int j0 = 0; j0 < d; j0 += 4) {
+      float f[4];
+      if (vec) {
+        const float4 q = __ldg((const float4*)(row + j0));
+        f[0] = q.x; f[1] = q.y; f[2] = q.z; f[3] = q.w;
+      } else {
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (i < m) acc[i] += (double)Hs[i * d + j] * v;
+        for (int t = 0; t < 4; ++t) f[t] = j0 + t < d ? row[j0 + t] : 0.0f;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const double v = (double)__uint_as_float((uint32_t)f32_to_bf16_rne(f[t]) << 16);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (i < m) acc[i] += (double)Hs[i * dp + j0 + t] * v;
+      }
     }
     float* out = (float*)S + x * m;
     for (int i = 0; i < m; ++i) out[i] = (float)acc[i];
@@ -62,7 +108,7 @@ pipnn_status sketch_impl(const pipnn_points* X, int m, uint64_t seed, void* sket
   const int64_t md = (int64_t)m * X->d;
   hyperplane_kernel<<<(unsigned)ceil_div(md, 256), 256, 0, c.st>>>(m, X->d, seed, H);
   PIPNN_LAUNCHED("hyperplane_kernel", c.st);
-  const int smem = (int)md;
+  const int smem = (int)((int64_t)m * ((X->d + 15) & ~15));
   if (X->dtype == PIPNN_U8) {
     if (smem > 48 * 1024)
       PIPNN_CUDA(cudaFuncSetAttribute(sketch_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
