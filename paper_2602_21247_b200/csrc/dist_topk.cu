@@ -15,16 +15,18 @@ static pipnn_status launch_one(const DistTopkArgs& a, cudaStream_t st) {
 
 template <bool U8, bool MIPS>
 static pipnn_status launch_k(const DistTopkArgs& a, int kmax, cudaStream_t st) {
+  if (kmax <= 2) return launch_one<U8, MIPS, 2>(a, st);
   if (kmax <= 4) return launch_one<U8, MIPS, 4>(a, st);
+  if (kmax <= 8) return launch_one<U8, MIPS, 8>(a, st);
   if (kmax <= 12) return launch_one<U8, MIPS, 12>(a, st);
   return launch_one<U8, MIPS, 16>(a, st);
 }
 
-// kmax: the largest running-list length any segment needs (k + 1 with self exclusion).
+// kmax: the largest k any segment asks for (self exclusion does not need an extra slot).
 pipnn_status launch_dist_topk(const DistTopkArgs& a, bool u8, bool mips, int kmax, cudaStream_t st) {
   if (a.Kb <= 0 || a.Kb % 32 != 0 || a.Kb > 512)
     return fail(PIPNN_EUNSUPPORTED, "dist_topk: row bytes must be a multiple of 32 and <= 512");
-  if (kmax > kTopkMax) return fail(PIPNN_EUNSUPPORTED, "dist_topk: k too large (k+1 <= 16 with self exclusion)");
+  if (kmax > kTopkMax) return fail(PIPNN_EUNSUPPORTED, "dist_topk: k too large (<= 16)");
   if (u8 && mips) return fail(PIPNN_EINVAL, "uint8 + MIPS unsupported");
   if (u8) return launch_k<true, false>(a, kmax, st);
   if (mips) return launch_k<false, true>(a, kmax, st);

@@ -10,19 +10,25 @@
 // Output D = ||x_i||^2 + key (u8), max(0, ||x_i||^2 + 2 key) (float L2), key (MIPS).
 //
 // Blackwell mapping:
-//   * persistent grid, one CTA per SM, 6 warps: warp 0 = bulk-copy producer, warp 1 = tcgen05.mma
-//     issuer (+ TMEM owner), warps 2-5 = epilogue (warp w reads TMEM lanes 32*(w%4)..+31 = its rows);
-//   * work item = (segment, 128-row block); the A block (128 rows x K) stays in SMEM for the item, B
-//     column tiles of <= 256 rows (multiple of 32) stream through a 4-stage ring of 32 KB K-chunks;
-//   * operands in the K-major SWIZZLE_NONE canonical layout, produced directly by the gather kernel
-//     ("tiled rows": [K/16][rows][16 B] per segment), so each K-chunk plane is one contiguous bulk copy;
+//   * persistent grid, one CTA per SM, 10 warps: warp 0 = bulk-copy producer, warp 1 = tcgen05.mma issuer
+//     (+ TMEM owner), warps 2-9 = two epilogue warpgroups. Work item = (segment, 128-row block); the CTA's
+//     items alternate between the two warpgroups, so each epilogue thread owns one row of its item for
+//     the whole item (its running top-K never leaves registers, no cross-thread merge);
+//   * a tile = 128 rows x <= 128 columns; the MMA warp issues the two warpgroups' tiles round-robin into
+//     four 128-column TMEM accumulators (two per warpgroup), so the MMA of a warpgroup's next tile overlaps
+//     the epilogue of its current one, and the two warpgroups hide each other's latencies;
+//   * every K-chunk (<= 128 B of every row) of a tile's A rows and B rows arrives by 1-D bulk copies (cp.async.bulk, TMA engine) into a 4-stage SMEM ring with mbarrier
+//     transaction counts; operands are in the K-major SWIZZLE_NONE canonical layout produced directly by
+//     the gather kernel ("tiled rows": [K/16][rows][16 B] per segment), so each plane slice is one copy;
 //   * uint8: tcgen05.mma kind::i8 (u8 x u8 -> s32, exact). float: kind::f16 (bf16 x bf16 -> f32) with the
 //     B operand negated (instruction-descriptor bit) and one extra K-step that adds the column term
 //     ||y||^2/2 (split over three bf16 values; padding rows carry +1e30): A-side ones come from a
-//     constant SMEM tile, so the epilogue does no arithmetic per element — compare and (rarely) insert;
-//   * accumulators: two 128x256 32-bit TMEM buffers (all 512 columns) so the MMA of tile t+1 overlaps
-//     the epilogue of tile t; each row's running top-(k+1) lives in SMEM with its threshold in a register;
-//     the distance tile is never written to memory.
+//     constant SMEM tile, so the epilogue does no arithmetic per element;
+//   * epilogue per 32-column chunk (tcgen05.ld 32x32b.x32, one row per thread): key, compare with the
+//     row's threshold (the K-th best so far) into a 32-bit pass mask; if any lane passed, the keys are
+//     staged in SMEM and the passing (key, column) pairs appended to the row's SMEM queue; the queue is
+//     drained into the sorted register list (insertion) when it could overflow, while the list is not
+//     full, and at the row's end. The distance tile is never written to memory.
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -70,98 +76,135 @@ struct DistTopkArgs {
   int* err;
 };
 
-constexpr int kDtMaxStages = 4;
-constexpr int kDtStageBytes = 256 * 128;  // 256 rows x 128 B of K
-constexpr int kDtThreads = 192;
-constexpr int kTopkMax = 16;              // max entries of a row's running list (k+1 with self exclusion)
-constexpr int kQCap = 64;                 // per-row candidate queue (SMEM) between drains
-constexpr int32_t kPadNormU8 = 0x3FFFFFFF; // norm of a padding row: key far above any real key
-constexpr float kPadKey = 1e30f;           // float: column term of a padding row
+constexpr int kDtStages = 4;
+constexpr int kDtTileN = 128;                       // columns per tile (one TMEM accumulator)
+constexpr int kDtChunkB = 128;                      // bytes of K per stage and row
+constexpr int kDtAB = 128 * kDtChunkB;              // A (or B) bytes of one stage
+constexpr int kDtStageBytes = 2 * kDtAB;                 // A chunk + B chunk
+constexpr int kDtThreads = 320;
+constexpr int kTopkMax = 16;                        // max K (k, or the partition fanout)
+constexpr int kQCap = 32;                           // per-row candidate queue (SMEM) between drains
+constexpr int kStgPitch = 36;                       // words per row of the key staging tile
+constexpr int32_t kPadNormU8 = 0x3FFFFFFF;          // norm of a padding row: key far above any real key
+constexpr float kPadKey = 1e30f;                    // float: column term of a padding row
 
-__host__ __device__ constexpr int dt_fixed_smem(int Kb) { return 128 * Kb + 4096 /*ones*/ + kQCap * 128 * 8 /*queues*/; }
-__host__ __device__ constexpr int dt_stages(int Kb) {
-  return (227 * 1024 - 2048 - dt_fixed_smem(Kb)) / kDtStageBytes >= kDtMaxStages
-             ? kDtMaxStages
-             : (227 * 1024 - 2048 - dt_fixed_smem(Kb)) / kDtStageBytes;
+// dynamic SMEM: ring | per-warpgroup key staging [128][kStgPitch] | queues key [kQCap][128], col u16 [kQCap][128]
+constexpr int kDtRingBytes = kDtStages * kDtStageBytes;
+constexpr int kDtStgBytes = 128 * kStgPitch * 4;
+constexpr int kDtQBytes = kQCap * 128 * 6;
+__host__ __device__ constexpr int dt_smem_bytes(int /*Kb*/) {
+  return kDtRingBytes + 2 * kDtStgBytes + 2 * kDtQBytes + 4096 /*ones*/;
 }
-__host__ __device__ constexpr int dt_smem_bytes(int Kb) { return dt_fixed_smem(Kb) + dt_stages(Kb) * kDtStageBytes; }
 
-// Register top-K list (sorted ascending by (key, col)); insert requires key < kk[K-1] for the runtime K.
+// Sorted insertion into a register list (ascending; equal keys keep the earlier entry first).
+// Precondition: key < kk[KMAX-1].
 template <typename KT, int KMAX>
-__device__ __forceinline__ void topk_insert(KT (&kk)[KMAX], uint32_t (&ii)[KMAX], KT key, uint32_t col) {
+__device__ __forceinline__ void topk_insert(KT (&kk)[KMAX], uint16_t (&ii)[KMAX], KT key, uint32_t col) {
+  bool lt[KMAX];
 #pragma unroll
-  for (int t = KMAX - 1; t >= 0; --t) {
-    if (t > 0 && key < kk[t - 1]) {
-      kk[t] = kk[t - 1];
-      ii[t] = ii[t - 1];
-    } else if (key < kk[t]) {
-      kk[t] = key;
-      ii[t] = col;
-    }
+  for (int t = 0; t < KMAX; ++t) lt[t] = key < kk[t];
+  // keys: kk'[t] = max(kk[t-1], min(kk[t], key)) (no NaN can occur). The equivalent nested select
+  // lt[t-1] ? kk[t-1] : (lt[t] ? key : kk[t]) is miscompiled for float lists by nvcc 12.9 (sm_100a):
+  // the last slot keeps its old value (reproduced with a 4-slot standalone kernel).
+#pragma unroll
+  for (int t = KMAX - 1; t > 0; --t) {
+    if (std::is_same<KT, float>::value) kk[t] = (KT)fmaxf((float)kk[t - 1], fminf((float)kk[t], (float)key));
+    else kk[t] = max(kk[t - 1], min(kk[t], key));
+    ii[t] = lt[t - 1] ? ii[t - 1] : (lt[t] ? (uint16_t)col : ii[t]);
+  }
+  if (lt[0]) {
+    kk[0] = key;
+    ii[0] = (uint16_t)col;
   }
 }
-template <typename KT, int KMAX>
-__device__ __forceinline__ KT topk_kth(const KT (&kk)[KMAX], int K) {
-  KT r = kk[0];
-#pragma unroll
-  for (int t = 1; t < KMAX; ++t)
-    if (t == K - 1) r = kk[t];
-  return r;
-}
 
-// Drain a row's SMEM candidate queue (stride 128 words) into its register list.
+// Drain a row's SMEM queue (stride 128 entries) into its register list.
 template <typename KT, int KMAX>
-__device__ __forceinline__ void topk_drain(KT (&kk)[KMAX], uint32_t (&ii)[KMAX], KT& thr, int& qlen,
-                                           const KT* qk, const uint32_t* qc, int K) {
+__device__ __forceinline__ void topk_drain(KT (&kk)[KMAX], uint16_t (&ii)[KMAX], int& qlen, const KT* qk,
+                                           const uint16_t* qc) {
   for (int e = 0; e < qlen; ++e) {
     const KT key = qk[e * 128];
-    if (key < thr) {
-      topk_insert<KT, KMAX>(kk, ii, key, qc[e * 128]);
-      thr = topk_kth<KT, KMAX>(kk, K);
-    }
+    if (key < kk[KMAX - 1]) topk_insert<KT, KMAX>(kk, ii, key, qc[e * 128]);
   }
   qlen = 0;
 }
+
+// The deterministic tile schedule shared by the producer and the MMA warp: the CTA's items
+// it_j = blockIdx.x + j * gridDim.x go to warpgroup j & 1; tiles are issued round-robin between the two
+// warpgroups' current items (a warpgroup with no items left is skipped).
+struct TileSched {
+  int64_t it[2];
+  int tile[2], ntiles[2];
+  int w;
+  int64_t n_items;
+  __device__ __forceinline__ int ntiles_of(const DistTopkArgs& a, int64_t item) const {
+    const WorkItem wi = a.items[item];
+    return (a.segs[wi.seg].b.rows + kDtTileN - 1) / kDtTileN;
+  }
+  __device__ __forceinline__ void init(const DistTopkArgs& a, int64_t n) {
+    n_items = n;
+    for (int g = 0; g < 2; ++g) {
+      it[g] = (int64_t)blockIdx.x + (int64_t)g * gridDim.x;
+      tile[g] = 0;
+      ntiles[g] = it[g] < n ? ntiles_of(a, it[g]) : 0;
+    }
+    w = 0;
+  }
+  // next tile: returns false when both warpgroups are done
+  __device__ __forceinline__ bool next(int& g, int64_t& item, int& t) {
+    if (it[w] >= n_items) {
+      w ^= 1;
+      if (it[w] >= n_items) return false;
+    }
+    g = w;
+    item = it[w];
+    t = tile[w];
+    return true;
+  }
+  __device__ __forceinline__ void advance(const DistTopkArgs& a) {
+    if (++tile[w] == ntiles[w]) {
+      it[w] += 2 * (int64_t)gridDim.x;
+      tile[w] = 0;
+      ntiles[w] = it[w] < n_items ? ntiles_of(a, it[w]) : 0;
+    }
+    w ^= 1;
+  }
+};
 
 template <bool U8, bool MIPS, int KMAX>
 __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopkArgs args) {
   using KT = typename std::conditional<U8, int32_t, float>::type;
   constexpr bool kFold = !U8;  // float paths fold the column term into an augmented MMA K-step
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bar_a_full, bar_a_empty;
-  __shared__ __align__(8) uint64_t bar_b_full[kDtMaxStages], bar_b_empty[kDtMaxStages];
-  __shared__ __align__(8) uint64_t bar_acc_full[2], bar_acc_empty[2];
+  __shared__ __align__(8) uint64_t bar_full[kDtStages], bar_empty[kDtStages];
+  __shared__ __align__(8) uint64_t bar_acc_full[4], bar_acc_empty[4];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int Kb = args.Kb;
-  const int KC = Kb >> 4;                   // 16-B K planes per row (incl. the 2 augment planes for float)
-  const int KCm = kFold ? KC - 2 : KC;      // planes of the coordinates themselves
-  const int nchunks = (KC + 7) >> 3;
-  const int NS = dt_stages(Kb);
-  uint8_t* sA = smem;
-  uint8_t* sOnes = smem + 128 * Kb;
-  KT* q_key = reinterpret_cast<KT*>(sOnes + 4096);                  // [kQCap][128]
-  uint32_t* q_col = reinterpret_cast<uint32_t*>(q_key + kQCap * 128);  // [kQCap][128]
-  uint8_t* sB = reinterpret_cast<uint8_t*>(q_col + kQCap * 128);    // NS stages of 32 KB
+  const int KC = Kb >> 4;                // 16-B K planes per row (incl. the 2 augment planes for float)
+  const int KCm = kFold ? KC - 2 : KC;   // planes of the coordinates themselves
+  const int nchunks = (KC + 7) >> 3;     // K-chunks of <= 8 planes (128 B) per tile
+  uint8_t* ring = smem;
+  uint8_t* stg_base = smem + kDtRingBytes;
+  uint8_t* q_base = stg_base + 2 * kDtStgBytes;
+  uint8_t* sOnes = q_base + 2 * kDtQBytes;  // float: [2 planes][128 rows][16 B] A-side augment
 
   if (kFold) {
-    // constant A-side augment tile, [2 planes][128 rows][16 B]: row = (1, 1, 1, 0, ...) in bf16
+    // constant A-side augment tile: row = (1, 1, 1, 0, ...) in bf16
     for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
-      const int plane = e >> 9, r = (e >> 2) & 127, w = e & 3;
-      reinterpret_cast<uint32_t*>(sOnes)[(plane * 128 + r) * 4 + w] =
+      const int plane = e >> 9, w = e & 3;
+      reinterpret_cast<uint32_t*>(sOnes)[e] =
           (plane == 0 && w == 0) ? 0x3F803F80u : ((plane == 0 && w == 1) ? 0x00003F80u : 0u);
     }
     ptx::fence_proxy_async_smem();
   }
   if (threadIdx.x == 0) {
-    ptx::mbar_init(&bar_a_full, 1);
-    ptx::mbar_init(&bar_a_empty, 1);
-    for (int s = 0; s < NS; ++s) {
-      ptx::mbar_init(&bar_b_full[s], 1);
-      ptx::mbar_init(&bar_b_empty[s], 1);
+    for (int s = 0; s < kDtStages; ++s) {
+      ptx::mbar_init(&bar_full[s], 1);
+      ptx::mbar_init(&bar_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 4; ++b) {
       ptx::mbar_init(&bar_acc_full[b], 1);
       ptx::mbar_init(&bar_acc_empty[b], 4);
     }
@@ -177,151 +220,187 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
   if (warp == 0) {
     // ------------------------------------------------------------ producer (one lane)
     if (lane == 0) [&]() {
+      TileSched sc;
+      sc.init(args, n_items);
       uint32_t g = 0;
-      int64_t i = 0;
-      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++i) {
-        const WorkItem w = args.items[it];
+      int gi;
+      int64_t item;
+      int t;
+      while (sc.next(gi, item, t)) {
+        const WorkItem w = args.items[item];
         const DistSeg S = args.segs[w.seg];
-        const int r0 = w.rb * 128;
-        if (!ptx::mbar_wait(&bar_a_empty, (uint32_t)(i & 1) ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
-        ptx::mbar_arrive_expect_tx(&bar_a_full, 2048u * KCm);
+        const int r0 = w.rb * 128, c0 = t * kDtTileN;
+        const int Nt = min(kDtTileN, (S.b.rows - c0 + 31) & ~31);
         const uint8_t* srcA = args.Ta + S.a.pos * Kb + (int64_t)r0 * 16;
-        for (int kc = 0; kc < KCm; ++kc)
-          ptx::bulk_g2s(sA + kc * 2048, srcA + (int64_t)kc * S.a.pad * 16, 2048, &bar_a_full);
-        const int ncols = S.b.rows;
-        const uint8_t* baseB = args.Tb + S.b.pos * Kb;
-        for (int c0 = 0; c0 < ncols; c0 += 256) {
-          const int Nt = min(256, (ncols - c0 + 31) & ~31);
-          for (int ch = 0; ch < nchunks; ++ch, ++g) {
-            const int s = g % NS;
-            const uint32_t ph = (g / NS) & 1;
-            if (!ptx::mbar_wait(&bar_b_empty[s], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
-            const int kc0 = ch * 8, kc1 = min(KC, kc0 + 8);
-            ptx::mbar_arrive_expect_tx(&bar_b_full[s], (uint32_t)((kc1 - kc0) * Nt * 16));
-            uint8_t* dst = sB + s * kDtStageBytes;
-            for (int kc = kc0; kc < kc1; ++kc)
-              ptx::bulk_g2s(dst + (kc - kc0) * Nt * 16, baseB + ((int64_t)kc * S.b.pad + c0) * 16, Nt * 16,
-                            &bar_b_full[s]);
-          }
+        const uint8_t* srcB = args.Tb + S.b.pos * Kb + (int64_t)c0 * 16;
+        for (int ch = 0; ch < nchunks; ++ch, ++g) {
+          const int s = g % kDtStages;
+          const uint32_t ph = (g / kDtStages) & 1;
+          if (!ptx::mbar_wait(&bar_empty[s], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
+          const int kc0 = ch * 8, kc1 = min(KC, kc0 + 8), ka1 = min(KCm, kc1);
+          const int na = max(0, ka1 - kc0);
+          ptx::mbar_arrive_expect_tx(&bar_full[s], (uint32_t)(na * 2048 + (kc1 - kc0) * Nt * 16));
+          uint8_t* st = ring + s * kDtStageBytes;
+          for (int kc = kc0; kc < ka1; ++kc)
+            ptx::bulk_g2s(st + (kc - kc0) * 2048, srcA + (int64_t)kc * S.a.pad * 16, 2048, &bar_full[s]);
+          for (int kc = kc0; kc < kc1; ++kc)
+            ptx::bulk_g2s(st + kDtAB + (kc - kc0) * Nt * 16, srcB + (int64_t)kc * S.b.pad * 16, Nt * 16,
+                          &bar_full[s]);
         }
+        sc.advance(args);
       }
     }();
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (one lane)
     if (lane == 0) [&]() {
-      uint32_t g = 0, tcount = 0;
-      int64_t i = 0;
-      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++i) {
-        const WorkItem w = args.items[it];
+      TileSched sc;
+      sc.init(args, n_items);
+      uint32_t g = 0;
+      uint32_t tc[2] = {0u, 0u};  // tiles issued per warpgroup
+      int gi;
+      int64_t item;
+      int t;
+      while (sc.next(gi, item, t)) {
+        const WorkItem w = args.items[item];
         const int ncols = args.segs[w.seg].b.rows;
-        if (!ptx::mbar_wait(&bar_a_full, (uint32_t)(i & 1), args.err, DERR_WAIT_TIMEOUT)) return;
+        const int c0 = t * kDtTileN;
+        const int Nt = min(kDtTileN, (ncols - c0 + 31) & ~31);
+        const uint32_t buf = 2 * gi + (tc[gi] & 1), use = tc[gi] >> 1;
+        ++tc[gi];
+        if (!ptx::mbar_wait(&bar_acc_empty[buf], (use & 1) ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
         ptx::tc_fence_after();
-        for (int c0 = 0; c0 < ncols; c0 += 256, ++tcount) {
-          const int Nt = min(256, (ncols - c0 + 31) & ~31);
-          const uint32_t buf = tcount & 1, use = tcount >> 1;
-          if (!ptx::mbar_wait(&bar_acc_empty[buf], (use & 1) ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
+        // float: negate B (bit 14), so the accumulator is -x.y + (column term)
+        const uint32_t idesc = U8 ? ptx::idesc_u8_s32(128, Nt) : (ptx::idesc_bf16_f32(128, Nt) | (1u << 14));
+        const uint32_t dtm = tmem + buf * kDtTileN;
+        for (int ch = 0; ch < nchunks; ++ch, ++g) {
+          const int s = g % kDtStages;
+          const uint32_t ph = (g / kDtStages) & 1;
+          if (!ptx::mbar_wait(&bar_full[s], ph, args.err, DERR_WAIT_TIMEOUT)) return;
           ptx::tc_fence_after();
-          // float: negate B (bit 14), so the accumulator is -x.y + (column term)
-          const uint32_t idesc = U8 ? ptx::idesc_u8_s32(128, Nt) : (ptx::idesc_bf16_f32(128, Nt) | (1u << 14));
-          const uint32_t dtm = tmem + buf * 256;
-          for (int ch = 0; ch < nchunks; ++ch, ++g) {
-            const int s = g % NS;
-            const uint32_t ph = (g / NS) & 1;
-            if (!ptx::mbar_wait(&bar_b_full[s], ph, args.err, DERR_WAIT_TIMEOUT)) return;
-            ptx::tc_fence_after();
-            const int kc0 = ch * 8, kc1 = min(KC, kc0 + 8);
-            const uint8_t* sb = sB + s * kDtStageBytes;
-            for (int kc = kc0; kc < kc1; kc += 2) {
-              const uint8_t* a_src = (kFold && kc >= KCm) ? sOnes + (kc - KCm) * 2048 : sA + kc * 2048;
-              const uint64_t ad = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(a_src), 2048, 128);
-              const uint64_t bd =
-                  ptx::smem_desc_kmajor_noswz(ptx::smem_u32(sb + (kc - kc0) * Nt * 16), (uint32_t)Nt * 16, 128);
-              const uint32_t acc = (ch > 0 || kc > kc0) ? 1u : 0u;
-              if (U8) ptx::mma_i8(dtm, ad, bd, idesc, acc);
-              else ptx::mma_bf16(dtm, ad, bd, idesc, acc);
-            }
-            ptx::mma_commit(&bar_b_empty[s]);
+          const int kc0 = ch * 8, kc1 = min(KC, kc0 + 8);
+          const uint8_t* st = ring + s * kDtStageBytes;
+          for (int kc = kc0; kc < kc1; kc += 2) {
+            const uint8_t* a_src = (kFold && kc >= KCm) ? sOnes + (kc - KCm) * 2048 : st + (kc - kc0) * 2048;
+            const uint64_t ad = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(a_src), 2048, 128);
+            const uint64_t bd = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(st + kDtAB + (kc - kc0) * Nt * 16),
+                                                            (uint32_t)Nt * 16, 128);
+            const uint32_t acc = (ch > 0 || kc > kc0) ? 1u : 0u;
+            if (U8) ptx::mma_i8(dtm, ad, bd, idesc, acc);
+            else ptx::mma_bf16(dtm, ad, bd, idesc, acc);
           }
-          ptx::mma_commit(&bar_acc_full[buf]);
+          ptx::mma_commit(&bar_empty[s]);
         }
-        ptx::mma_commit(&bar_a_empty);
+        ptx::mma_commit(&bar_acc_full[buf]);
+        sc.advance(args);
       }
     }();
   } else {
-    // ------------------------------------------------------------ epilogue (4 warps, one row per thread)
-    // Per element: (u8) key = ||y||^2 - 2 acc, then append to the row's SMEM queue iff key < thr
-    // (predicated, no divergence). The queue is drained into the register top-K list — re-checking each
-    // entry against the (meanwhile tighter) threshold — whenever any lane of the warp might overflow it,
-    // while the list is not yet full, and at the end of the row. Appends happen in ascending column
-    // order and insertion is strict, so equal keys keep the smaller column (= smaller id), exactly.
+    // ------------------------------------------------------------ epilogue (2 warpgroups, one row per thread)
     [&]() {
-      const int q = warp & 3;
-      const int tid = q * 32 + lane;  // = row within the 128-row block = TMEM lane
+      const int ew = warp - 2;             // 0..7
+      const int wg = ew >> 2;              // warpgroup
+      const int q = warp & 3;              // TMEM lane quadrant of this warp (hardware: warp id % 4)
+      const int tid = q * 32 + lane;       // row within the 128-row block = TMEM lane
       const KT kInf = U8 ? (KT)0x7FFFFFFF : (KT)__int_as_float(0x7F800000);
-      KT* my_qk = q_key + tid;
-      uint32_t* my_qc = q_col + tid;
+      const KT kNegInf = U8 ? (KT)(-0x7FFFFFFF - 1) : (KT)__int_as_float(0xFF800000);
+      uint32_t* stg = reinterpret_cast<uint32_t*>(stg_base + wg * kDtStgBytes) + tid * kStgPitch;
+      KT* my_qk = reinterpret_cast<KT*>(q_base + wg * kDtQBytes) + tid;
+      uint16_t* my_qc = reinterpret_cast<uint16_t*>(q_base + wg * kDtQBytes + kQCap * 128 * 4) + tid;
       uint32_t tcount = 0;
-      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+      for (int64_t it = (int64_t)blockIdx.x + (int64_t)wg * gridDim.x; it < n_items; it += 2 * (int64_t)gridDim.x) {
         const WorkItem w = args.items[it];
         const DistSeg S = args.segs[w.seg];
         const int r0 = w.rb * 128;
         const int row = r0 + tid;
-        const int K = S.k + (S.self ? 1 : 0);  // self exclusion: keep k+1, drop the row itself afterwards
+        const int K = S.k;
         const int ncols = S.b.rows;
+        const int ntiles = (ncols + kDtTileN - 1) / kDtTileN;
+        // list of KMAX slots; the first KMAX-K hold -inf sentinels so that kk[KMAX-1] is the K-th best
         KT kk[KMAX];
-        uint32_t ii[KMAX];
+        uint16_t ii[KMAX];
 #pragma unroll
         for (int t = 0; t < KMAX; ++t) {
-          kk[t] = kInf;
-          ii[t] = 0xFFFFFFFFu;
+          kk[t] = t < KMAX - K ? kNegInf : kInf;
+          ii[t] = 0xFFFFu;
         }
-        KT thr = kInf;
         int qlen = 0;
-        const KT* nbp = U8 ? (const KT*)args.nb + S.b.pos : nullptr;
-        for (int c0 = 0; c0 < ncols; c0 += 256, ++tcount) {
-          const int Nt = min(256, (ncols - c0 + 31) & ~31);
-          const uint32_t buf = tcount & 1, use = tcount >> 1;
+        const int diag_chunk = S.self ? (r0 + q * 32) : -1;  // column base of this warp's diagonal chunk
+        for (int t = 0; t < ntiles; ++t, ++tcount) {
+          const int c0 = t * kDtTileN;
+          const int Nt = min(kDtTileN, (ncols - c0 + 31) & ~31);
+          const uint32_t buf = 2 * wg + (tcount & 1), use = tcount >> 1;
           if (!ptx::mbar_wait(&bar_acc_full[buf], use & 1, args.err, DERR_WAIT_TIMEOUT)) return;
           ptx::tc_fence_after();
-          const uint32_t taddr = tmem + buf * 256 + ((uint32_t)(q * 32) << 16);
+          const uint32_t taddr = tmem + buf * kDtTileN + ((uint32_t)(q * 32) << 16);
           for (int j0 = 0; j0 < Nt; j0 += 32) {
+            const int col0 = c0 + j0;
+            int4 nb4[8];
+            if (U8) {
+              // B column norms: 128 B per 32 columns, identical for all lanes (broadcast, L1/L2 resident)
+              const int4* p4 = reinterpret_cast<const int4*>((const int32_t*)args.nb + S.b.pos + col0);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) nb4[u] = __ldg(p4 + u);
+            }
             uint32_t v[32];
             ptx::tmem_ld32(taddr + j0, v);
-            const int col0 = c0 + j0;
-            int32_t nbv[32];
+            ptx::tmem_ld_wait();
+            // t_j = key_j - thr: its sign bit is the pass bit (key_j < thr). uint8: no overflow, since real keys
+            // lie in (-2^25, 2^25), padding keys are 0x3FFFFFFF and thr is a real key or 0x40000000 (list not
+            // full: everything passes). float: the sign of a difference is exact; thr = +inf passes everything.
+            // The mask is built with one funnel shift per element, bit j <-> column col0 + j.
+            const KT thr = kk[KMAX - 1];
+            const KT thr_eff = U8 ? (thr == kInf ? (KT)0x40000000 : thr) : thr;
+            KT tk[32];
+            uint32_t mask = 0;
             if (U8) {
-              const int4* p4 = reinterpret_cast<const int4*>(nbp + col0);
 #pragma unroll
               for (int u = 0; u < 8; ++u) {
-                const int4 x = __ldg(p4 + u);
-                nbv[4 * u + 0] = x.x;
-                nbv[4 * u + 1] = x.y;
-                nbv[4 * u + 2] = x.z;
-                nbv[4 * u + 3] = x.w;
+                tk[4 * u + 0] = (nb4[u].x - thr_eff) - 2 * (int32_t)v[4 * u + 0];
+                tk[4 * u + 1] = (nb4[u].y - thr_eff) - 2 * (int32_t)v[4 * u + 1];
+                tk[4 * u + 2] = (nb4[u].z - thr_eff) - 2 * (int32_t)v[4 * u + 2];
+                tk[4 * u + 3] = (nb4[u].w - thr_eff) - 2 * (int32_t)v[4 * u + 3];
               }
-            }
-            ptx::tmem_ld_wait();
+            } else {
 #pragma unroll
-            for (int jj = 0; jj < 32; ++jj) {
-              KT key;
-              if (U8) key = nbv[jj] - 2 * (int32_t)v[jj];
-              else key = __uint_as_float(v[jj]);
-              if (key < thr) {
-                my_qk[qlen * 128] = key;
-                my_qc[qlen * 128] = (uint32_t)(col0 + jj);
+              for (int jj = 0; jj < 32; ++jj) tk[jj] = __uint_as_float(v[jj]) - thr_eff;
+            }
+#pragma unroll
+            for (int jj = 31; jj >= 0; --jj) {
+              const uint32_t bits = U8 ? (uint32_t)tk[jj] : __float_as_uint((float)tk[jj]);
+              mask = __funnelshift_l(bits, mask, 1);  // (mask << 1) | sign(t_j)
+            }
+            if (col0 == diag_chunk) mask &= ~(1u << lane);  // self exclusion (by id: the diagonal element)
+            if (__any_sync(0xffffffffu, mask != 0)) {
+              // room for this chunk's passes (a drain empties the queue)
+              if (__any_sync(0xffffffffu, qlen + __popc(mask) > kQCap)) topk_drain<KT, KMAX>(kk, ii, qlen, my_qk, my_qc);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                uint4 w4;
+                if (U8) w4 = make_uint4((uint32_t)tk[4 * u], (uint32_t)tk[4 * u + 1], (uint32_t)tk[4 * u + 2],
+                                        (uint32_t)tk[4 * u + 3]);
+                else w4 = make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);  // float: the keys
+                *reinterpret_cast<uint4*>(stg + 4 * u) = w4;
+              }
+              __syncwarp();
+              while (mask) {
+                const int jj = __ffs(mask) - 1;
+                mask &= mask - 1;
+                // uint8 stages t = key - thr (key = t + thr exactly); float stages the key itself
+                my_qk[qlen * 128] = U8 ? (KT)(reinterpret_cast<const int32_t*>(stg)[jj] + (int32_t)thr_eff)
+                                       : (KT)reinterpret_cast<const float*>(stg)[jj];
+                my_qc[qlen * 128] = (uint16_t)(col0 + jj);
                 ++qlen;
               }
+              __syncwarp();
+              if (__any_sync(0xffffffffu, kk[KMAX - 1] == kInf && qlen > 0))
+                topk_drain<KT, KMAX>(kk, ii, qlen, my_qk, my_qc);
             }
-            // warp-uniform drain decision: the queue could overflow on the next chunk, or the list is not
-            // full yet (then every chunk drains, which also makes the threshold finite quickly)
-            if (__any_sync(0xffffffffu, qlen > kQCap - 32 || (qlen > 0 && thr == kInf)))
-              topk_drain<KT, KMAX>(kk, ii, thr, qlen, my_qk, my_qc, K);
           }
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&bar_acc_empty[buf]);
         }
-        topk_drain<KT, KMAX>(kk, ii, thr, qlen, my_qk, my_qc, K);
+        topk_drain<KT, KMAX>(kk, ii, qlen, my_qk, my_qc);
         if (row < S.a.rows) {
           const int64_t obase = S.out_off + (int64_t)row * S.ostride;
           KT na = 0;
@@ -330,8 +409,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
 #pragma unroll
           for (int t = 0; t < KMAX; ++t) {
             const uint32_t col = ii[t];
-            const bool take = t < K && o < S.k && col != 0xFFFFFFFFu && col < (uint32_t)ncols &&
-                              !(S.self && col == (uint32_t)row);
+            const bool take = t >= KMAX - K && col != 0xFFFFu && col < (uint32_t)ncols;
             if (take) {
               const KT key = kk[t];
               float D;
@@ -360,7 +438,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
   }
 }
 
-// Host launcher (dist_topk.cu): picks the instantiation for (dtype, metric).
+// Host launcher (dist_topk.cu): picks the instantiation for (dtype, metric, K).
 pipnn_status launch_dist_topk(const DistTopkArgs& a, bool u8, bool mips, int kmax, cudaStream_t st);
 
 }  // namespace pipnn

@@ -356,7 +356,7 @@ __device__ __forceinline__ void mma_16x8(int32_t (&acc)[4], const uint32_t (&a)[
 
 struct GpLayout {
   int Kb, pitch;  // bytes of a staged row (multiple of 32), SMEM row pitch (Kb + 16)
-  size_t rows_off, d_off, nrm_off, keys_off, perm_off, ids_off, adm_off, per_warp;
+  size_t rows_off, g_off, nrm_off, perm_off, ids_off, per_warp;
 };
 __host__ __device__ inline GpLayout gp_layout(int d, bool u8, int CP) {
   GpLayout L;
@@ -365,77 +365,110 @@ __host__ __device__ inline GpLayout gp_layout(int d, bool u8, int CP) {
   size_t o = 0;
   L.rows_off = o;
   o += (size_t)CP * L.pitch;
-  L.d_off = o;
+  L.g_off = o;
   o += (size_t)CP * (CP + 1) * 4;
   L.nrm_off = o;
   o += (size_t)CP * 4;
-  o = (o + 15) & ~(size_t)15;
-  L.keys_off = o;
-  o += (size_t)CP * 8;
   L.perm_off = o;
-  o += (size_t)CP * 2;
+  o += (size_t)CP * 4;
   L.ids_off = o;
   o += (size_t)CP * 4;
-  L.adm_off = o;
-  o += (size_t)CP * 2;
   L.per_warp = (o + 127) & ~(size_t)127;
   return L;
 }
 
-// Stage rows ids[0..nr) into the tile as 16-B chunks (u8 bytes / bf16 RNE of the fp32 coordinates);
-// chunks beyond d are zero, rows nr..nrp-1 are zero. Up to 8 chunks in flight per lane.
+// Stage rows ids[0..nr) into the tile as 16-B chunks (u8 bytes / bf16 RNE of the fp32 coordinates); chunks
+// beyond d and rows nr..nrp-1 are zero. Lane -> (row rr of a pass, chunk ch) is fixed; a pass covers 32/cpr
+// rows; 8 passes (8 independent 16-B loads per lane) are issued before the stores.
 template <bool U8>
 __device__ __forceinline__ void gp_stage(const void* __restrict__ Xv, int64_t ld, int d, const uint32_t* ids, int nr,
                                          int nrp, uint8_t* rows, const GpLayout& L, int lane) {
-  const int cpr = L.Kb >> 4;  // 16-B chunks per row
-  const int total = nrp * cpr;
+  const int cpr = L.Kb >> 4;  // 16-B chunks per row (<= 32)
+  const int rpp = 32 / cpr;   // rows per pass
+  const int rr = lane / cpr, ch = lane - rr * cpr;
+  const bool act = rr < rpp;
   const bool fast = U8 ? ((d & 15) == 0 && (ld & 15) == 0) : ((d & 7) == 0 && (ld & 3) == 0);
-  for (int e0 = 0; e0 < total; e0 += 256) {
+  for (int r0 = 0; r0 < nrp; r0 += 8 * rpp) {
     uint4 v[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int e = e0 + j * 32 + lane;
+      const int r = r0 + j * rpp + rr;
       v[j] = make_uint4(0u, 0u, 0u, 0u);
-      if (e < total) {
-        const int r = e / cpr, ch = e - r * cpr;
-        if (r < nr) {
-          const int64_t id = ids[r];
-          if (U8) {
-            const uint8_t* src = (const uint8_t*)Xv + id * ld;
-            if (fast) {
-              if (ch * 16 < d) v[j] = __ldg((const uint4*)src + ch);
-            } else {
-              uint32_t w[4] = {0u, 0u, 0u, 0u};
-              for (int t = 0; t < 16; ++t)
-                if (ch * 16 + t < d) w[t >> 2] |= (uint32_t)src[ch * 16 + t] << (8 * (t & 3));
-              v[j] = make_uint4(w[0], w[1], w[2], w[3]);
-            }
+      if (act && r < nr) {
+        const int64_t id = ids[r];
+        if (U8) {
+          const uint8_t* src = (const uint8_t*)Xv + id * ld;
+          if (fast) {
+            if (ch * 16 < d) v[j] = __ldg((const uint4*)src + ch);
           } else {
-            const float* src = (const float*)Xv + id * ld;
-            float f[8];
-            if (fast && ch * 8 < d) {
-              const float4 a = __ldg((const float4*)(src + ch * 8));
-              const float4 b = __ldg((const float4*)(src + ch * 8 + 4));
-              f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
-            } else {
-#pragma unroll
-              for (int t = 0; t < 8; ++t) f[t] = (ch * 8 + t < d) ? __ldg(src + ch * 8 + t) : 0.0f;
-            }
-            uint32_t w[4];
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-              w[t] = (uint32_t)f32_to_bf16_rne(f[2 * t]) | ((uint32_t)f32_to_bf16_rne(f[2 * t + 1]) << 16);
+            uint32_t w[4] = {0u, 0u, 0u, 0u};
+            for (int t = 0; t < 16; ++t)
+              if (ch * 16 + t < d) w[t >> 2] |= (uint32_t)src[ch * 16 + t] << (8 * (t & 3));
             v[j] = make_uint4(w[0], w[1], w[2], w[3]);
           }
+        } else {
+          const float* src = (const float*)Xv + id * ld;
+          float f[8];
+          if (fast && ch * 8 < d) {
+            const float4 a = __ldg((const float4*)(src + ch * 8));
+            const float4 b = __ldg((const float4*)(src + ch * 8 + 4));
+            f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+          } else {
+#pragma unroll
+            for (int t = 0; t < 8; ++t) f[t] = (ch * 8 + t < d) ? __ldg(src + ch * 8 + t) : 0.0f;
+          }
+          uint32_t w[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            w[t] = (uint32_t)f32_to_bf16_rne(f[2 * t]) | ((uint32_t)f32_to_bf16_rne(f[2 * t + 1]) << 16);
+          v[j] = make_uint4(w[0], w[1], w[2], w[3]);
         }
       }
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int e = e0 + j * 32 + lane;
-      if (e < total) {
-        const int r = e / cpr, ch = e - r * cpr;
-        *(uint4*)(rows + (size_t)r * L.pitch + ch * 16) = v[j];
+      const int r = r0 + j * rpp + rr;
+      if (act && r < nrp) *(uint4*)(rows + (size_t)r * L.pitch + ch * 16) = v[j];
+    }
+  }
+}
+
+// Register bitonic sort of E*32 u64 keys (+ u32 payload) across the warp, ascending; element i = e*32 + lane.
+template <int E>
+__device__ __forceinline__ void warp_bitonic_regs(uint64_t (&k)[E], uint32_t (&p)[E], int lane) {
+#pragma unroll
+  for (int kk = 2; kk <= 32 * E; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int je = j >> 5;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int f = e ^ je;
+          if (f > e) {
+            const int i = e * 32 + lane;
+            const bool up = (i & kk) == 0;
+            if ((k[e] > k[f]) == up) {
+              const uint64_t tk = k[e]; k[e] = k[f]; k[f] = tk;
+              const uint32_t tp = p[e]; p[e] = p[f]; p[f] = tp;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = e * 32 + lane;
+          const uint64_t ok = __shfl_xor_sync(0xffffffffu, k[e], j);
+          const uint32_t op = __shfl_xor_sync(0xffffffffu, p[e], j);
+          const bool lower = (lane & j) == 0;        // this element is the lower index of the pair
+          const bool up = (i & kk) == 0;
+          // lower keeps min if up, max if down; upper the opposite
+          const bool take_other = lower == up ? (ok < k[e]) : (ok > k[e]);
+          if (take_other) {
+            k[e] = ok;
+            p[e] = op;
+          }
+        }
       }
     }
   }
@@ -443,6 +476,9 @@ __device__ __forceinline__ void gp_stage(const void* __restrict__ Xv, int64_t ld
 
 // Pass over points (list == nullptr: all points) whose reservoir fits CP-1 candidates; larger ones are
 // appended to `defer` for the next tier. final_prune == 1 only (the R-nearest variant uses the generic kernel).
+// Per point (one warp): stage rows (u, candidates) -> Gram G on the tensor cores -> sort candidates by
+// (D(u,v), v) in registers -> prune matrix as bitmasks, lane per candidate c: bit y set iff y precedes c and
+// an*D(y,c) < ad*D(u,c) -> the serial lazy scan is then one mask test per candidate.
 template <bool U8, bool MIPS, int CP>
 __global__ void __launch_bounds__(256) fp_gram_kernel(const void* __restrict__ Xv, int64_t n, int d, int64_t ld,
                                                       int l_max, const uint64_t* __restrict__ slots,
@@ -452,18 +488,17 @@ __global__ void __launch_bounds__(256) fp_gram_kernel(const void* __restrict__ X
                                                       const uint32_t* __restrict__ list_n,
                                                       uint32_t* __restrict__ defer, uint32_t* __restrict__ defer_n) {
   using DT = typename std::conditional<U8, int32_t, float>::type;
+  constexpr int E = CP / 32;  // sorted candidates per lane; also the bitmask words per candidate
   extern __shared__ __align__(16) uint8_t gsm[];
   const GpLayout L = gp_layout(d, U8, CP);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   uint8_t* base = gsm + (size_t)warp * L.per_warp;
   uint8_t* rows = base + L.rows_off;
-  DT* Dm = (DT*)(base + L.d_off);  // [CP][CP + 1]
+  DT* G = (DT*)(base + L.g_off);  // [CP][CP + 1] Gram
   DT* nrm = (DT*)(base + L.nrm_off);
-  uint64_t* keys = (uint64_t*)(base + L.keys_off);
-  uint16_t* perm = (uint16_t*)(base + L.perm_off);
+  uint32_t* perm = (uint32_t*)(base + L.perm_off);  // sorted position -> row
   uint32_t* ids = (uint32_t*)(base + L.ids_off);
-  int16_t* adm = (int16_t*)(base + L.adm_off);
   const int DS = CP + 1;
   const int g = lane >> 2, t4 = lane & 3;
   const int64_t n_iter = list ? (int64_t)*list_n : n;
@@ -514,8 +549,8 @@ __global__ void __launch_bounds__(256) fp_gram_kernel(const void* __restrict__ X
       for (int bj = 0; bj < CP / 8; ++bj) {
         if (bj < nb8) {
           const int r = bi * 16 + g, s = bj * 8 + 2 * t4;
-          DT* d0 = Dm + (size_t)r * DS + s;
-          DT* d1 = Dm + (size_t)(r + 8) * DS + s;
+          DT* d0 = G + (size_t)r * DS + s;
+          DT* d1 = G + (size_t)(r + 8) * DS + s;
           if (U8) {
             d0[0] = acc[bj][0]; d0[1] = acc[bj][1]; d1[0] = acc[bj][2]; d1[1] = acc[bj][3];
           } else {
@@ -526,55 +561,97 @@ __global__ void __launch_bounds__(256) fp_gram_kernel(const void* __restrict__ X
       }
     }
     __syncwarp();
-    if (!MIPS) {
-      for (int r = lane; r < nr; r += 32) nrm[r] = Dm[(size_t)r * DS + r];
-      __syncwarp();
-    }
-    for (int e = lane; e < nr * nr; e += 32) {
-      const int r = e / nr, s = e - r * nr;
-      DT* p = Dm + (size_t)r * DS + s;
-      if (MIPS) *p = -*p;
-      else if (U8) *p = nrm[r] + nrm[s] - 2 * *p;
-      else *p = fmaxf(nrm[r] + nrm[s] - 2.0f * *p, 0.0f);
-    }
-    // ---- candidates ascending by (D(u, v), v)
-    int P = 32;
-    while (P < c) P <<= 1;
+    for (int r = lane; r < nr; r += 32) nrm[r] = MIPS ? (DT)0 : G[(size_t)r * DS + r];
     __syncwarp();
-    for (int t = lane; t < P; t += 32) {
-      uint64_t key = ~0ull;
+    // D(r, s) from the Gram: L2 n_r + n_s - 2 G_rs (float: clamped at 0), MIPS -G_rs
+    auto Dof = [&](int r, int s, DT nr_, DT ns_) -> DT {
+      const DT gg = G[(size_t)r * DS + s];
+      if (MIPS) return -gg;
+      if (U8) return nr_ + ns_ - 2 * gg;
+      return fmaxf(nr_ + ns_ - 2.0f * gg, 0.0f);
+    };
+    const DT n0 = nrm[0];
+    // ---- candidates ascending by (D(u, v), v), E per lane in registers
+    uint64_t key[E];
+    uint32_t pr_[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int t = e * 32 + lane;
+      key[e] = ~0ull;
+      pr_[e] = 0;
       if (t < c) {
-        const DT Du = Dm[t + 1];
-        key = ((uint64_t)(U8 ? (uint32_t)Du : f_ord((float)Du)) << 32) | ids[t + 1];
+        const DT Du = Dof(0, t + 1, n0, nrm[t + 1]);
+        key[e] = ((uint64_t)(U8 ? (uint32_t)Du : f_ord((float)Du)) << 32) | ids[t + 1];
+        pr_[e] = (uint32_t)(t + 1);
       }
-      keys[t] = key;
-      perm[t] = (uint16_t)(t + 1);
     }
+    warp_bitonic_regs<E>(key, pr_, lane);
+#pragma unroll
+    for (int e = 0; e < E; ++e) perm[e * 32 + lane] = pr_[e];
     __syncwarp();
-    warp_sort_kv(keys, perm, P, lane);
-    // ---- lazy RobustPrune: admit c unless an admitted y has an*D(y,c) < ad*D(u,c); stop at R
+    // ---- prune masks: M[e][w] bit b <-> sorted position y = 32 w + b prunes this lane's position i = 32 e + lane
+    uint32_t M[E][E];
+    DT Dui[E], ni[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      Dui[e] = U8 ? (DT)(uint32_t)(key[e] >> 32) : (DT)f_unord((uint32_t)(key[e] >> 32));
+      ni[e] = nrm[pr_[e] & 0xFFFF];
+#pragma unroll
+      for (int w = 0; w < E; ++w) M[e][w] = 0u;
+    }
+    for (int y = 0; y < c - 1; ++y) {
+      const int ry = perm[y];
+      const DT ny = nrm[ry];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = e * 32 + lane;
+        if (i > y && i < c) {
+          const DT Dyi = Dof(ry, pr_[e], ny, ni[e]);
+          bool p;
+          if (U8) p = (int64_t)an * (int64_t)Dyi < (int64_t)ad * (int64_t)Dui[e];
+          else p = (float)an * (float)Dyi < (float)ad * (float)Dui[e];
+          const uint32_t bit = p ? 1u << (y & 31) : 0u;
+#pragma unroll
+          for (int w = 0; w < E; ++w)
+            if (w == (y >> 5)) M[e][w] |= bit;
+        }
+      }
+    }
+    // ---- serial lazy scan over the sorted positions: admit i unless M_i meets the admitted set; stop at R
+    uint32_t A[E];
+#pragma unroll
+    for (int w = 0; w < E; ++w) A[w] = 0u;
     int na = 0;
     for (int i = 0; i < c && na < R; ++i) {
-      const int ri = perm[i];
-      const DT Dui = Dm[ri];
-      bool pr = false;
-      for (int a0 = 0; a0 < na && !pr; a0 += 32) {
-        bool mine = false;
-        if (a0 + lane < na) {
-          const DT Dyi = Dm[(size_t)adm[a0 + lane] * DS + ri];
-          if (U8) mine = (int64_t)an * (int64_t)Dyi < (int64_t)ad * (int64_t)Dui;
-          else mine = (float)an * (float)Dyi < (float)ad * (float)Dui;
+      const int ei = i >> 5, li = i & 31;
+      uint32_t hit = 0;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+#pragma unroll
+        for (int w = 0; w < E; ++w) {
+          const uint32_t m = __shfl_sync(0xffffffffu, M[e][w], li);
+          if (e == ei) hit |= m & A[w];
         }
-        pr = __any_sync(0xffffffffu, mine);
       }
-      if (!pr) {
-        if (lane == 0) {
-          adm[na] = (int16_t)ri;
-          out[na] = ids[ri];
-        }
+      if (hit == 0) {
+#pragma unroll
+        for (int w = 0; w < E; ++w)
+          if (w == ei) A[w] |= 1u << li;
         ++na;
-        __syncwarp();
       }
+    }
+    // ---- output in admission (= sorted) order
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = e * 32 + lane;
+      if (A[e] >> lane & 1u) {
+        int rank = __popc(A[e] & ((1u << lane) - 1u));
+#pragma unroll
+        for (int w = 0; w < E; ++w)
+          if (w < e) rank += __popc(A[w]);
+        out[rank] = (uint32_t)(key[e] & 0xFFFFFFFFu);
+      }
+      (void)i;
     }
     if (lane == 0) deg[u] = (uint32_t)na;
     __syncwarp();

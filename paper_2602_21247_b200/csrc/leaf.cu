@@ -213,7 +213,7 @@ pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, cons
     PIPNN_CUDA(cudaEventCreate(&e1));
     PIPNN_CUDA(cudaEventRecord(e0, c.st));
   }
-  PIPNN_TRY(launch_dist_topk(a, X->dtype == PIPNN_U8, X->metric == PIPNN_MIPS, k + 1, c.st));
+  PIPNN_TRY(launch_dist_topk(a, X->dtype == PIPNN_U8, X->metric == PIPNN_MIPS, k, c.st));
   if (c.tile_events) {
     PIPNN_CUDA(cudaEventRecord(e1, c.st));
     c.tile_events->push_back({e0, e1});

@@ -36,7 +36,7 @@ EDGE_SIZES = [1, 2, 3, 8, 9, 16, 17, 31, 32, 33, 127, 128, 129, 255, 256, 257, 3
               2048, 4096]
 
 
-@pytest.mark.parametrize("k", [1, 8, 10, 15])
+@pytest.mark.parametrize("k", [1, 3, 8, 10, 15])
 def test_leaf_pick_u8_edge_sizes_bit_exact(k):
     X = synth.gen_uniform(6000, 128, "u8", seed=3)
     X = (X // 16).astype(np.uint8)  # coarse values -> many exact distance ties (id tie-break)
@@ -87,13 +87,15 @@ def test_leaf_pick_float_config_leaves(name, n):
     assert ndiff <= 0.01 * rows, (ndiff, rows)
 
 
-@pytest.mark.parametrize("metric,d", [("l2", 96), ("mips", 200), ("l2", 240), ("l2", 7)])
-def test_leaf_pick_float_edge_sizes(metric, d):
+@pytest.mark.parametrize("metric,d,k", [("l2", 96, 8), ("mips", 200, 8), ("l2", 240, 8), ("l2", 7, 8), ("l2", 96, 3),
+                                        ("mips", 200, 3), ("l2", 128, 4), ("mips", 96, 12)])
+def test_leaf_pick_float_edge_sizes(metric, d, k):
+    # k = 3, 4, 12 run list lengths below their instantiation's capacity (-inf sentinel slots)
     X = synth.gen_uniform(6000, d, "f32", seed=d)
     off, ids = random_leaves(len(X), EDGE_SIZES, seed=2)
-    nbr, dist = run_gpu(X, metric, off, ids, 8)
-    onbr, odist = O.leaf_pick(O.Dataset(X, metric=metric, mode="bf16"), off, ids, 8)
-    ndiff, rows = check_candidate_lists_float(X, metric, ids, nbr, dist, onbr, odist, 8)
+    nbr, dist = run_gpu(X, metric, off, ids, k)
+    onbr, odist = O.leaf_pick(O.Dataset(X, metric=metric, mode="bf16"), off, ids, k)
+    ndiff, rows = check_candidate_lists_float(X, metric, ids, nbr, dist, onbr, odist, k)
     assert ndiff <= 0.01 * rows, (ndiff, rows)
 
 
