@@ -88,8 +88,8 @@ typedef struct {
   uint64_t seed;
 } pipnn_hashprune_params;
 
-/* Final prune: RobustPrune (Alg. 2) with alpha = alpha_num/alpha_den on the dissimilarity
- * values, max degree R (1..256). final_prune = 0 keeps the R nearest reservoir entries instead. */
+/* Final prune: RobustPrune (Alg. 2) with alpha = alpha_num/alpha_den (1 <= terms <= 127, so
+ * uint8 alpha tests stay exact in 32-bit integers) on the dissimilarity values, max degree R (1..256). final_prune = 0 keeps the R nearest reservoir entries instead. */
 typedef struct {
   int32_t R;
   int32_t alpha_num, alpha_den;

@@ -63,7 +63,8 @@ static pipnn_status validate_hp(const pipnn_hashprune_params* p) {
 static pipnn_status validate_prune(const pipnn_prune_params* p) {
   if (!p) return fail(PIPNN_EINVAL, "prune params NULL");
   if (p->R < 1 || p->R > 256) return fail(PIPNN_EINVAL, "R must be in [1, 256]");
-  if (p->alpha_num < 1 || p->alpha_den < 1) return fail(PIPNN_EINVAL, "alpha must be a positive rational");
+  if (p->alpha_num < 1 || p->alpha_den < 1 || p->alpha_num > 127 || p->alpha_den > 127)
+    return fail(PIPNN_EINVAL, "alpha must be a positive rational alpha_num/alpha_den with terms <= 127");
   return PIPNN_OK;
 }
 

@@ -2,10 +2,11 @@
 // Alg. 2 P:227-248 in its lazy form P:938-942), one warp per point u (fp_gram_kernel):
 //   1. rows = u and its c reservoir candidates, staged in shared memory (uint8 bytes, or the bf16 RNE
 //      coordinates of float rows: the path precision of DESIGN.md R19/R24);
-//   2. the (c+1)x(c+1) Gram on the tensor cores with warp-level MMAs (u8 x u8 -> s32, exact; bf16 -> f32),
-//      turned into D in place: D(r,s) = G_rr + G_ss - 2 G_rs (L2), -G_rs (MIPS);
-//   3. candidates sorted by (D(u,v), v) (R4); lazy scan: admit c unless an admitted y has
-//      alpha_num*D(y,c) < alpha_den*D(u,c); stop at R (lanes test the admitted set, one ballot per 32).
+//   2. the (c+1)x(c+1) Gram on the tensor cores with warp-level MMAs (u8 x u8 -> s32, exact; bf16 -> f32);
+//      D(r,s) = G_rr + G_ss - 2 G_rs (L2), -G_rs (MIPS);
+//   3. lane per candidate: bitmasks of the candidates that precede it in the (D(u,.), id) order (DESIGN.md
+//      R4) and of those that would prune it (alpha_num*D(y,c) < alpha_den*D(u,c)); the lazy scan (admit c
+//      unless an admitted y prunes it; stop at R) is solved as a fixpoint over warp ballots — no sort.
 //   Tiers by reservoir occupancy (<= 31, <= 63, <= 127 candidates; larger reservoirs take the generic
 //   final_prune_kernel), so the common case runs many warps per SM with small tiles.
 // final_prune = 0 (keep the R nearest reservoir entries) uses the generic kernel.
@@ -356,7 +357,7 @@ __device__ __forceinline__ void mma_16x8(int32_t (&acc)[4], const uint32_t (&a)[
 
 struct GpLayout {
   int Kb, pitch;  // bytes of a staged row (multiple of 32), SMEM row pitch (Kb + 16)
-  size_t rows_off, g_off, nrm_off, perm_off, ids_off, per_warp;
+  size_t rows_off, g_off, nrm_off, ids_off, per_warp;
 };
 __host__ __device__ inline GpLayout gp_layout(int d, bool u8, int CP) {
   GpLayout L;
@@ -368,8 +369,6 @@ __host__ __device__ inline GpLayout gp_layout(int d, bool u8, int CP) {
   L.g_off = o;
   o += (size_t)CP * (CP + 1) * 4;
   L.nrm_off = o;
-  o += (size_t)CP * 4;
-  L.perm_off = o;
   o += (size_t)CP * 4;
   L.ids_off = o;
   o += (size_t)CP * 4;
@@ -433,52 +432,12 @@ __device__ __forceinline__ void gp_stage(const void* __restrict__ Xv, int64_t ld
   }
 }
 
-// Register bitonic sort of E*32 u64 keys (+ u32 payload) across the warp, ascending; element i = e*32 + lane.
-template <int E>
-__device__ __forceinline__ void warp_bitonic_regs(uint64_t (&k)[E], uint32_t (&p)[E], int lane) {
-#pragma unroll
-  for (int kk = 2; kk <= 32 * E; kk <<= 1) {
-#pragma unroll
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      if (j >= 32) {
-        const int je = j >> 5;
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int f = e ^ je;
-          if (f > e) {
-            const int i = e * 32 + lane;
-            const bool up = (i & kk) == 0;
-            if ((k[e] > k[f]) == up) {
-              const uint64_t tk = k[e]; k[e] = k[f]; k[f] = tk;
-              const uint32_t tp = p[e]; p[e] = p[f]; p[f] = tp;
-            }
-          }
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int i = e * 32 + lane;
-          const uint64_t ok = __shfl_xor_sync(0xffffffffu, k[e], j);
-          const uint32_t op = __shfl_xor_sync(0xffffffffu, p[e], j);
-          const bool lower = (lane & j) == 0;        // this element is the lower index of the pair
-          const bool up = (i & kk) == 0;
-          // lower keeps min if up, max if down; upper the opposite
-          const bool take_other = lower == up ? (ok < k[e]) : (ok > k[e]);
-          if (take_other) {
-            k[e] = ok;
-            p[e] = op;
-          }
-        }
-      }
-    }
-  }
-}
-
 // Pass over points (list == nullptr: all points) whose reservoir fits CP-1 candidates; larger ones are
 // appended to `defer` for the next tier. final_prune == 1 only (the R-nearest variant uses the generic kernel).
-// Per point (one warp): stage rows (u, candidates) -> Gram G on the tensor cores -> sort candidates by
-// (D(u,v), v) in registers -> prune matrix as bitmasks, lane per candidate c: bit y set iff y precedes c and
-// an*D(y,c) < ad*D(u,c) -> the serial lazy scan is then one mask test per candidate.
+// Per point (one warp): stage rows (u, candidates) -> Gram G on the tensor cores -> lane per candidate i:
+// bitmasks P_i (y precedes i in the (D(u,.), id) order) and M_i (y precedes i and an*D(y,i) < ad*D(u,i)) ->
+// the lazy scan of P:938-942 (admit i unless an admitted y prunes it) solved as a fixpoint over ballots, no
+// sort: the admission order is the (D, id) order, so an admitted i lands at rank popc(admitted & P_i).
 template <bool U8, bool MIPS, int CP>
 __global__ void __launch_bounds__(256) fp_gram_kernel(const void* __restrict__ Xv, int64_t n, int d, int64_t ld,
                                                       int l_max, const uint64_t* __restrict__ slots,
@@ -497,7 +456,6 @@ __global__ void __launch_bounds__(256) fp_gram_kernel(const void* __restrict__ X
   uint8_t* rows = base + L.rows_off;
   DT* G = (DT*)(base + L.g_off);  // [CP][CP + 1] Gram
   DT* nrm = (DT*)(base + L.nrm_off);
-  uint32_t* perm = (uint32_t*)(base + L.perm_off);  // sorted position -> row
   uint32_t* ids = (uint32_t*)(base + L.ids_off);
   const int DS = CP + 1;
   const int g = lane >> 2, t4 = lane & 3;
@@ -571,87 +529,100 @@ __global__ void __launch_bounds__(256) fp_gram_kernel(const void* __restrict__ X
       return fmaxf(nr_ + ns_ - 2.0f * gg, 0.0f);
     };
     const DT n0 = nrm[0];
-    // ---- candidates ascending by (D(u, v), v), E per lane in registers
+    // ---- lane-per-candidate (E per lane): position i = 32 e + lane is candidate row i + 1, key (D(u,v), v)
     uint64_t key[E];
-    uint32_t pr_[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int t = e * 32 + lane;
-      key[e] = ~0ull;
-      pr_[e] = 0;
-      if (t < c) {
-        const DT Du = Dof(0, t + 1, n0, nrm[t + 1]);
-        key[e] = ((uint64_t)(U8 ? (uint32_t)Du : f_ord((float)Du)) << 32) | ids[t + 1];
-        pr_[e] = (uint32_t)(t + 1);
-      }
-    }
-    warp_bitonic_regs<E>(key, pr_, lane);
-#pragma unroll
-    for (int e = 0; e < E; ++e) perm[e * 32 + lane] = pr_[e];
-    __syncwarp();
-    // ---- prune masks: M[e][w] bit b <-> sorted position y = 32 w + b prunes this lane's position i = 32 e + lane
-    uint32_t M[E][E];
-    DT Dui[E], ni[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      Dui[e] = U8 ? (DT)(uint32_t)(key[e] >> 32) : (DT)f_unord((uint32_t)(key[e] >> 32));
-      ni[e] = nrm[pr_[e] & 0xFFFF];
-#pragma unroll
-      for (int w = 0; w < E; ++w) M[e][w] = 0u;
-    }
-    for (int y = 0; y < c - 1; ++y) {
-      const int ry = perm[y];
-      const DT ny = nrm[ry];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int i = e * 32 + lane;
-        if (i > y && i < c) {
-          const DT Dyi = Dof(ry, pr_[e], ny, ni[e]);
-          bool p;
-          if (U8) p = (int64_t)an * (int64_t)Dyi < (int64_t)ad * (int64_t)Dui[e];
-          else p = (float)an * (float)Dyi < (float)ad * (float)Dui[e];
-          const uint32_t bit = p ? 1u << (y & 31) : 0u;
-#pragma unroll
-          for (int w = 0; w < E; ++w)
-            if (w == (y >> 5)) M[e][w] |= bit;
-        }
-      }
-    }
-    // ---- serial lazy scan over the sorted positions: admit i unless M_i meets the admitted set; stop at R
-    uint32_t A[E];
-#pragma unroll
-    for (int w = 0; w < E; ++w) A[w] = 0u;
-    int na = 0;
-    for (int i = 0; i < c && na < R; ++i) {
-      const int ei = i >> 5, li = i & 31;
-      uint32_t hit = 0;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-#pragma unroll
-        for (int w = 0; w < E; ++w) {
-          const uint32_t m = __shfl_sync(0xffffffffu, M[e][w], li);
-          if (e == ei) hit |= m & A[w];
-        }
-      }
-      if (hit == 0) {
-#pragma unroll
-        for (int w = 0; w < E; ++w)
-          if (w == ei) A[w] |= 1u << li;
-        ++na;
-      }
-    }
-    // ---- output in admission (= sorted) order
+    DT ni[E];
+    uint32_t thr_i[E];  // uint8: ad * D(u, v) (exact in 32 bits: D < 2^25, alpha terms <= 127)
+    float thr_f[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const int i = e * 32 + lane;
-      if (A[e] >> lane & 1u) {
-        int rank = __popc(A[e] & ((1u << lane) - 1u));
-#pragma unroll
-        for (int w = 0; w < E; ++w)
-          if (w < e) rank += __popc(A[w]);
-        out[rank] = (uint32_t)(key[e] & 0xFFFFFFFFu);
+      key[e] = ~0ull;
+      ni[e] = 0;
+      thr_i[e] = 0;
+      thr_f[e] = 0.0f;
+      if (i < c) {
+        ni[e] = nrm[i + 1];
+        const DT Du = Dof(0, i + 1, n0, ni[e]);
+        key[e] = ((uint64_t)(U8 ? (uint32_t)Du : f_ord((float)Du)) << 32) | ids[i + 1];
+        if (U8) thr_i[e] = (uint32_t)ad * (uint32_t)Du;
+        else thr_f[e] = (float)ad * (float)Du;
       }
-      (void)i;
+    }
+    // ---- precedence and prune masks, bit y of word w <-> position 32 w + b:
+    //   P_i: y precedes i in the (D(u,.), id) order;  M_i: y precedes i and an*D(y,i) < ad*D(u,i)
+    uint32_t Pm[E][E], M[E][E];
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+#pragma unroll
+      for (int w = 0; w < E; ++w) Pm[e][w] = M[e][w] = 0u;
+#pragma unroll
+    for (int wy = 0; wy < E; ++wy) {
+      const int ylim = min(32, c - 32 * wy);
+      for (int b = 0; b < ylim; ++b) {
+        const int y = 32 * wy + b;
+        const uint64_t ky = __shfl_sync(0xffffffffu, key[wy], b);
+        const DT ny = nrm[y + 1];
+        const uint32_t bit = 1u << b;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const bool prec = ky < key[e];
+          const DT Dyi = Dof(y + 1, e * 32 + lane + 1, ny, ni[e]);
+          bool p;
+          if (U8) p = (uint32_t)an * (uint32_t)Dyi < thr_i[e];
+          else p = (float)an * (float)Dyi < thr_f[e];
+          if (prec) {
+            Pm[e][wy] |= bit;
+            if (p) M[e][wy] |= bit;
+          }
+        }
+      }
+    }
+    // ---- lazy RobustPrune as a fixpoint: i is admitted iff no admitted y in M_i. Decided lanes never change;
+    // each round decides at least the earliest undecided position, so <= c rounds (typically 2-4).
+    uint32_t KA[E], KR[E];  // admitted / rejected positions (warp-uniform)
+#pragma unroll
+    for (int w = 0; w < E; ++w) {
+      const int valid = min(32, max(0, c - 32 * w));
+      KA[w] = 0u;
+      KR[w] = valid == 32 ? 0u : ~((1u << valid) - 1u);  // positions >= c count as rejected
+    }
+    for (int round = 0; round < c; ++round) {
+      bool undecided_any = false;
+      uint32_t adm[E], rej[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const bool undecided = !((KA[e] | KR[e]) >> lane & 1u);
+        bool hit = false, open = false;
+#pragma unroll
+        for (int w = 0; w < E; ++w) {
+          hit |= (M[e][w] & KA[w]) != 0u;
+          open |= (M[e][w] & ~KR[w]) != 0u;
+        }
+        adm[e] = __ballot_sync(0xffffffffu, undecided && !hit && !open);
+        rej[e] = __ballot_sync(0xffffffffu, undecided && hit);
+      }
+#pragma unroll
+      for (int w = 0; w < E; ++w) {
+        KA[w] |= adm[w];
+        KR[w] |= rej[w];
+        undecided_any |= (KA[w] | KR[w]) != 0xFFFFFFFFu;
+      }
+      if (!undecided_any) break;
+    }
+    // ---- output: the first R admitted positions in (D(u,.), id) order ("stop at R")
+    int na = 0;
+#pragma unroll
+    for (int w = 0; w < E; ++w) na += __popc(KA[w]);
+    na = min(na, R);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      if (KA[e] >> lane & 1u) {
+        int rank = 0;
+#pragma unroll
+        for (int w = 0; w < E; ++w) rank += __popc(KA[w] & Pm[e][w]);
+        if (rank < R) out[rank] = (uint32_t)(key[e] & 0xFFFFFFFFu);
+      }
     }
     if (lane == 0) deg[u] = (uint32_t)na;
     __syncwarp();
