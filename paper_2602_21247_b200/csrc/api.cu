@@ -126,7 +126,7 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   int64_t* leaf_off = ar.take<int64_t>(bp.leaf_off_cap);
   uint32_t* leaf_ids = ar.take<uint32_t>(bp.leaf_ids_cap);
   const int k = p->pick.k;
-  uint32_t* nbr = ar.take<uint32_t>((size_t)bp.leaf_ids_cap * k);
+  uint16_t* cols = ar.take<uint16_t>((size_t)bp.leaf_ids_cap * k);  // picks as local leaf columns
   float* dist = ar.take<float>((size_t)bp.leaf_ids_cap * k);
   const bool sk_int = X->dtype == PIPNN_U8;
   void* sketch = ar.take<int32_t>((size_t)X->n * p->hp.m);
@@ -170,14 +170,19 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   // (a3, a4) leaf distance tiles + fused pick, in waves of at most `budget` 128-row blocks so
   // the tiled leaf buffer stays bounded (one wave at 1M points).
   const int64_t budget = std::min<int64_t>(bp.leaf_ids_cap / 64 + 1024, (int64_t)1 << 16);
+  int max_leaf_h = p->part.c_max;
   if (ar.measuring()) {
-    s = leaf_pick_impl(X, nullptr, nullptr, budget, budget * 128, k, nbr, dist, ar, c, budget);
+    s = leaf_pick_impl(X, nullptr, nullptr, budget, budget * 128, k, nullptr, dist, ar, c, budget, cols);
     if (s != PIPNN_OK) { cleanup(); return s; }
   } else if (n_leaves > 0) {
     std::vector<int64_t> off(n_leaves + 1);
     PIPNN_CUDA(cudaMemcpyAsync(off.data(), leaf_off, (n_leaves + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     PIPNN_CUDA(cudaStreamSynchronize(st));
-    for (int64_t b = 0; b < n_leaves; ++b) leaf_pairs += (off[b + 1] - off[b]) * (off[b + 1] - off[b]);
+    max_leaf_h = 1;
+    for (int64_t b = 0; b < n_leaves; ++b) {
+      leaf_pairs += (off[b + 1] - off[b]) * (off[b + 1] - off[b]);
+      max_leaf_h = std::max<int>(max_leaf_h, (int)(off[b + 1] - off[b]));
+    }
     if (stats_h) c.tile_events = &tile_ev;
     int64_t b0 = 0;
     while (b0 < n_leaves) {
@@ -187,7 +192,7 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
         ++b1;
       }
       if (b1 == b0) { cleanup(); return fail(PIPNN_EUNSUPPORTED, "leaf larger than the wave budget"); }
-      s = leaf_pick_impl(X, leaf_off + b0, leaf_ids, b1 - b0, off[b1] - off[b0], k, nbr, dist, ar, c, budget);
+      s = leaf_pick_impl(X, leaf_off + b0, leaf_ids, b1 - b0, off[b1] - off[b0], k, nullptr, dist, ar, c, budget, cols);
       if (s != PIPNN_OK) { cleanup(); return s; }
       ar.release(mark);
       b0 = b1;
@@ -197,12 +202,11 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   ar.release(mark);
   if (!ar.measuring()) cudaEventRecord(ev[3], st);
   // (a5, a6) bidirected edges -> HashPrune reservoirs (Alg. 3)
-  if (!ar.measuring()) {
-    PIPNN_CUDA(cudaMemsetAsync(slots, 0xFF, (size_t)X->n * p->hp.l_max * sizeof(uint64_t), st));
-    PIPNN_CUDA(cudaMemsetAsync(count, 0, (size_t)X->n * sizeof(uint32_t), st));
-  }
-  s = hashprune_from_lists(p->hp.m, p->hp.l_max, X->n, sketch, sk_int, slots, count, leaf_ids, n_inst, k, nbr, dist,
-                           n_edges_dev, ar, c);
+  // Reservoirs start empty (count = 0). The build never reads a slot at or beyond count[u] (merge and final
+  // prune), so the n*l_max arena is not initialised here (it is internal to pipnn_build).
+  if (!ar.measuring()) PIPNN_CUDA(cudaMemsetAsync(count, 0, (size_t)X->n * sizeof(uint32_t), st));
+  s = hashprune_from_leaves(p->hp.m, p->hp.l_max, X->n, sketch, sk_int, slots, count, leaf_off, n_leaves, leaf_ids,
+                            n_inst, k, cols, dist, max_leaf_h, n_edges_dev, ar, c);
   if (s != PIPNN_OK) { cleanup(); return s; }
   ar.release(mark);
   if (!ar.measuring()) cudaEventRecord(ev[4], st);

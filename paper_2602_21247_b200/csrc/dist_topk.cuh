@@ -71,7 +71,8 @@ struct DistTopkArgs {
   const WorkItem* items;
   const int64_t* n_items;  // device scalar
   const uint32_t* col_ids; // nullable: output id of column j = col_ids[b.id_off + j], else j
-  uint32_t* out_idx;       // output picks (column ids), layout given by DistSeg::out_off / ostride
+  uint32_t* out_idx;       // output picks (column ids), layout given by DistSeg::out_off / ostride; nullable
+  uint16_t* out_col;       // nullable: the picks' local column indices (same layout; 0xFFFF = none)
   float* out_dist;         // output D, same layout, nullable
   int* err;
 };
@@ -416,13 +417,15 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
               if (MIPS) D = (float)key;
               else if (U8) D = (float)(na + key);
               else D = fmaxf(fmaf(2.0f, (float)key, (float)na), 0.0f);
-              args.out_idx[obase + o] = args.col_ids ? args.col_ids[S.b.id_off + col] : col;
+              if (args.out_idx) args.out_idx[obase + o] = args.col_ids ? args.col_ids[S.b.id_off + col] : col;
+              if (args.out_col) args.out_col[obase + o] = (uint16_t)col;
               if (args.out_dist) args.out_dist[obase + o] = D;
               ++o;
             }
           }
           for (; o < S.ostride; ++o) {
-            args.out_idx[obase + o] = 0xFFFFFFFFu;
+            if (args.out_idx) args.out_idx[obase + o] = 0xFFFFFFFFu;
+            if (args.out_col) args.out_col[obase + o] = 0xFFFFu;
             if (args.out_dist) args.out_dist[obase + o] = __int_as_float(0x7F800000);
           }
         }

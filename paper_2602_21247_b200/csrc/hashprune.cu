@@ -50,47 +50,6 @@ __global__ void hp_scatter_kernel(const uint32_t* __restrict__ owner, const uint
   }
 }
 
-// ------------------------------------------------------------------ grouping of candidate lists (build path)
-// Instance i holds point p = leaf_ids[i] and its picks nbr[i*k + t] with D = dist[i*k + t]. Every valid pick
-// q yields the forward edge p -> q (owner p) and the reverse edge q -> p (owner q), both carrying D (P:565,
-// P:914; each directed edge goes to its source's reservoir).
-__global__ void hp_hist_lists_kernel(const uint32_t* __restrict__ leaf_ids, int64_t I, int k,
-                                     const uint32_t* __restrict__ nbr, uint32_t* __restrict__ cnt) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t p = leaf_ids[i];
-    uint32_t nv = 0;
-    for (int t = 0; t < k; ++t) {
-      const uint32_t q = nbr[i * k + t];
-      if (q == 0xFFFFFFFFu) break;
-      ++nv;
-      atomicAdd(&cnt[q], 1u);
-    }
-    if (nv) atomicAdd(&cnt[p], nv);
-  }
-}
-
-template <typename ST>
-__global__ void hp_scatter_lists_kernel(const uint32_t* __restrict__ leaf_ids, int64_t I, int k,
-                                        const uint32_t* __restrict__ nbr, const float* __restrict__ dist,
-                                        const ST* __restrict__ S, int m, const uint64_t* __restrict__ start,
-                                        uint32_t* __restrict__ cursor, uint64_t* __restrict__ keys) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t p = leaf_ids[i];
-    uint32_t nv = 0;
-    for (int t = 0; t < k; ++t)
-      if (nbr[i * k + t] != 0xFFFFFFFFu) ++nv;
-    if (!nv) continue;
-    uint64_t fwd = start[p] + atomicAdd(&cursor[p], nv);
-    for (int t = 0; t < (int)nv; ++t) {
-      const uint32_t q = nbr[i * k + t];
-      const float D = dist[i * k + t];
-      keys[fwd + t] = slot_key<ST>(S, m, p, q, D);
-      const uint64_t rev = start[q] + atomicAdd(&cursor[q], 1u);
-      keys[rev] = slot_key<ST>(S, m, q, p, D);
-    }
-  }
-}
-
 // ------------------------------------------------------------------ per-owner merge (warp per owner)
 __device__ __forceinline__ void warp_bitonic_sort(uint64_t* a, int P, int lane) {
   for (int k = 2; k <= P; k <<= 1)
@@ -250,32 +209,370 @@ pipnn_status hashprune_impl(int m, int l_max, int64_t n, const void* sketch, boo
   return launch_merge(n, l_max, g.start, keys, slots, count, c);
 }
 
-pipnn_status hashprune_from_lists(int m, int l_max, int64_t n, const void* sketch, bool sk_int, uint64_t* slots,
-                                  uint32_t* count, const uint32_t* leaf_ids, int64_t n_inst, int k,
-                                  const uint32_t* nbr, const float* dist, int64_t* n_edges_dev, Arena& ar,
-                                  const Ctx& c) {
-  Grouping g = take_grouping(n, ar);
-  uint64_t* keys = ar.take<uint64_t>(std::max<int64_t>(1, 2 * n_inst * k));
+// ------------------------------------------------------------------ build path: leaf-local edge grouping
+// Every edge a leaf emits has its owner inside that leaf (p -> q with owner p, q -> p with
+// owner q, both members of the leaf). So the edges are grouped per leaf in shared memory, without any
+// global sort: forward keys go to fwd[i*k + t] (instance i = p's position in leaf_ids), reverse keys of
+// owner instance j are laid out contiguously in rev[] inside the leaf's own block [off_b*k, off_{b+1}*k)
+// (the leaf emits as many reverse as forward edges), with rev_start[j] / rev_cnt[j]. The residual hashes
+// (Eq. 1 via sketches) of both directions come from the leaf members' sketches staged in SMEM.
+template <typename ST>
+__global__ void __launch_bounds__(256) hp_emit_kernel(const int64_t* __restrict__ leaf_off, const uint32_t* __restrict__ leaf_ids,
+                                                      int k, const uint16_t* __restrict__ cols,
+                                                      const float* __restrict__ dist, const ST* __restrict__ S, int m,
+                                                      int stage_sk, uint64_t* __restrict__ fwd, uint64_t* __restrict__ rev,
+                                                      uint32_t* __restrict__ rev_start, uint32_t* __restrict__ rev_cnt,
+                                                      int64_t* __restrict__ n_edges) {
+  extern __shared__ __align__(16) uint8_t esm[];
+  __shared__ uint32_t tot_sh;
+  const int64_t b = blockIdx.x;
+  const int64_t o0 = leaf_off[b];
+  const int s = (int)(leaf_off[b + 1] - o0);
+  uint32_t* ids = (uint32_t*)esm;   // [s]
+  uint32_t* rc = ids + s;           // [s] reverse in-degree, then cursor
+  uint32_t* rs = rc + s;            // [s] exclusive scan of rc
+  ST* sk = (ST*)(rs + s);           // [s][m] when staged
+  if (threadIdx.x == 0) tot_sh = 0;
+  for (int j = threadIdx.x; j < s; j += blockDim.x) {
+    ids[j] = leaf_ids[o0 + j];
+    rc[j] = 0;
+  }
+  __syncthreads();
+  if (stage_sk)
+    for (int e = threadIdx.x; e < s * m; e += blockDim.x) {
+      const int j = e / m;
+      sk[e] = S[(int64_t)ids[j] * m + (e - j * m)];
+    }
+  const int P = s * k;
+  const uint16_t* cl = cols + o0 * k;
+  for (int e = threadIdx.x; e < P; e += blockDim.x) {
+    const uint16_t q = cl[e];
+    if (q != 0xFFFFu) atomicAdd(&rc[q], 1u);
+  }
+  __syncthreads();
+  // exclusive scan of rc (block-wide, thread-serial chunks + warp scan of chunk sums)
+  {
+    const int per = (s + blockDim.x - 1) / blockDim.x;
+    const int j0 = threadIdx.x * per, j1 = min(s, j0 + per);
+    uint32_t sum = 0;
+    for (int j = j0; j < j1; ++j) sum += rc[j];
+    __shared__ uint32_t part[256];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      uint32_t run = 0;
+      for (int w0 = 0; w0 < (int)blockDim.x; w0 += 32) {
+        uint32_t v = part[w0 + threadIdx.x], x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if ((int)threadIdx.x >= o) x += y;
+        }
+        part[w0 + threadIdx.x] = run + x - v;
+        run += __shfl_sync(0xffffffffu, x, 31);
+      }
+      if (threadIdx.x == 0) tot_sh = run;
+    }
+    __syncthreads();
+    uint32_t acc = part[threadIdx.x];
+    for (int j = j0; j < j1; ++j) {
+      rs[j] = acc;
+      acc += rc[j];
+    }
+  }
+  __syncthreads();
+  const uint64_t rbase = (uint64_t)o0 * k;
+  for (int j = threadIdx.x; j < s; j += blockDim.x) {
+    rev_start[o0 + j] = (uint32_t)(rbase + rs[j]);  // absolute offset into rev (I*k < 2^32, checked on the host)
+    rev_cnt[o0 + j] = rc[j];
+    rc[j] = 0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < P; e += blockDim.x) {
+    const int i = e / k;
+    const uint16_t q = cl[e];
+    uint64_t kf = ~0ull;
+    if (q != 0xFFFFu) {
+      const uint32_t pid = ids[i], qid = ids[q];
+      const ST* sp = stage_sk ? sk + (int64_t)i * m : S + (int64_t)pid * m;
+      const ST* sq = stage_sk ? sk + (int64_t)q * m : S + (int64_t)qid * m;
+      uint32_t hf = 0, hr = 0;
+      for (int t = 0; t < m; ++t) {
+        const ST a = sp[t], c = sq[t];
+        hf |= (uint32_t)(c >= a) << t;  // h_p(q): bit t = [S(q)_t >= S(p)_t]
+        hr |= (uint32_t)(a >= c) << t;  // h_q(p)
+      }
+      const uint64_t dk = (uint64_t)dist_order_key(dist[o0 * k + e]) << 32;
+      kf = ((uint64_t)hf << 48) | dk | qid;
+      const uint32_t pos = rs[q] + atomicAdd(&rc[q], 1u);
+      rev[rbase + pos] = ((uint64_t)hr << 48) | dk | pid;
+    }
+    fwd[o0 * k + e] = kf;
+  }
+  if (threadIdx.x == 0) atomicAdd((unsigned long long*)n_edges, 2ull * tot_sh);
+}
+
+// point -> instances (inverse of leaf_ids): counting sort; the order inside a point's list is irrelevant.
+__global__ void hp_inv_hist_kernel(const uint32_t* __restrict__ leaf_ids, int64_t I, uint32_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[leaf_ids[i]], 1u);
+}
+__global__ void hp_inv_fill_kernel(const uint32_t* __restrict__ leaf_ids, int64_t I, const uint64_t* __restrict__ start,
+                                   uint32_t* __restrict__ cursor, uint32_t* __restrict__ inv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = leaf_ids[i];
+    inv[start[p] + atomicAdd(&cursor[p], 1u)] = (uint32_t)i;
+  }
+}
+
+// Register bitonic sort of E*32 u64 keys across a warp, ascending; element i = e*32 + lane.
+template <int E>
+__device__ __forceinline__ void warp_sort_regs(uint64_t (&k)[E], int lane) {
+#pragma unroll
+  for (int kk = 2; kk <= 32 * E; kk <<= 1) {
+#pragma unroll
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int f = e ^ (j >> 5);
+          if (f > e) {
+            const bool up = ((e * 32 + lane) & kk) == 0;
+            const uint64_t a = k[e], c = k[f];
+            const bool sw = (a > c) == up;
+            k[e] = sw ? c : a;
+            k[f] = sw ? a : c;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, k[e], j);
+          const bool lower = (lane & j) == 0;
+          const bool up = ((e * 32 + lane) & kk) == 0;
+          const uint64_t mn = o < k[e] ? o : k[e], mx = o < k[e] ? k[e] : o;
+          k[e] = (lower == up) ? mn : mx;
+        }
+      }
+    }
+  }
+}
+
+// The keys streamed to owner u, addressed by a flat index: its reservoir (c keys), then for each of its
+// instances the k forward keys and the rev_cnt reverse keys. Forward keys of missing picks are ~0.
+struct OwnerKeys {
+  const uint64_t* res;
+  int c, k;
+  const uint32_t* inst;  // the owner's instance ids
+  int ninst;
+  const uint64_t* fwd;
+  const uint64_t* rev;
+  const uint32_t* rev_start;
+  const uint32_t* rev_cnt;
+  __device__ __forceinline__ uint64_t get(int idx) const {
+    if (idx < c) return res[idx];
+    idx -= c;
+    for (int t = 0; t < ninst; ++t) {
+      const uint32_t i = inst[t];
+      if (idx < k) return fwd[(int64_t)i * k + idx];
+      idx -= k;
+      const int rcn = (int)rev_cnt[i];
+      if (idx < rcn) return rev[(uint64_t)rev_start[i] + idx];
+      idx -= rcn;
+    }
+    return ~0ull;
+  }
+};
+
+// Fast merge: one warp per owner, all of its keys (reservoir + new, <= 32*E) in registers: bitonic sort,
+// keep the first key of every hash run (bucket minimum, Alg. 3's collision rule), write back sorted by hash.
+// Owners with more keys, more instances than lanes, or more than l_max buckets go to the generic merge.
+template <int E>
+__global__ void __launch_bounds__(256) hp_merge_inst_kernel(int64_t n, int l_max, int k, const uint64_t* __restrict__ inv_start,
+                                                            const uint32_t* __restrict__ inv, const uint64_t* __restrict__ fwd,
+                                                            const uint64_t* __restrict__ rev,
+                                                            const uint32_t* __restrict__ rev_start,
+                                                            const uint32_t* __restrict__ rev_cnt,
+                                                            uint64_t* __restrict__ slots, uint32_t* __restrict__ count,
+                                                            uint32_t* __restrict__ defer, uint32_t* __restrict__ defer_n) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = wid; u < n; u += nw) {
+    const uint64_t i0 = inv_start[u];
+    const int ni = (int)(inv_start[u + 1] - i0);
+    if (ni == 0) continue;
+    const int c = (int)count[u];
+    int sz = 0;
+    if (lane < ni) sz = k + (int)rev_cnt[inv[i0 + lane]];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, o);
+    const int T = c + sz;
+    if (ni > 32 || T > 32 * E) {
+      if (lane == 0) defer[atomicAdd(defer_n, 1u)] = (uint32_t)u;
+      continue;
+    }
+    uint64_t* res = slots + u * (int64_t)l_max;
+    OwnerKeys ok{res, c, k, inv + i0, ni, fwd, rev, rev_start, rev_cnt};
+    uint64_t key[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int idx = e * 32 + lane;
+      key[e] = idx < T ? ok.get(idx) : ~0ull;
+    }
+    warp_sort_regs<E>(key, lane);
+    // bucket minima: first key of each hash run; ~0 keys (missing picks, padding) are never kept
+    bool keep[E];
+    int B = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint64_t up = __shfl_up_sync(0xffffffffu, key[e], 1);
+      const uint64_t last = __shfl_sync(0xffffffffu, key[e > 0 ? e - 1 : 0], 31);  // element 32e - 1
+      const uint64_t prev = lane > 0 ? up : last;
+      const bool first = (e == 0 && lane == 0) || ((prev >> 48) != (key[e] >> 48));
+      keep[e] = key[e] != ~0ull && first;
+      B += __popc(__ballot_sync(0xffffffffu, keep[e]));
+    }
+    if (B > l_max) {
+      if (lane == 0) defer[atomicAdd(defer_n, 1u)] = (uint32_t)u;
+      continue;
+    }
+    int base = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep[e]);
+      if (keep[e]) res[base + __popc(bal & ((1u << lane) - 1u))] = key[e];
+      base += __popc(bal);
+    }
+    if (lane == 0) count[u] = (uint32_t)B;
+  }
+}
+
+// Generic merge for the deferred owners: the chunked SMEM algorithm of hp_merge_kernel over OwnerKeys.
+__global__ void __launch_bounds__(128) hp_merge_inst_generic_kernel(int l_max, int cap, int k,
+                                                                    const uint64_t* __restrict__ inv_start,
+                                                                    const uint32_t* __restrict__ inv,
+                                                                    const uint64_t* __restrict__ fwd,
+                                                                    const uint64_t* __restrict__ rev,
+                                                                    const uint32_t* __restrict__ rev_start,
+                                                                    const uint32_t* __restrict__ rev_cnt,
+                                                                    uint64_t* __restrict__ slots, uint32_t* __restrict__ count,
+                                                                    const uint32_t* __restrict__ list,
+                                                                    const uint32_t* __restrict__ list_n) {
+  extern __shared__ uint64_t gm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* buf = gm + (size_t)warp * 2 * cap;
+  uint64_t* tmp = buf + cap;
+  const int64_t nl = *list_n;
+  for (int64_t it = blockIdx.x * 4 + warp; it < nl; it += (int64_t)gridDim.x * 4) {
+    const int64_t u = list[it];
+    const uint64_t i0 = inv_start[u];
+    const int ni = (int)(inv_start[u + 1] - i0);
+    uint64_t* res = slots + u * (int64_t)l_max;
+    int c = (int)count[u];
+    int total_new = 0;
+    for (int t = lane; t < ni; t += 32) total_new += k + (int)rev_cnt[inv[i0 + t]];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) total_new += __shfl_xor_sync(0xffffffffu, total_new, o);
+    OwnerKeys ok{res, 0, k, inv + i0, ni, fwd, rev, rev_start, rev_cnt};
+    for (int t = lane; t < c; t += 32) buf[t] = res[t];
+    int e = 0;
+    while (e < total_new) {
+      const int chunk = min(total_new - e, cap - c);
+      for (int t = lane; t < chunk; t += 32) buf[c + t] = ok.get(e + t);
+      const int total = c + chunk;
+      const int P = pow2_at_least(total);
+      for (int t = total + lane; t < P; t += 32) buf[t] = ~0ull;
+      __syncwarp();
+      warp_bitonic_sort(buf, P, lane);
+      // drop ~0 keys (missing picks) before taking bucket minima
+      int tv = total;
+      while (tv > 0 && buf[tv - 1] == ~0ull) --tv;
+      int B = warp_bucket_minima(buf, tv, tmp, lane);
+      if (B > l_max) {
+        const int PB = pow2_at_least(B);
+        for (int t = lane; t < PB; t += 32) {
+          const uint64_t x = t < B ? tmp[t] : ~0ull;
+          tmp[t] = t < B ? ((x << 16) | (x >> 48)) : ~0ull;
+        }
+        __syncwarp();
+        warp_bitonic_sort(tmp, PB, lane);
+        const int PL = pow2_at_least(l_max);
+        for (int t = lane; t < PL; t += 32) {
+          const uint64_t x = tmp[t];
+          tmp[t] = t < l_max ? ((x >> 16) | (x << 48)) : ~0ull;
+        }
+        __syncwarp();
+        warp_bitonic_sort(tmp, PL, lane);
+        B = l_max;
+      }
+      for (int t = lane; t < B; t += 32) buf[t] = tmp[t];
+      __syncwarp();
+      c = B;
+      e += chunk;
+    }
+    for (int t = lane; t < c; t += 32) res[t] = buf[t];
+    if (lane == 0) count[u] = (uint32_t)c;
+  }
+}
+
+pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sketch, bool sk_int, uint64_t* slots,
+                                   uint32_t* count, const int64_t* leaf_off, int64_t n_leaves, const uint32_t* leaf_ids,
+                                   int64_t n_inst, int k, const uint16_t* cols, const float* dist, int max_leaf,
+                                   int64_t* n_edges_dev, Arena& ar, const Ctx& c) {
+  const int64_t P = std::max<int64_t>(1, n_inst * k);
+  uint64_t* fwd = ar.take<uint64_t>(P);
+  uint64_t* rev = ar.take<uint64_t>(P);
+  uint32_t* rev_start = ar.take<uint32_t>(std::max<int64_t>(1, n_inst));
+  uint32_t* rev_cnt = ar.take<uint32_t>(std::max<int64_t>(1, n_inst));
+  Grouping g = take_grouping(n, ar);  // point -> instances
+  uint32_t* inv = ar.take<uint32_t>(std::max<int64_t>(1, n_inst));
+  uint32_t* defer = ar.take<uint32_t>(n);
+  uint32_t* defer_n = ar.take<uint32_t>(1);
   if (ar.measuring()) return PIPNN_OK;
   if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (hashprune)");
+  if (P >= ((int64_t)1 << 32)) return fail(PIPNN_EUNSUPPORTED, "hashprune: more than 2^32 picks in one wave");
+  PIPNN_CUDA(cudaMemsetAsync(n_edges_dev, 0, sizeof(int64_t), c.st));
+  if (n_inst == 0 || n_leaves == 0) return PIPNN_OK;
+  // (1) leaf-local emission of both edge directions
+  max_leaf = std::max(1, std::min(max_leaf, 4096));
+  const size_t sk_bytes = (size_t)max_leaf * m * 4;
+  const int stage_sk = sk_bytes <= 96 * 1024 ? 1 : 0;
+  const int smem = (int)((size_t)max_leaf * 12 + (stage_sk ? sk_bytes : 0));
+  if (sk_int) {
+    PIPNN_CUDA(cudaFuncSetAttribute(hp_emit_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    hp_emit_kernel<int32_t><<<(unsigned)n_leaves, 256, smem, c.st>>>(leaf_off, leaf_ids, k, cols, dist,
+                                                                      (const int32_t*)sketch, m, stage_sk, fwd, rev,
+                                                                      rev_start, rev_cnt, n_edges_dev);
+  } else {
+    PIPNN_CUDA(cudaFuncSetAttribute(hp_emit_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    hp_emit_kernel<float><<<(unsigned)n_leaves, 256, smem, c.st>>>(leaf_off, leaf_ids, k, cols, dist,
+                                                                    (const float*)sketch, m, stage_sk, fwd, rev,
+                                                                    rev_start, rev_cnt, n_edges_dev);
+  }
+  PIPNN_LAUNCHED("hp_emit_kernel", c.st);
+  // (2) point -> instances
   PIPNN_CUDA(cudaMemsetAsync(g.cnt, 0, (n + 1) * sizeof(uint32_t), c.st));
   PIPNN_CUDA(cudaMemsetAsync(g.cursor, 0, n * sizeof(uint32_t), c.st));
-  if (n_inst > 0) {
-    hp_hist_lists_kernel<<<(unsigned)grid_for(n_inst), 256, 0, c.st>>>(leaf_ids, n_inst, k, nbr, g.cnt);
-    PIPNN_LAUNCHED("hp_hist_lists_kernel", c.st);
-  }
+  hp_inv_hist_kernel<<<(unsigned)grid_for(n_inst), 256, 0, c.st>>>(leaf_ids, n_inst, g.cnt);
+  PIPNN_LAUNCHED("hp_inv_hist_kernel", c.st);
   PIPNN_CUDA(cub::DeviceScan::ExclusiveSum(g.tmp, g.tmp_bytes, g.cnt, g.start, (int)(n + 1), c.st));
-  if (n_edges_dev)
-    PIPNN_CUDA(cudaMemcpyAsync(n_edges_dev, g.start + n, sizeof(int64_t), cudaMemcpyDeviceToDevice, c.st));
-  if (n_inst == 0) return PIPNN_OK;
-  if (sk_int)
-    hp_scatter_lists_kernel<int32_t><<<(unsigned)grid_for(n_inst), 256, 0, c.st>>>(
-        leaf_ids, n_inst, k, nbr, dist, (const int32_t*)sketch, m, g.start, g.cursor, keys);
-  else
-    hp_scatter_lists_kernel<float><<<(unsigned)grid_for(n_inst), 256, 0, c.st>>>(
-        leaf_ids, n_inst, k, nbr, dist, (const float*)sketch, m, g.start, g.cursor, keys);
-  PIPNN_LAUNCHED("hp_scatter_lists_kernel", c.st);
-  return launch_merge(n, l_max, g.start, keys, slots, count, c);
+  hp_inv_fill_kernel<<<(unsigned)grid_for(n_inst), 256, 0, c.st>>>(leaf_ids, n_inst, g.start, g.cursor, inv);
+  PIPNN_LAUNCHED("hp_inv_fill_kernel", c.st);
+  // (3) merge per owner (register path), deferred owners through the generic chunked path
+  PIPNN_CUDA(cudaMemsetAsync(defer_n, 0, sizeof(uint32_t), c.st));
+  const int64_t blocks = std::min<int64_t>(ceil_div(n, 8), (int64_t)num_sms() * 32);
+  hp_merge_inst_kernel<2><<<(unsigned)blocks, 256, 0, c.st>>>(n, l_max, k, g.start, inv, fwd, rev, rev_start, rev_cnt,
+                                                               slots, count, defer, defer_n);
+  PIPNN_LAUNCHED("hp_merge_inst_kernel", c.st);
+  const int cap = merge_cap(l_max);
+  const int gsm = 4 * 2 * cap * (int)sizeof(uint64_t);
+  PIPNN_CUDA(cudaFuncSetAttribute(hp_merge_inst_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gsm));
+  hp_merge_inst_generic_kernel<<<(unsigned)(num_sms() * 4), 128, gsm, c.st>>>(l_max, cap, k, g.start, inv, fwd, rev,
+                                                                              rev_start, rev_cnt, slots, count, defer,
+                                                                              defer_n);
+  PIPNN_LAUNCHED("hp_merge_inst_generic_kernel", c.st);
+  return PIPNN_OK;
 }
 
 }  // namespace pipnn

@@ -37,7 +37,7 @@ pipnn_status csr_dist_segs(const int64_t* off, int64_t ns, int k, int self, Dist
 int64_t leaf_items_bound(int64_t n_leaves, int64_t n_inst);
 pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, const uint32_t* leaf_ids, int64_t n_leaves,
                             int64_t n_inst, int k, uint32_t* nbr, float* dist, Arena& ar, const Ctx& c,
-                            int64_t max_items = 0);
+                            int64_t max_items = 0, uint16_t* cols = nullptr);
 
 pipnn_status sketch_impl(const pipnn_points* X, int m, uint64_t seed, void* sketch, Arena& ar, const Ctx& c);
 
@@ -45,12 +45,13 @@ pipnn_status hashprune_impl(int m, int l_max, int64_t n, const void* sketch, boo
                             uint32_t* count, const uint32_t* owner, const uint32_t* cand, const float* dist,
                             int64_t n_edges, Arena& ar, const Ctx& c);
 
-// Fused edge emission for pipnn_build: the bidirected edges of the candidate lists nbr/dist ([I, k])
-// grouped by owner and merged into the reservoirs.
-pipnn_status hashprune_from_lists(int m, int l_max, int64_t n, const void* sketch, bool sk_int, uint64_t* slots,
-                                  uint32_t* count, const uint32_t* leaf_ids, int64_t n_inst, int k,
-                                  const uint32_t* nbr, const float* dist, int64_t* n_edges_dev, Arena& ar,
-                                  const Ctx& c);
+// Edge emission + merge for pipnn_build: the bidirected edges of the candidate lists (local columns cols and
+// distances dist, [I, k], of the leaves leaf_off/leaf_ids) grouped by owner instance inside each leaf and
+// merged into the reservoirs (which must start empty: count = 0).
+pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sketch, bool sk_int, uint64_t* slots,
+                                   uint32_t* count, const int64_t* leaf_off, int64_t n_leaves, const uint32_t* leaf_ids,
+                                   int64_t n_inst, int k, const uint16_t* cols, const float* dist, int max_leaf,
+                                   int64_t* n_edges_dev, Arena& ar, const Ctx& c);
 
 pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* slots, const uint32_t* count,
                               const pipnn_prune_params* p, uint64_t* row_ptr, uint32_t* col_idx, Arena& ar,

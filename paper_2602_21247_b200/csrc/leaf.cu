@@ -176,7 +176,7 @@ int64_t leaf_items_bound(int64_t n_leaves, int64_t n_inst) { return n_inst / 128
 
 pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, const uint32_t* leaf_ids, int64_t n_leaves,
                             int64_t n_inst, int k, uint32_t* nbr, float* dist, Arena& ar, const Ctx& c,
-                            int64_t max_items) {
+                            int64_t max_items, uint16_t* cols) {
   const int Kb = tiled_row_bytes(X);
   if (max_items <= 0) max_items = leaf_items_bound(n_leaves, n_inst);
   const int64_t seg_cap = std::min<int64_t>(n_leaves, max_items);
@@ -205,6 +205,7 @@ pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, cons
   a.n_items = n_items;
   a.col_ids = leaf_ids;
   a.out_idx = nbr;
+  a.out_col = cols;
   a.out_dist = dist;
   a.err = c.err;
   cudaEvent_t e0 = nullptr, e1 = nullptr;

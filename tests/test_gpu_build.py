@@ -25,12 +25,15 @@ def gpu_build(X, params, metric):
     return out.row_ptr.cpu().numpy(), out.col_idx.cpu().numpy().view(np.uint32), out.stats
 
 
-@pytest.mark.parametrize("n,c_max,fanout", [(20000, 1024, (2,)), (50000, 1024, (2,)), (20000, 256, (3,))])
-def test_build_u8_bit_exact(n, c_max, fanout):
+@pytest.mark.parametrize("n,c_max,fanout,l_max", [(20000, 1024, (2,), 128), (50000, 1024, (2,), 128),
+                                                  (20000, 256, (3,), 128), (20000, 1024, (2,), 8),
+                                                  (20000, 512, (2,), 24)])
+def test_build_u8_bit_exact(n, c_max, fanout, l_max):
+    # l_max = 8 / 24: reservoirs overflow, so the eviction rule of Alg. 3 runs in the build's merge
     cfg = synth.C2.scaled(n)
     X = synth.gen_points(cfg)
     p = cfg.params()
-    p.update(c_max=c_max, p_den=c_max, fanout=fanout, c_min=min(100, c_max // 4))
+    p.update(c_max=c_max, p_den=c_max, fanout=fanout, c_min=min(100, c_max // 4), l_max=l_max)
     rp, ci, stats = gpu_build(X, p, "l2")
     ref = O.build(O.Dataset(X), p)
     assert ref.check_failed == 0
