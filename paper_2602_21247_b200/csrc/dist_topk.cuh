@@ -42,7 +42,7 @@ namespace pipnn {
 struct TileSeg {
   int64_t id_off;  // ids[id_off + i] is the point id of local row i
   int64_t pos;     // first row position in the tiled buffer / norm array (multiple of 128)
-  int32_t pad;     // padded row count (multiple of 128): the plane stride of the [K/16][pad][16] layout
+  int32_t pad;     // padded row count (multiple of 128)
   int32_t rows;    // valid rows
 };
 
@@ -138,9 +138,10 @@ struct TileSched {
   int tile[2], ntiles[2];
   int w;
   int64_t n_items;
+  // every item's column tiles are computed twice (pass 1: threshold, pass 2: exact picks)
   __device__ __forceinline__ int ntiles_of(const DistTopkArgs& a, int64_t item) const {
     const WorkItem wi = a.items[item];
-    return (a.segs[wi.seg].b.rows + kDtTileN - 1) / kDtTileN;
+    return 2 * ((a.segs[wi.seg].b.rows + kDtTileN - 1) / kDtTileN);
   }
   __device__ __forceinline__ void init(const DistTopkArgs& a, int64_t n) {
     n_items = n;
@@ -230,23 +231,24 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
       while (sc.next(gi, item, t)) {
         const WorkItem w = args.items[item];
         const DistSeg S = args.segs[w.seg];
-        const int r0 = w.rb * 128, c0 = t * kDtTileN;
+        const int T = (S.b.rows + kDtTileN - 1) / kDtTileN;
+        const int r0 = w.rb * 128, c0 = (t % T) * kDtTileN;
         const int Nt = min(kDtTileN, (S.b.rows - c0 + 31) & ~31);
-        const uint8_t* srcA = args.Ta + S.a.pos * Kb + (int64_t)r0 * 16;
-        const uint8_t* srcB = args.Tb + S.b.pos * Kb + (int64_t)c0 * 16;
+        // block-major tiled layout: 128-row block j of a segment = KC planes x 2 KB, contiguous
+        const uint8_t* srcA = args.Ta + (S.a.pos / 128 + w.rb) * (int64_t)KC * 2048;
+        const uint8_t* srcB = args.Tb + (S.b.pos / 128 + c0 / 128) * (int64_t)KC * 2048;
+        (void)r0;
+        (void)Nt;
         for (int ch = 0; ch < nchunks; ++ch, ++g) {
           const int s = g % kDtStages;
           const uint32_t ph = (g / kDtStages) & 1;
           if (!ptx::mbar_wait(&bar_empty[s], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
           const int kc0 = ch * 8, kc1 = min(KC, kc0 + 8), ka1 = min(KCm, kc1);
           const int na = max(0, ka1 - kc0);
-          ptx::mbar_arrive_expect_tx(&bar_full[s], (uint32_t)(na * 2048 + (kc1 - kc0) * Nt * 16));
+          ptx::mbar_arrive_expect_tx(&bar_full[s], (uint32_t)((na + (kc1 - kc0)) * 2048));
           uint8_t* st = ring + s * kDtStageBytes;
-          for (int kc = kc0; kc < ka1; ++kc)
-            ptx::bulk_g2s(st + (kc - kc0) * 2048, srcA + (int64_t)kc * S.a.pad * 16, 2048, &bar_full[s]);
-          for (int kc = kc0; kc < kc1; ++kc)
-            ptx::bulk_g2s(st + kDtAB + (kc - kc0) * Nt * 16, srcB + (int64_t)kc * S.b.pad * 16, Nt * 16,
-                          &bar_full[s]);
+          if (na > 0) ptx::bulk_g2s(st, srcA + (int64_t)kc0 * 2048, na * 2048, &bar_full[s]);
+          ptx::bulk_g2s(st + kDtAB, srcB + (int64_t)kc0 * 2048, (kc1 - kc0) * 2048, &bar_full[s]);
         }
         sc.advance(args);
       }
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
       while (sc.next(gi, item, t)) {
         const WorkItem w = args.items[item];
         const int ncols = args.segs[w.seg].b.rows;
-        const int c0 = t * kDtTileN;
+        const int c0 = (t % ((ncols + kDtTileN - 1) / kDtTileN)) * kDtTileN;
         const int Nt = min(kDtTileN, (ncols - c0 + 31) & ~31);
         const uint32_t buf = 2 * gi + (tc[gi] & 1), use = tc[gi] >> 1;
         ++tc[gi];
@@ -283,8 +285,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
           for (int kc = kc0; kc < kc1; kc += 2) {
             const uint8_t* a_src = (kFold && kc >= KCm) ? sOnes + (kc - KCm) * 2048 : st + (kc - kc0) * 2048;
             const uint64_t ad = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(a_src), 2048, 128);
-            const uint64_t bd = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(st + kDtAB + (kc - kc0) * Nt * 16),
-                                                            (uint32_t)Nt * 16, 128);
+            const uint64_t bd = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(st + kDtAB + (kc - kc0) * 2048), 2048, 128);
             const uint32_t acc = (ch > 0 || kc > kc0) ? 1u : 0u;
             if (U8) ptx::mma_i8(dtm, ad, bd, idesc, acc);
             else ptx::mma_bf16(dtm, ad, bd, idesc, acc);
@@ -297,6 +298,14 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
     }();
   } else {
     // ------------------------------------------------------------ epilogue (2 warpgroups, one row per thread)
+    // Pass 1 (threshold): the row's keys in groups of 16 consecutive columns; the K1 = K + self smallest group
+    // minima (a sorted value list, min/max network, branch free) are K1 distinct elements, at most one of them
+    // the row itself, so U = the K1-th smallest group minimum bounds the K-th smallest key from above.
+    // Pass 2 (exact): the same tiles again; a key passes iff key <= U (until the exact list is full) or
+    // key < the list's K-th key, so only ~K+2 elements per row reach the (key, column) insertion.
+    // Passing keys are staged in SMEM and appended to the row's queue; the queue is drained into the sorted
+    // register list when it could overflow and at the row's end. Columns arrive in ascending order and the
+    // insertion is strict, so equal keys keep the smaller column (= smaller id).
     [&]() {
       const int ew = warp - 2;             // 0..7
       const int wg = ew >> 2;              // warpgroup
@@ -304,6 +313,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
       const int tid = q * 32 + lane;       // row within the 128-row block = TMEM lane
       const KT kInf = U8 ? (KT)0x7FFFFFFF : (KT)__int_as_float(0x7F800000);
       const KT kNegInf = U8 ? (KT)(-0x7FFFFFFF - 1) : (KT)__int_as_float(0xFF800000);
+      constexpr int VK = KMAX + 1;         // value list of pass 1: K + self <= KMAX + 1
       uint32_t* stg = reinterpret_cast<uint32_t*>(stg_base + wg * kDtStgBytes) + tid * kStgPitch;
       KT* my_qk = reinterpret_cast<KT*>(q_base + wg * kDtQBytes) + tid;
       uint16_t* my_qc = reinterpret_cast<uint16_t*>(q_base + wg * kDtQBytes + kQCap * 128 * 4) + tid;
@@ -314,9 +324,13 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
         const int r0 = w.rb * 128;
         const int row = r0 + tid;
         const int K = S.k;
+        const int K1 = K + (S.self ? 1 : 0);
         const int ncols = S.b.rows;
-        const int ntiles = (ncols + kDtTileN - 1) / kDtTileN;
-        // list of KMAX slots; the first KMAX-K hold -inf sentinels so that kk[KMAX-1] is the K-th best
+        const int T = (ncols + kDtTileN - 1) / kDtTileN;
+        KT vk[VK];
+#pragma unroll
+        for (int t = 0; t < VK; ++t) vk[t] = t < VK - K1 ? kNegInf : kInf;
+        // exact list of KMAX slots; the first KMAX-K hold -inf sentinels so that kk[KMAX-1] is the K-th best
         KT kk[KMAX];
         uint16_t ii[KMAX];
 #pragma unroll
@@ -324,15 +338,71 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
           kk[t] = t < KMAX - K ? kNegInf : kInf;
           ii[t] = 0xFFFFu;
         }
+        KT U = kInf;
         int qlen = 0;
         const int diag_chunk = S.self ? (r0 + q * 32) : -1;  // column base of this warp's diagonal chunk
-        for (int t = 0; t < ntiles; ++t, ++tcount) {
-          const int c0 = t * kDtTileN;
+        for (int t2 = 0; t2 < 2 * T; ++t2, ++tcount) {
+          const bool pass2 = t2 >= T;
+          const int c0 = (pass2 ? t2 - T : t2) * kDtTileN;
           const int Nt = min(kDtTileN, (ncols - c0 + 31) & ~31);
           const uint32_t buf = 2 * wg + (tcount & 1), use = tcount >> 1;
           if (!ptx::mbar_wait(&bar_acc_full[buf], use & 1, args.err, DERR_WAIT_TIMEOUT)) return;
           ptx::tc_fence_after();
           const uint32_t taddr = tmem + buf * kDtTileN + ((uint32_t)(q * 32) << 16);
+          if (t2 == T) {
+            U = vk[VK - 1];
+            if (U8 && U != kInf) U = U + 1;  // key <= U  <=>  key < U + 1
+            if (!U8) U = (KT)nextafterf((float)U, __int_as_float(0x7F800000));
+          }
+          if (!pass2) {
+            for (int j0 = 0; j0 < Nt; j0 += 32) {
+              // ---- pass 1: group minima of 16 keys, inserted into the value list
+              const int col0 = c0 + j0;
+              int4 nb4[8];
+              if (U8) {
+                const int4* p4 = reinterpret_cast<const int4*>((const int32_t*)args.nb + S.b.pos + col0);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) nb4[u] = __ldg(p4 + u);
+              }
+              uint32_t v[32];
+              ptx::tmem_ld32(taddr + j0, v);
+              ptx::tmem_ld_wait();
+              KT key[32];
+              if (U8) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                  key[4 * u + 0] = nb4[u].x - 2 * (int32_t)v[4 * u + 0];
+                  key[4 * u + 1] = nb4[u].y - 2 * (int32_t)v[4 * u + 1];
+                  key[4 * u + 2] = nb4[u].z - 2 * (int32_t)v[4 * u + 2];
+                  key[4 * u + 3] = nb4[u].w - 2 * (int32_t)v[4 * u + 3];
+                }
+              } else {
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) key[jj] = __uint_as_float(v[jj]);
+              }
+#pragma unroll
+              for (int gq = 0; gq < 2; ++gq) {
+                const KT* k8 = key + 16 * gq;
+                KT gm;
+                if (U8) {
+                  gm = min(min(min(k8[0], k8[1]), min(k8[2], k8[3])), min(min(k8[4], k8[5]), min(k8[6], k8[7])));
+                  gm = min(gm, min(min(min(k8[8], k8[9]), min(k8[10], k8[11])),
+                                   min(min(k8[12], k8[13]), min(k8[14], k8[15]))));
+                } else {
+                  gm = fminf(fminf(fminf(k8[0], k8[1]), fminf(k8[2], k8[3])), fminf(fminf(k8[4], k8[5]), fminf(k8[6], k8[7])));
+                  gm = fminf(gm, fminf(fminf(fminf(k8[8], k8[9]), fminf(k8[10], k8[11])),
+                                       fminf(fminf(k8[12], k8[13]), fminf(k8[14], k8[15]))));
+                }
+#pragma unroll
+                for (int t = VK - 1; t > 0; --t) {
+                  if (U8) vk[t] = max(vk[t - 1], min(vk[t], gm));
+                  else vk[t] = fmaxf(vk[t - 1], fminf(vk[t], gm));
+                }
+                if (U8) vk[0] = min(vk[0], gm);  // (no ?: — it would mix int and float types)
+                else vk[0] = fminf(vk[0], gm);
+              }
+            }
+          } else {
           for (int j0 = 0; j0 < Nt; j0 += 32) {
             const int col0 = c0 + j0;
             int4 nb4[8];
@@ -345,11 +415,10 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
             uint32_t v[32];
             ptx::tmem_ld32(taddr + j0, v);
             ptx::tmem_ld_wait();
-            // t_j = key_j - thr: its sign bit is the pass bit (key_j < thr). uint8: no overflow, since real keys
-            // lie in (-2^25, 2^25), padding keys are 0x3FFFFFFF and thr is a real key or 0x40000000 (list not
-            // full: everything passes). float: the sign of a difference is exact; thr = +inf passes everything.
-            // The mask is built with one funnel shift per element, bit j <-> column col0 + j.
-            const KT thr = kk[KMAX - 1];
+            // ---- pass 2: t_j = key_j - thr, its sign bit is the pass bit (key_j < thr). uint8: no overflow
+            // (real keys lie in (-2^25, 2^25), padding keys are 0x3FFFFFFF, thr is a real key + 1 or 0x40000000);
+            // float: the sign of a difference is exact. The mask is built with one funnel shift per element.
+            const KT thr = kk[KMAX - 1] != kInf ? kk[KMAX - 1] : U;
             const KT thr_eff = U8 ? (thr == kInf ? (KT)0x40000000 : thr) : thr;
             KT tk[32];
             uint32_t mask = 0;
@@ -393,9 +462,8 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
                 ++qlen;
               }
               __syncwarp();
-              if (__any_sync(0xffffffffu, kk[KMAX - 1] == kInf && qlen > 0))
-                topk_drain<KT, KMAX>(kk, ii, qlen, my_qk, my_qc);
             }
+          }
           }
           ptx::tc_fence_before();
           __syncwarp();

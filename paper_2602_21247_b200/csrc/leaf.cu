@@ -15,7 +15,7 @@ int tiled_row_bytes(const pipnn_points* X) {
 // ------------------------------------------------------------------ gather
 // One CTA per (segment, 128-row block). Phase 1: warp-per-row coalesced loads of the source rows into a
 // row-major SMEM staging tile (fp32 -> bf16 RNE for float data) + the row's squared norm. Phase 2: the
-// tile is written as [K/16][pad][16 B] planes — each plane slice of the block is 2 KB contiguous.
+// tile is written block-major as [K/16][128][16 B] planes: the whole 128-row block is contiguous.
 // Float rows end with the 16-element augment K-step of dist_topk.cuh: (t_hi, t_mid, t_lo, 0...) with
 // t = -||y||^2/2 (L2) or 0 (MIPS), split over three bf16 values; padding rows get t = -1e30 (u8 padding
 // rows get the norm kPadNormU8 instead), so padded columns never enter a top-k.
@@ -91,11 +91,11 @@ __global__ void __launch_bounds__(256) gather_tiled_kernel(const void* __restric
   }
   __syncthreads();
   const int KC = Kb >> 4;
-  uint8_t* dst = T + S.pos * (int64_t)Kb;
+  uint8_t* dst = T + (S.pos / 128 + w.rb) * (int64_t)KC * 2048;  // block-major: the block is contiguous
   for (int p = threadIdx.x; p < 128 * KC; p += 256) {
     const int kc = p >> 7, r = p & 127;
     const uint4 v = *(const uint4*)(st + r * pitch + kc * 16);
-    *(uint4*)(dst + ((int64_t)kc * S.pad + r0 + r) * 16) = v;
+    *(uint4*)(dst + (int64_t)kc * 2048 + r * 16) = v;
   }
 }
 

@@ -105,3 +105,18 @@ def test_leaf_pick_rejects_k16():
     ids = torch.arange(10, dtype=torch.int32, device="cuda")
     with pytest.raises(P().PipnnError):
         P().pipnn_leaf_pick(X, off, ids, 16)
+
+
+def test_leaf_pick_u8_large_distances_bit_exact():
+    # d = 512 with coordinates in {0, 255}: squared distances and ranking keys exceed 2^24 (not exact in fp32),
+    # so any float detour in the integer path would show up as a wrong pick or distance
+    rng = np.random.default_rng(11)
+    X = (rng.integers(0, 2, size=(3000, 512)) * 255).astype(np.uint8)
+    off, ids = random_leaves(len(X), [5, 130, 700, 1024], seed=4)
+    nbr, dist = run_gpu(X, "l2", off, ids, 8)
+    onbr, odist = O.leaf_pick(O.Dataset(X), off, ids, 8)
+    assert odist[onbr != UINT32_MAX].max() > 2 ** 24
+    assert np.array_equal(nbr, onbr)
+    ok = onbr != UINT32_MAX
+    # the ABI's dist is float32: the exact integer D rounded to nearest (pipnn.h)
+    assert np.array_equal(dist[ok], odist[ok].astype(np.float32))
