@@ -5,7 +5,8 @@ namespace pipnn {
 
 template <bool U8, bool MIPS, int KMAX>
 static pipnn_status launch_one(const DistTopkArgs& a, cudaStream_t st) {
-  const int smem = dt_smem_bytes(a.Kb);
+  const int smem = dt_smem_bytes(a.Kb, U8);
+  if (dt_stages(a.Kb, U8) < 2) return fail(PIPNN_EUNSUPPORTED, "dist_topk: row too long for the SMEM pipeline");
   auto* fn = dist_topk_kernel<U8, MIPS, KMAX>;
   PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   fn<<<num_sms(), kDtThreads, smem, st>>>(a);

@@ -10,13 +10,13 @@
 // Output D = ||x_i||^2 + key (u8), max(0, ||x_i||^2 + 2 key) (float L2), key (MIPS).
 //
 // Blackwell mapping:
-//   * persistent grid, one CTA per SM, 10 warps: warp 0 = bulk-copy producer, warp 1 = tcgen05.mma issuer
-//     (+ TMEM owner), warps 2-9 = two epilogue warpgroups. Work item = (segment, 128-row block); the CTA's
-//     items alternate between the two warpgroups, so each epilogue thread owns one row of its item for
+//   * persistent grid, one CTA per SM, 12 warps = two independent pipelines (producer warp g, tcgen05.mma
+//     issuer warp 2+g, epilogue warpgroup g = warps 4+4g..7+4g). Work item = (segment, 128-row block); the
+//     CTA's items alternate between the two pipelines, so each epilogue thread owns one row of its item for
 //     the whole item (its running top-K never leaves registers, no cross-thread merge);
-//   * a tile = 128 rows x <= 128 columns; the MMA warp issues the two warpgroups' tiles round-robin into
-//     four 128-column TMEM accumulators (two per warpgroup), so the MMA of a warpgroup's next tile overlaps
-//     the epilogue of its current one, and the two warpgroups hide each other's latencies;
+//   * a tile = 128 rows x <= 128 columns; each pipeline has two 128-column TMEM accumulators, so the MMA of
+//     a warpgroup's next tile overlaps the epilogue of its current one, and the two pipelines hide each
+//     other's latencies without waiting for each other;
 //   * every K-chunk (<= 128 B of every row) of a tile's A rows and B rows arrives by 1-D bulk copies (cp.async.bulk, TMA engine) into a 4-stage SMEM ring with mbarrier
 //     transaction counts; operands are in the K-major SWIZZLE_NONE canonical layout produced directly by
 //     the gather kernel ("tiled rows": [K/16][rows][16 B] per segment), so each plane slice is one copy;
@@ -77,24 +77,39 @@ struct DistTopkArgs {
   int* err;
 };
 
-constexpr int kDtStages = 4;
+constexpr int kDtMaxStages = 8;
 constexpr int kDtTileN = 128;                       // columns per tile (one TMEM accumulator)
-constexpr int kDtChunkB = 128;                      // bytes of K per stage and row
-constexpr int kDtAB = 128 * kDtChunkB;              // A (or B) bytes of one stage
-constexpr int kDtStageBytes = 2 * kDtAB;                 // A chunk + B chunk
-constexpr int kDtThreads = 320;
+constexpr int kDtStageBytes = 128 * 128;            // one B K-chunk: 128 columns x 128 B of K
+constexpr int kDtThreads = 384;
 constexpr int kTopkMax = 16;                        // max K (k, or the partition fanout)
-constexpr int kQCap = 32;                           // per-row candidate queue (SMEM) between drains
+constexpr int kQCap = 16;                           // per-row candidate queue (SMEM) between drains
 constexpr int kStgPitch = 36;                       // words per row of the key staging tile
 constexpr int32_t kPadNormU8 = 0x3FFFFFFF;          // norm of a padding row: key far above any real key
 constexpr float kPadKey = 1e30f;                    // float: column term of a padding row
 
-// dynamic SMEM: ring | per-warpgroup key staging [128][kStgPitch] | queues key [kQCap][128], col u16 [kQCap][128]
-constexpr int kDtRingBytes = kDtStages * kDtStageBytes;
+// dynamic SMEM: A block per warpgroup [2][KCa planes][128 rows][16 B] | B ring [NS][16 KB] |
+//               key staging per warpgroup [128][kStgPitch] | queues key [kQCap][128] + col u16 [kQCap][128] |
+//               ones tile (float augment)
 constexpr int kDtStgBytes = 128 * kStgPitch * 4;
 constexpr int kDtQBytes = kQCap * 128 * 6;
-__host__ __device__ constexpr int dt_smem_bytes(int /*Kb*/) {
-  return kDtRingBytes + 2 * kDtStgBytes + 2 * kDtQBytes + 4096 /*ones*/;
+constexpr int kDtSmemBudget = 227 * 1024 - 1024;
+__host__ __device__ constexpr int dt_a_planes(int Kb, bool u8) { return u8 ? Kb / 16 : Kb / 16 - 2; }
+// A slots per warpgroup: 2 (the next item's A block loads while the current item runs) when that still leaves
+// room for 4 B stages, else 1
+__host__ __device__ constexpr int dt_fixed_bytes_na(int Kb, bool u8, int na) {
+  return 2 * na * dt_a_planes(Kb, u8) * 2048 + 2 * kDtStgBytes + 2 * kDtQBytes + 4096;
+}
+__host__ __device__ constexpr int dt_a_slots(int Kb, bool u8) {
+  return dt_fixed_bytes_na(Kb, u8, 2) + 4 * kDtStageBytes <= kDtSmemBudget ? 2 : 1;
+}
+__host__ __device__ constexpr int dt_fixed_bytes(int Kb, bool u8) { return dt_fixed_bytes_na(Kb, u8, dt_a_slots(Kb, u8)); }
+__host__ __device__ constexpr int dt_stages(int Kb, bool u8) {
+  return (kDtSmemBudget - dt_fixed_bytes(Kb, u8)) / kDtStageBytes > kDtMaxStages
+             ? kDtMaxStages
+             : (kDtSmemBudget - dt_fixed_bytes(Kb, u8)) / kDtStageBytes;
+}
+__host__ __device__ constexpr int dt_smem_bytes(int Kb, bool u8) {
+  return dt_fixed_bytes(Kb, u8) + dt_stages(Kb, u8) * kDtStageBytes;
 }
 
 // Sorted insertion into a register list (ascending; equal keys keep the earlier entry first).
@@ -130,55 +145,13 @@ __device__ __forceinline__ void topk_drain(KT (&kk)[KMAX], uint16_t (&ii)[KMAX],
   qlen = 0;
 }
 
-// The deterministic tile schedule shared by the producer and the MMA warp: the CTA's items
-// it_j = blockIdx.x + j * gridDim.x go to warpgroup j & 1; tiles are issued round-robin between the two
-// warpgroups' current items (a warpgroup with no items left is skipped).
-struct TileSched {
-  int64_t it[2];
-  int tile[2], ntiles[2];
-  int w;
-  int64_t n_items;
-  // every item's column tiles are computed twice (pass 1: threshold, pass 2: exact picks)
-  __device__ __forceinline__ int ntiles_of(const DistTopkArgs& a, int64_t item) const {
-    const WorkItem wi = a.items[item];
-    return 2 * ((a.segs[wi.seg].b.rows + kDtTileN - 1) / kDtTileN);
-  }
-  __device__ __forceinline__ void init(const DistTopkArgs& a, int64_t n) {
-    n_items = n;
-    for (int g = 0; g < 2; ++g) {
-      it[g] = (int64_t)blockIdx.x + (int64_t)g * gridDim.x;
-      tile[g] = 0;
-      ntiles[g] = it[g] < n ? ntiles_of(a, it[g]) : 0;
-    }
-    w = 0;
-  }
-  // next tile: returns false when both warpgroups are done
-  __device__ __forceinline__ bool next(int& g, int64_t& item, int& t) {
-    if (it[w] >= n_items) {
-      w ^= 1;
-      if (it[w] >= n_items) return false;
-    }
-    g = w;
-    item = it[w];
-    t = tile[w];
-    return true;
-  }
-  __device__ __forceinline__ void advance(const DistTopkArgs& a) {
-    if (++tile[w] == ntiles[w]) {
-      it[w] += 2 * (int64_t)gridDim.x;
-      tile[w] = 0;
-      ntiles[w] = it[w] < n_items ? ntiles_of(a, it[w]) : 0;
-    }
-    w ^= 1;
-  }
-};
-
 template <bool U8, bool MIPS, int KMAX>
 __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopkArgs args) {
   using KT = typename std::conditional<U8, int32_t, float>::type;
   constexpr bool kFold = !U8;  // float paths fold the column term into an augmented MMA K-step
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t bar_full[kDtStages], bar_empty[kDtStages];
+  __shared__ __align__(8) uint64_t bar_full[2][kDtMaxStages / 2], bar_empty[2][kDtMaxStages / 2];
+  __shared__ __align__(8) uint64_t bar_a_full[2][2], bar_a_empty[2][2];  // [warpgroup][slot]
   __shared__ __align__(8) uint64_t bar_acc_full[4], bar_acc_empty[4];
   __shared__ uint32_t tmem_base_sh;
 
@@ -187,8 +160,12 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
   const int KC = Kb >> 4;                // 16-B K planes per row (incl. the 2 augment planes for float)
   const int KCm = kFold ? KC - 2 : KC;   // planes of the coordinates themselves
   const int nchunks = (KC + 7) >> 3;     // K-chunks of <= 8 planes (128 B) per tile
-  uint8_t* ring = smem;
-  uint8_t* stg_base = smem + kDtRingBytes;
+  const int NS = dt_stages(Kb, U8) / 2;  // B stages per warpgroup pipeline
+  const int KCa = dt_a_planes(Kb, U8);   // == KCm: the A planes held in SMEM
+  const int NA = dt_a_slots(Kb, U8);     // A slots per warpgroup
+  uint8_t* sA = smem;                    // [2 warpgroups][NA][KCa][128][16]
+  uint8_t* ring = sA + 2 * NA * KCa * 2048;  // [2 warpgroups][NS][16 KB]
+  uint8_t* stg_base = ring + dt_stages(Kb, U8) * kDtStageBytes;
   uint8_t* q_base = stg_base + 2 * kDtStgBytes;
   uint8_t* sOnes = q_base + 2 * kDtQBytes;  // float: [2 planes][128 rows][16 B] A-side augment
 
@@ -202,9 +179,15 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
     ptx::fence_proxy_async_smem();
   }
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kDtStages; ++s) {
-      ptx::mbar_init(&bar_full[s], 1);
-      ptx::mbar_init(&bar_empty[s], 1);
+    for (int g = 0; g < 2; ++g) {
+      for (int s = 0; s < NS; ++s) {
+        ptx::mbar_init(&bar_full[g][s], 1);
+        ptx::mbar_init(&bar_empty[g][s], 1);
+      }
+      for (int a = 0; a < 2; ++a) {
+        ptx::mbar_init(&bar_a_full[g][a], 1);
+        ptx::mbar_init(&bar_a_empty[g][a], 1);
+      }
     }
     for (int b = 0; b < 4; ++b) {
       ptx::mbar_init(&bar_acc_full[b], 1);
@@ -212,88 +195,95 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc(&tmem_base_sh, 512);
+  if (warp == 2) ptx::tmem_alloc(&tmem_base_sh, 512);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   const int64_t n_items = *args.n_items;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer (one lane)
+  // Two independent pipelines, one per epilogue warpgroup g: producer warp g, MMA warp 2 + g, TMEM
+  // accumulators 2g and 2g + 1, its own A slots and B ring. Warpgroup g takes the CTA's items
+  // it = blockIdx.x + (2 j + g) * gridDim.x; every item's column tiles are computed twice (pass 1: threshold,
+  // pass 2: exact picks).
+  if (warp < 2) {
+    // ------------------------------------------------------------ producer of pipeline g (one lane)
+    const int g = warp;
     if (lane == 0) [&]() {
-      TileSched sc;
-      sc.init(args, n_items);
-      uint32_t g = 0;
-      int gi;
-      int64_t item;
-      int t;
-      while (sc.next(gi, item, t)) {
-        const WorkItem w = args.items[item];
+      uint32_t sg = 0, ia = 0;
+      uint8_t* my_ring = ring + g * NS * kDtStageBytes;
+      for (int64_t it = (int64_t)blockIdx.x + (int64_t)g * gridDim.x; it < n_items; it += 2 * (int64_t)gridDim.x) {
+        const WorkItem w = args.items[it];
         const DistSeg S = args.segs[w.seg];
         const int T = (S.b.rows + kDtTileN - 1) / kDtTileN;
-        const int r0 = w.rb * 128, c0 = (t % T) * kDtTileN;
-        const int Nt = min(kDtTileN, (S.b.rows - c0 + 31) & ~31);
-        // block-major tiled layout: 128-row block j of a segment = KC planes x 2 KB, contiguous
-        const uint8_t* srcA = args.Ta + (S.a.pos / 128 + w.rb) * (int64_t)KC * 2048;
-        const uint8_t* srcB = args.Tb + (S.b.pos / 128 + c0 / 128) * (int64_t)KC * 2048;
-        (void)r0;
-        (void)Nt;
-        for (int ch = 0; ch < nchunks; ++ch, ++g) {
-          const int s = g % kDtStages;
-          const uint32_t ph = (g / kDtStages) & 1;
-          if (!ptx::mbar_wait(&bar_empty[s], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
-          const int kc0 = ch * 8, kc1 = min(KC, kc0 + 8), ka1 = min(KCm, kc1);
-          const int na = max(0, ka1 - kc0);
-          ptx::mbar_arrive_expect_tx(&bar_full[s], (uint32_t)((na + (kc1 - kc0)) * 2048));
-          uint8_t* st = ring + s * kDtStageBytes;
-          if (na > 0) ptx::bulk_g2s(st, srcA + (int64_t)kc0 * 2048, na * 2048, &bar_full[s]);
-          ptx::bulk_g2s(st + kDtAB, srcB + (int64_t)kc0 * 2048, (kc1 - kc0) * 2048, &bar_full[s]);
+        // the item's A block stays in SMEM for all of its tiles (both passes); block-major tiled layout:
+        // 128-row block j of a segment = KC planes x 2 KB, contiguous
+        {
+          const int slot = (int)(ia % NA);
+          const uint32_t ph = (ia / NA) & 1;
+          ++ia;
+          if (!ptx::mbar_wait(&bar_a_empty[g][slot], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
+          ptx::mbar_arrive_expect_tx(&bar_a_full[g][slot], (uint32_t)(KCa * 2048));
+          ptx::bulk_g2s(sA + (g * NA + slot) * KCa * 2048, args.Ta + (S.a.pos / 128 + w.rb) * (int64_t)KC * 2048,
+                        KCa * 2048, &bar_a_full[g][slot]);
         }
-        sc.advance(args);
+        for (int t = 0; t < 2 * T; ++t) {
+          const int c0 = (t % T) * kDtTileN;
+          const uint8_t* srcB = args.Tb + (S.b.pos / 128 + c0 / 128) * (int64_t)KC * 2048;
+          for (int ch = 0; ch < nchunks; ++ch, ++sg) {
+            const int s = sg % NS;
+            const uint32_t ph = (sg / NS) & 1;
+            if (!ptx::mbar_wait(&bar_empty[g][s], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
+            const int kc0 = ch * 8, kc1 = min(KC, kc0 + 8);
+            ptx::mbar_arrive_expect_tx(&bar_full[g][s], (uint32_t)((kc1 - kc0) * 2048));
+            ptx::bulk_g2s(my_ring + s * kDtStageBytes, srcB + (int64_t)kc0 * 2048, (kc1 - kc0) * 2048,
+                          &bar_full[g][s]);
+          }
+        }
       }
     }();
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (one lane)
+  } else if (warp < 4) {
+    // ------------------------------------------------------------ MMA issuer of pipeline g (one lane)
+    const int g = warp - 2;
     if (lane == 0) [&]() {
-      TileSched sc;
-      sc.init(args, n_items);
-      uint32_t g = 0;
-      uint32_t tc[2] = {0u, 0u};  // tiles issued per warpgroup
-      int gi;
-      int64_t item;
-      int t;
-      while (sc.next(gi, item, t)) {
-        const WorkItem w = args.items[item];
+      uint32_t sg = 0, ia = 0, tc = 0;
+      const uint8_t* my_ring = ring + g * NS * kDtStageBytes;
+      for (int64_t it = (int64_t)blockIdx.x + (int64_t)g * gridDim.x; it < n_items; it += 2 * (int64_t)gridDim.x) {
+        const WorkItem w = args.items[it];
         const int ncols = args.segs[w.seg].b.rows;
-        const int c0 = (t % ((ncols + kDtTileN - 1) / kDtTileN)) * kDtTileN;
-        const int Nt = min(kDtTileN, (ncols - c0 + 31) & ~31);
-        const uint32_t buf = 2 * gi + (tc[gi] & 1), use = tc[gi] >> 1;
-        ++tc[gi];
-        if (!ptx::mbar_wait(&bar_acc_empty[buf], (use & 1) ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
-        ptx::tc_fence_after();
-        // float: negate B (bit 14), so the accumulator is -x.y + (column term)
-        const uint32_t idesc = U8 ? ptx::idesc_u8_s32(128, Nt) : (ptx::idesc_bf16_f32(128, Nt) | (1u << 14));
-        const uint32_t dtm = tmem + buf * kDtTileN;
-        for (int ch = 0; ch < nchunks; ++ch, ++g) {
-          const int s = g % kDtStages;
-          const uint32_t ph = (g / kDtStages) & 1;
-          if (!ptx::mbar_wait(&bar_full[s], ph, args.err, DERR_WAIT_TIMEOUT)) return;
+        const int T = (ncols + kDtTileN - 1) / kDtTileN;
+        const int slot = (int)(ia % NA);
+        if (!ptx::mbar_wait(&bar_a_full[g][slot], (ia / NA) & 1, args.err, DERR_WAIT_TIMEOUT)) return;
+        ++ia;
+        const uint8_t* a_base = sA + (g * NA + slot) * KCa * 2048;
+        for (int t = 0; t < 2 * T; ++t, ++tc) {
+          const int c0 = (t % T) * kDtTileN;
+          const int Nt = min(kDtTileN, (ncols - c0 + 31) & ~31);
+          const uint32_t buf = 2 * g + (tc & 1), use = tc >> 1;
+          if (!ptx::mbar_wait(&bar_acc_empty[buf], (use & 1) ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
           ptx::tc_fence_after();
-          const int kc0 = ch * 8, kc1 = min(KC, kc0 + 8);
-          const uint8_t* st = ring + s * kDtStageBytes;
-          for (int kc = kc0; kc < kc1; kc += 2) {
-            const uint8_t* a_src = (kFold && kc >= KCm) ? sOnes + (kc - KCm) * 2048 : st + (kc - kc0) * 2048;
-            const uint64_t ad = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(a_src), 2048, 128);
-            const uint64_t bd = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(st + kDtAB + (kc - kc0) * 2048), 2048, 128);
-            const uint32_t acc = (ch > 0 || kc > kc0) ? 1u : 0u;
-            if (U8) ptx::mma_i8(dtm, ad, bd, idesc, acc);
-            else ptx::mma_bf16(dtm, ad, bd, idesc, acc);
+          // float: negate B (bit 14), so the accumulator is -x.y + (column term)
+          const uint32_t idesc = U8 ? ptx::idesc_u8_s32(128, Nt) : (ptx::idesc_bf16_f32(128, Nt) | (1u << 14));
+          const uint32_t dtm = tmem + buf * kDtTileN;
+          for (int ch = 0; ch < nchunks; ++ch, ++sg) {
+            const int s = sg % NS;
+            if (!ptx::mbar_wait(&bar_full[g][s], (sg / NS) & 1, args.err, DERR_WAIT_TIMEOUT)) return;
+            ptx::tc_fence_after();
+            const int kc0 = ch * 8, kc1 = min(KC, kc0 + 8);
+            const uint8_t* st = my_ring + s * kDtStageBytes;
+            for (int kc = kc0; kc < kc1; kc += 2) {
+              const uint8_t* a_src = (kFold && kc >= KCm) ? sOnes + (kc - KCm) * 2048 : a_base + kc * 2048;
+              const uint64_t ad = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(a_src), 2048, 128);
+              const uint64_t bd = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(st + (kc - kc0) * 2048), 2048, 128);
+              const uint32_t acc = (ch > 0 || kc > kc0) ? 1u : 0u;
+              if (U8) ptx::mma_i8(dtm, ad, bd, idesc, acc);
+              else ptx::mma_bf16(dtm, ad, bd, idesc, acc);
+            }
+            ptx::mma_commit(&bar_empty[g][s]);
           }
-          ptx::mma_commit(&bar_empty[s]);
+          ptx::mma_commit(&bar_acc_full[buf]);
         }
-        ptx::mma_commit(&bar_acc_full[buf]);
-        sc.advance(args);
+        ptx::mma_commit(&bar_a_empty[g][slot]);  // all of the item's MMAs issued: release its A block
       }
     }();
   } else {
@@ -307,7 +297,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
     // register list when it could overflow and at the row's end. Columns arrive in ascending order and the
     // insertion is strict, so equal keys keep the smaller column (= smaller id).
     [&]() {
-      const int ew = warp - 2;             // 0..7
+      const int ew = warp - 4;             // 0..7
       const int wg = ew >> 2;              // warpgroup
       const int q = warp & 3;              // TMEM lane quadrant of this warp (hardware: warp id % 4)
       const int tid = q * 32 + lane;       // row within the 128-row block = TMEM lane
@@ -441,7 +431,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
             }
             if (col0 == diag_chunk) mask &= ~(1u << lane);  // self exclusion (by id: the diagonal element)
             if (__any_sync(0xffffffffu, mask != 0)) {
-              // room for this chunk's passes (a drain empties the queue)
+              // room for this chunk's passes (a drain empties the queue; a chunk can still exceed kQCap)
               if (__any_sync(0xffffffffu, qlen + __popc(mask) > kQCap)) topk_drain<KT, KMAX>(kk, ii, qlen, my_qk, my_qc);
 #pragma unroll
               for (int u = 0; u < 8; ++u) {
@@ -455,6 +445,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
               while (mask) {
                 const int jj = __ffs(mask) - 1;
                 mask &= mask - 1;
+                if (qlen == kQCap) topk_drain<KT, KMAX>(kk, ii, qlen, my_qk, my_qc);  // (per lane) never overflow
                 // uint8 stages t = key - thr (key = t + thr exactly); float stages the key itself
                 my_qk[qlen * 128] = U8 ? (KT)(reinterpret_cast<const int32_t*>(stg)[jj] + (int32_t)thr_eff)
                                        : (KT)reinterpret_cast<const float*>(stg)[jj];
@@ -503,7 +494,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);
   }
