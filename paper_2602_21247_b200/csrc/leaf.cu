@@ -13,8 +13,8 @@ int tiled_row_bytes(const pipnn_points* X) {
 }
 
 // ------------------------------------------------------------------ gather
-// One CTA per (segment, 128-row block). Phase 1: warp-per-row coalesced loads of the source rows into a
-// row-major SMEM staging tile (fp32 -> bf16 RNE for float data) + the row's squared norm. Phase 2: the
+// One CTA per (segment, 128-row block). Phase 1: 16-B vector loads of the source rows (a lane group per row)
+// into a row-major SMEM staging tile (fp32 -> bf16 RNE for float data) + the row's squared norm. Phase 2: the
 // tile is written block-major as [K/16][128][16 B] planes: the whole 128-row block is contiguous.
 // Float rows end with the 16-element augment K-step of dist_topk.cuh: (t_hi, t_mid, t_lo, 0...) with
 // t = -||y||^2/2 (L2) or 0 (MIPS), split over three bf16 values; padding rows get t = -1e30 (u8 padding
@@ -34,44 +34,73 @@ __global__ void __launch_bounds__(256) gather_tiled_kernel(const void* __restric
   const int pitch = Kb + 16;  // staging row pitch (bank-conflict-free 16-B column reads)
   const int r0 = w.rb * 128;
   const int ldm = U8 ? Kb : (Kb - 32) / 2;  // elements of the coordinate part
-  for (int r = warp; r < 128; r += 8) {
+  // Phase 1: a group of L = Kb/16 (uint8) or ldm/8 (float) lanes per row, one 16-B destination chunk per
+  // lane (16 bytes, or 8 floats -> 8 bf16), loaded with 16-B vector loads when the row is aligned; the
+  // row's squared norm by a shuffle reduction inside the lane group (int32 exact / fp32 of the bf16 values).
+  const int cpr = U8 ? (Kb >> 4) : (ldm >> 3);  // 16-B destination chunks per row (<= 32)
+  int L = 1;
+  while (L < cpr) L <<= 1;  // lanes per row (power of two, <= 32)
+  const int rpw = 32 / L;   // rows per warp step
+  const int sub = lane / L, ch = lane % L;
+  const bool vec = U8 ? ((d & 15) == 0 && (ld & 15) == 0) : ((d & 3) == 0 && (ld & 3) == 0);
+  for (int rbase = warp * rpw; rbase < 128; rbase += 8 * rpw) {
+    const int r = rbase + sub;
     const int local = r0 + r;
     uint8_t* srow = st + r * pitch;
-    float nf = 0.0f;
-    int ni = 0;
     const bool valid = local < S.rows;
-    if (valid) {
-      const int64_t id = ids ? (int64_t)ids[S.id_off + local] : (S.id_off + local);
-      if (U8) {
-        const uint8_t* src = (const uint8_t*)Xv + id * ld;
-        for (int j = lane; j < Kb; j += 32) {
-          const int v = j < d ? src[j] : 0;
-          srow[j] = (uint8_t)v;
-          ni += v * v;
-        }
-      } else {
-        const float* src = (const float*)Xv + id * ld;
-        uint16_t* drow = (uint16_t*)srow;
-        bool bad = false;
-        for (int j = lane; j < ldm; j += 32) {
-          const float x = j < d ? src[j] : 0.0f;
-          bad |= !isfinite(x);
-          const uint16_t b = f32_to_bf16_rne(x);
-          drow[j] = b;
-          const float xb = __uint_as_float((uint32_t)b << 16);
-          nf = fmaf(xb, xb, nf);
-        }
-        if (bad) atomicExch(err, DERR_NONFINITE);
-      }
-    } else {
-      for (int j = lane * 4; j < Kb; j += 128) *(uint32_t*)(srow + j) = 0u;
-    }
+    int ni = 0;
+    float nf = 0.0f;
+    if (ch < cpr) {
+      uint4 out = make_uint4(0u, 0u, 0u, 0u);
+      if (valid) {
+        const int64_t id = ids ? (int64_t)ids[S.id_off + local] : (S.id_off + local);
+        if (U8) {
+          const uint8_t* src = (const uint8_t*)Xv + id * ld;
+          if (vec) {
+            if (ch * 16 < d) out = __ldg((const uint4*)src + ch);
+          } else {
+            uint32_t wv[4] = {0u, 0u, 0u, 0u};
+            for (int t = 0; t < 16; ++t)
+              if (ch * 16 + t < d) wv[t >> 2] |= (uint32_t)src[ch * 16 + t] << (8 * (t & 3));
+            out = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+          }
+          ni = __dp4a(out.x, out.x, 0u);
+          ni = __dp4a(out.y, out.y, (uint32_t)ni);
+          ni = __dp4a(out.z, out.z, (uint32_t)ni);
+          ni = __dp4a(out.w, out.w, (uint32_t)ni);
+        } else {
+          const float* src = (const float*)Xv + id * ld;
+          float f[8];
+          if (vec && ch * 8 + 8 <= d) {
+            const float4 a = __ldg((const float4*)(src + ch * 8));
+            const float4 b = __ldg((const float4*)(src + ch * 8 + 4));
+            f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+          } else {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+            for (int t = 0; t < 8; ++t) f[t] = ch * 8 + t < d ? __ldg(src + ch * 8 + t) : 0.0f;
+          }
+          bool bad = false;
+          uint32_t wv[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const uint16_t lo = f32_to_bf16_rne(f[2 * t]), hi = f32_to_bf16_rne(f[2 * t + 1]);
+            bad |= !isfinite(f[2 * t]) || !isfinite(f[2 * t + 1]);
+            const float xl = __uint_as_float((uint32_t)lo << 16), xh = __uint_as_float((uint32_t)hi << 16);
+            nf = fmaf(xl, xl, nf);
+            nf = fmaf(xh, xh, nf);
+            wv[t] = (uint32_t)lo | ((uint32_t)hi << 16);
+          }
+          if (bad) atomicExch(err, DERR_NONFINITE);
+          out = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+      }
+      *(uint4*)(srow + ch * 16) = out;
+    }
+    for (int o = L >> 1; o > 0; o >>= 1) {
       ni += __shfl_xor_sync(0xffffffffu, ni, o);
       nf += __shfl_xor_sync(0xffffffffu, nf, o);
     }
-    if (lane == 0) {
+    if (ch == 0) {
       if (U8) {
         ((int32_t*)nrm)[S.pos + local] = valid ? ni : kPadNormU8;
       } else {
