@@ -640,9 +640,40 @@ __global__ void csr_copy_kernel(int64_t n, int R, const uint32_t* __restrict__ n
   }
 }
 
+// Processing order of the final prune in pipnn_build: every point once, at its first instance in leaf order,
+// so the warps of an SM at any moment gather candidate rows of the same few leaves (L2 reuse).
+__global__ void first_instance_kernel(const uint32_t* __restrict__ leaf_ids, int64_t I, uint32_t* __restrict__ first) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x)
+    atomicMin(&first[leaf_ids[i]], (uint32_t)i);
+}
+__global__ void first_flag_kernel(const uint32_t* __restrict__ leaf_ids, int64_t I, const uint32_t* __restrict__ first,
+                                  uint8_t* __restrict__ flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = first[leaf_ids[i]] == (uint32_t)i;
+}
+
+pipnn_status leaf_order(const uint32_t* leaf_ids, int64_t n_inst, int64_t n, uint32_t* order, uint32_t* order_n,
+                        Arena& ar, const Ctx& c) {
+  uint32_t* first = ar.take<uint32_t>(n);
+  uint8_t* flag = ar.take<uint8_t>(std::max<int64_t>(1, n_inst));
+  size_t tb = 0;
+  cub::DeviceSelect::Flagged(nullptr, tb, leaf_ids, flag, order, order_n, (int)std::max<int64_t>(1, n_inst));
+  void* tmp = ar.take<uint8_t>(tb);
+  if (ar.measuring()) return PIPNN_OK;
+  if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (leaf_order)");
+  PIPNN_CUDA(cudaMemsetAsync(first, 0xFF, (size_t)n * sizeof(uint32_t), c.st));
+  const int64_t g = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_inst, 256), num_sms() * 32));
+  first_instance_kernel<<<(unsigned)g, 256, 0, c.st>>>(leaf_ids, n_inst, first);
+  PIPNN_LAUNCHED("first_instance_kernel", c.st);
+  first_flag_kernel<<<(unsigned)g, 256, 0, c.st>>>(leaf_ids, n_inst, first, flag);
+  PIPNN_LAUNCHED("first_flag_kernel", c.st);
+  PIPNN_CUDA(cub::DeviceSelect::Flagged(tmp, tb, leaf_ids, flag, order, order_n, (int)n_inst, c.st));
+  return PIPNN_OK;
+}
+
 pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* slots, const uint32_t* count,
                               const pipnn_prune_params* p, uint64_t* row_ptr, uint32_t* col_idx, Arena& ar,
-                              const Ctx& c) {
+                              const Ctx& c, const uint32_t* order, const uint32_t* order_n) {
   const int64_t n = X->n;
   const int R = p->R;
   uint32_t* nbr_tmp = ar.take<uint32_t>((size_t)n * R);
@@ -665,8 +696,9 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
   const int smem1 = (int)(L1.per_warp + pair_bytes);
   if (p->final_prune) {
     // tiers of the Gram path: <= 31, <= 63, <= 127 candidates; anything larger -> generic kernel
-    const uint32_t* in_list = nullptr;
-    const uint32_t* in_n = nullptr;
+    const uint32_t* in_list = order;  // nullptr: points in id order
+    const uint32_t* in_n = order_n;
+    bool first_tier = true;
 #define GP_TIER(U, M, CPV, T)                                                                                      \
   do {                                                                                                             \
     const GpLayout GL = gp_layout(X->d, U, CPV);                                                                   \
@@ -675,7 +707,8 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
     const int sm = (int)(w * GL.per_warp);                                                                         \
     auto* fn = fp_gram_kernel<U, M, CPV>;                                                                          \
     PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));                         \
-    const int64_t blocks = in_list ? (int64_t)num_sms() * 4 : std::min<int64_t>(ceil_div(n, w), num_sms() * 32);   \
+    const int64_t blocks = first_tier ? std::min<int64_t>(ceil_div(n, w), num_sms() * 32) : (int64_t)num_sms() * 4; \
+    first_tier = false;                                                                                            \
     fn<<<(unsigned)blocks, 32 * w, sm, c.st>>>(X->data, n, X->d, X->ld, l_max, slots, count, R, p->alpha_num,      \
                                                p->alpha_den, nbr_tmp, deg, in_list, in_n, defer + (T) * n,        \
                                                defer_n + (T));                                                     \

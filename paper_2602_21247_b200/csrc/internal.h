@@ -53,9 +53,14 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
                                    int64_t n_inst, int k, const uint16_t* cols, const float* dist, int max_leaf,
                                    int64_t* n_edges_dev, Arena& ar, const Ctx& c);
 
+// order/order_n (device, nullable): the points to prune, in this order (pipnn_build: leaf order, see
+// leaf_order); without it every point in id order.
 pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* slots, const uint32_t* count,
                               const pipnn_prune_params* p, uint64_t* row_ptr, uint32_t* col_idx, Arena& ar,
-                              const Ctx& c);
+                              const Ctx& c, const uint32_t* order = nullptr, const uint32_t* order_n = nullptr);
+// Every point once, at its first instance in leaf_ids order (order[0..*order_n)).
+pipnn_status leaf_order(const uint32_t* leaf_ids, int64_t n_inst, int64_t n, uint32_t* order, uint32_t* order_n,
+                        Arena& ar, const Ctx& c);
 
 pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params* p, int64_t* leaf_off,
                             int64_t leaf_off_cap, uint32_t* leaf_ids, int64_t leaf_ids_cap, int64_t* n_leaves_h,
