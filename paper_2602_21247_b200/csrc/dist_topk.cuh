@@ -74,6 +74,9 @@ struct DistTopkArgs {
   uint32_t* out_idx;       // output picks (column ids), layout given by DistSeg::out_off / ostride; nullable
   uint16_t* out_col;       // nullable: the picks' local column indices (same layout; 0xFFFF = none)
   float* out_dist;         // output D, same layout, nullable
+  const uint32_t* row_ids; // with out_rowid: id of local row i = row_ids[a.id_off + i]
+  uint32_t* out_rowid;     // nullable: the row's id next to every output slot (same layout)
+  uint32_t* out_cnt;       // nullable: out_cnt[pick id] += 1 for every valid pick (group-by histogram)
   int* err;
 };
 
@@ -476,11 +479,17 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
               if (MIPS) D = (float)key;
               else if (U8) D = (float)(na + key);
               else D = fmaxf(fmaf(2.0f, (float)key, (float)na), 0.0f);
-              if (args.out_idx) args.out_idx[obase + o] = args.col_ids ? args.col_ids[S.b.id_off + col] : col;
+              const uint32_t pid = args.col_ids ? args.col_ids[S.b.id_off + col] : col;
+              if (args.out_idx) args.out_idx[obase + o] = pid;
               if (args.out_col) args.out_col[obase + o] = (uint16_t)col;
               if (args.out_dist) args.out_dist[obase + o] = D;
+              if (args.out_cnt) atomicAdd(&args.out_cnt[pid], 1u);
               ++o;
             }
+          }
+          if (args.out_rowid) {
+            const uint32_t rid = args.row_ids[S.a.id_off + row];
+            for (int t = 0; t < S.ostride; ++t) args.out_rowid[obase + t] = rid;
           }
           for (; o < S.ostride; ++o) {
             if (args.out_idx) args.out_idx[obase + o] = 0xFFFFFFFFu;

@@ -3,14 +3,17 @@
 // depth are processed together, which is equivalent because every subproblem is carved independently
 // from its own key (docs/DETERMINISM.md). Per level:
 //   1. leaders: the l_g members with the smallest mix(K_g, id) (line 2, "SampleLeaders"): a threshold
-//      filter (count pass + scatter pass) keeps ~4 l_g + 64 candidates per subproblem, a segmented sort
-//      orders them, the first l_g are sorted by id. mix(K, .) is injective, so the selection is exact;
-//      a subproblem whose filter kept fewer than l_g candidates is redone with no filter.
+//      filter keeps ~4 l_g + 64 candidates per subproblem in a segment of capacity 8 l_g + 256, a
+//      (segmented) sort orders them, the first l_g are sorted by id. mix(K, .) is injective, so the selection
+//      is exact; if any subproblem's filter kept more than its capacity or fewer than l_g candidates, the
+//      level is redone without the filter.
 //   2. nearest leaders (lines 5-9): members and leaders are gathered into the tiled MMA layout and the
 //      dist_topk kernel (tcgen05, the same kernel as the leaf pick) returns each member's f_g nearest
 //      leaders by (D, leader id) — leaders are in ascending id order, so "smaller column" = "smaller id".
-//   3. group-by: (child, id) pairs in member order, stable radix sort by child -> every child ascending.
-//   4. one device->host copy of the child sizes and leader ids; the host applies the merge rule of small
+//   3. group-by: the distance kernel writes (child, id) pairs in member order and the child histogram;
+//      a stable radix sort by child -> every child ascending.
+//   4. one device->host copy of the child sizes and leader ids (the level's only synchronisation); the
+//      host applies the merge rule of small
 //      siblings (line 10, R15), the base case, the degenerate-input guard, and schedules
 //      (a) leaf jobs (plain copies, or sorted + deduplicated unions for merged groups) and
 //      (b) the next level's subproblems (children larger than C_max, key mix(K_g, l + 1)).
@@ -33,6 +36,8 @@ struct PGroup {       // device view of an open subproblem at the current level
   int64_t lead_off;   // leader buffer offset (= child base)
   int64_t pair_off;   // (member, slot) pair offset
   int32_t l, f;
+  int32_t cap;        // candidate segment capacity
+  int32_t pad_;
 };
 
 struct LeafPart {
@@ -62,10 +67,13 @@ __device__ __forceinline__ int find_group(const int64_t* __restrict__ cbase, int
   return lo;
 }
 
-template <bool kScatter>
+// Leader candidates: members whose priority mix(K_g, id) is below the group's filter threshold, scattered into
+// the group's candidate segment [cand_off, cand_off + cap) (the rest of the segment stays ~0 and sorts last).
+// A group whose filter kept more than cap or fewer than l candidates raises *redo (the level is then redone
+// without the filter, exactly).
 __global__ void prio_kernel(const PGroup* __restrict__ gs, const int64_t* __restrict__ cbase, int G, int64_t M,
                             const uint32_t* __restrict__ mem, uint32_t* __restrict__ cnt, uint64_t* __restrict__ ck,
-                            uint32_t* __restrict__ cv) {
+                            uint32_t* __restrict__ cv, int* __restrict__ redo) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M; e += (int64_t)gridDim.x * blockDim.x) {
     const int g = find_group(cbase, G, e);
     const PGroup& p = gs[g];
@@ -73,12 +81,25 @@ __global__ void prio_kernel(const PGroup* __restrict__ gs, const int64_t* __rest
     const uint64_t pri = mix64(p.key, id);
     if (pri < p.thr || p.thr == ~0ull) {
       const uint32_t slot = atomicAdd(&cnt[g], 1u);
-      if (kScatter) {
+      if (slot < (uint32_t)p.cap) {
         ck[p.cand_off + slot] = pri;
         cv[p.cand_off + slot] = id;
+      } else {
+        *redo = 1;
       }
     }
   }
+}
+
+__global__ void prio_check_kernel(const PGroup* __restrict__ gs, int G, const uint32_t* __restrict__ cnt,
+                                  int* __restrict__ redo) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < G && cnt[g] < (uint32_t)gs[g].l) *redo = 1;
+}
+
+__global__ void iota_kernel(uint32_t* __restrict__ out, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    out[e] = (uint32_t)e;
 }
 
 // first l_g sorted candidates -> leaders (then sorted by id with a segmented sort)
@@ -88,31 +109,6 @@ __global__ void take_leaders_kernel(const PGroup* __restrict__ gs, int G, const 
   if (g >= G) return;
   const PGroup& p = gs[g];
   for (int j = threadIdx.x; j < p.l; j += blockDim.x) lead[p.lead_off + j] = cv_sorted[p.cand_off + j];
-}
-
-// (child, id) pairs in member order from the assignment; child sizes by atomics
-__global__ void pairs_kernel(const PGroup* __restrict__ gs, const int64_t* __restrict__ cbase, int G, int64_t M,
-                             const uint32_t* __restrict__ mem, const uint32_t* __restrict__ assign,
-                             uint32_t* __restrict__ pk, uint32_t* __restrict__ pv, uint32_t* __restrict__ ccnt,
-                             int* err) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < M; e += (int64_t)gridDim.x * blockDim.x) {
-    const int g = find_group(cbase, G, e);
-    const PGroup& p = gs[g];
-    const int64_t r = e - p.cbase;
-    const uint32_t id = mem[p.off + r];
-    for (int t = 0; t < p.f; ++t) {
-      const int64_t q = p.pair_off + r * p.f + t;
-      const uint32_t j = assign[q];
-      if (j >= (uint32_t)p.l) {  // cannot happen: every member has >= f leaders
-        atomicExch(err, DERR_CAPACITY);
-        continue;
-      }
-      const uint32_t child = (uint32_t)p.lead_off + j;
-      pk[q] = child;
-      pv[q] = id;
-      atomicAdd(&ccnt[child], 1u);
-    }
-  }
 }
 
 // One CTA per leaf job: a plain copy, or the sorted, deduplicated union of several sibling groups.
@@ -304,8 +300,9 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
   WorkItem* itA = ar.take<WorkItem>(cp.rowsA / 128 + 1);
   WorkItem* itB = ar.take<WorkItem>(cp.rowsB / 128 + 1);
   int64_t* n_it = ar.take<int64_t>(2);
-  uint32_t* assign = ar.take<uint32_t>(cp.L);
   uint32_t* pk = ar.take<uint32_t>(cp.L);
+  uint32_t* iota = ar.take<uint32_t>(cp.C);
+  int* d_redo = ar.take<int>(1);
   uint32_t* pk2 = ar.take<uint32_t>(cp.L);
   LeafJob* d_jobs = ar.take<LeafJob>(cp.J);
   LeafPart* d_parts = ar.take<LeafPart>(cp.J);
@@ -318,8 +315,12 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
   cub::DeviceRadixSort::SortPairs(nullptr, t3, (const uint32_t*)nullptr, (uint32_t*)nullptr, (const uint32_t*)nullptr,
                                   (uint32_t*)nullptr, (int)std::min<int64_t>(cp.L, INT32_MAX));
   cub::DeviceScan::ExclusiveSum(nullptr, t4, (const int64_t*)nullptr, (int64_t*)nullptr, (int)cp.leaves);
-  void* cub_tmp = ar.take<uint8_t>(std::max(std::max(t1, t2), std::max(t3, t4)));
-  const size_t cub_bytes = std::max(std::max(t1, t2), std::max(t3, t4));
+  size_t t5 = 0, t6 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t5, (const uint64_t*)nullptr, (uint64_t*)nullptr, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (int)std::min<int64_t>(cp.L, INT32_MAX), 0, 64);
+  cub::DeviceRadixSort::SortKeys(nullptr, t6, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)cp.C, 0, 32);
+  const size_t cub_bytes = std::max(std::max(std::max(t1, t2), std::max(t3, t4)), std::max(t5, t6));
+  void* cub_tmp = ar.take<uint8_t>(cub_bytes);
   if (ar.measuring()) return PIPNN_OK;
   if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (partition)");
   if (leaf_ids_cap < cp.L || leaf_off_cap < cp.L + 1) return fail(PIPNN_ECAPACITY, "leaf capacities too small");
@@ -330,6 +331,8 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
   // level 0: one subproblem per replica, members 0..n-1 each
   iota_reps_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n * reps, 256), num_sms() * 64), 256, 0, st>>>(memA, n, reps);
   PIPNN_LAUNCHED("iota_reps_kernel", st);
+  iota_kernel<<<(unsigned)std::min<int64_t>(ceil_div(cp.C, 256), num_sms() * 16), 256, 0, st>>>(iota, cp.C);
+  PIPNN_LAUNCHED("iota_kernel", st);
   std::vector<HGroup> open;
   uint32_t* mem = memA;
   uint32_t* nxt = memB;
@@ -345,8 +348,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     PIPNN_CUDA(cudaMemcpyAsync(d_parts, parts.data(), parts.size() * sizeof(LeafPart), cudaMemcpyHostToDevice, st));
     leaf_job_kernel<<<(unsigned)jobs.size(), 256, 0, st>>>(d_jobs, (int)jobs.size(), d_parts, src, staging, leaf_size);
     PIPNN_LAUNCHED("leaf_job_kernel", st);
-    // jobs/parts host vectors must stay valid until the copies complete
-    PIPNN_CUDA(cudaStreamSynchronize(st));
+    // (host->device copies from pageable memory have consumed jobs/parts when they return)
     jobs.clear();
     parts.clear();
     return PIPNN_OK;
@@ -402,48 +404,53 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     }
     if (C > cp.C || Q > cp.L || M > cp.L) return fail(PIPNN_ECAPACITY, "partition: level capacity");
     (void)fmax;
-    // ---- 1. leaders
-    std::vector<uint32_t> hcnt(G);
-    for (int attempt = 0; attempt < 2; ++attempt) {
-      PIPNN_CUDA(cudaMemcpyAsync(d_groups, hg.data(), G * sizeof(PGroup), cudaMemcpyHostToDevice, st));
-      PIPNN_CUDA(cudaMemcpyAsync(d_cbase, cb.data(), G * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-      PIPNN_CUDA(cudaMemsetAsync(d_cnt, 0, G * sizeof(uint32_t), st));
-      prio_kernel<false><<<(unsigned)std::min<int64_t>(ceil_div(M, 256), num_sms() * 64), 256, 0, st>>>(
-          d_groups, d_cbase, G, M, mem, d_cnt, nullptr, nullptr);
-      PIPNN_LAUNCHED("prio_kernel(count)", st);
-      PIPNN_CUDA(cudaMemcpyAsync(hcnt.data(), d_cnt, G * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-      PIPNN_CUDA(cudaStreamSynchronize(st));
-      bool redo = false;
-      for (int g = 0; g < G; ++g)
-        if ((int64_t)hcnt[g] < hg[g].l) {
-          hg[g].thr = ~0ull;  // exceedingly rare: keep every member as a candidate
-          redo = true;
-        }
-      if (!redo) break;
-    }
+    // ---- 1. leaders: capacity-bounded filter by priority, sort each group's candidates by (priority, id)
+    // [the candidate keys are distinct: mix(K, .) is injective], first l_g, then sorted by id. A group whose
+    // filter kept more than its capacity or fewer than l_g candidates makes the whole level run again
+    // without the filter (checked at the level's single host synchronisation below).
     std::vector<int64_t> cand_seg(G + 1, 0), lead_seg(G + 1, 0);
+    bool redo_unfiltered = false;
+  level_again:
     for (int g = 0; g < G; ++g) {
-      hg[g].cand_off = cand_seg[g];
-      cand_seg[g + 1] = cand_seg[g] + hcnt[g];
-      lead_seg[g + 1] = lead_seg[g] + hg[g].l;
+      PGroup& q = hg[g];
+      if (redo_unfiltered) q.thr = ~0ull;
+      const int64_t cap = q.thr == ~0ull ? q.size : std::min<int64_t>(q.size, 8 * (int64_t)q.l + 256);
+      q.cap = (int32_t)cap;
+      q.cand_off = cand_seg[g];
+      cand_seg[g + 1] = cand_seg[g] + cap;
+      lead_seg[g + 1] = lead_seg[g] + q.l;
     }
     const int64_t NC = cand_seg[G];
     PIPNN_CUDA(cudaMemcpyAsync(d_groups, hg.data(), G * sizeof(PGroup), cudaMemcpyHostToDevice, st));
+    PIPNN_CUDA(cudaMemcpyAsync(d_cbase, cb.data(), G * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     PIPNN_CUDA(cudaMemcpyAsync(d_cand_seg, cand_seg.data(), (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     PIPNN_CUDA(cudaMemcpyAsync(d_lead_seg, lead_seg.data(), (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     PIPNN_CUDA(cudaMemsetAsync(d_cnt, 0, G * sizeof(uint32_t), st));
-    prio_kernel<true><<<(unsigned)std::min<int64_t>(ceil_div(M, 256), num_sms() * 64), 256, 0, st>>>(
-        d_groups, d_cbase, G, M, mem, d_cnt, ck, cv);
-    PIPNN_LAUNCHED("prio_kernel(scatter)", st);
+    PIPNN_CUDA(cudaMemsetAsync(d_redo, 0, sizeof(int), st));
+    PIPNN_CUDA(cudaMemsetAsync(ck, 0xFF, NC * sizeof(uint64_t), st));
+    prio_kernel<<<(unsigned)std::min<int64_t>(ceil_div(M, 256), num_sms() * 64), 256, 0, st>>>(
+        d_groups, d_cbase, G, M, mem, d_cnt, ck, cv, d_redo);
+    PIPNN_LAUNCHED("prio_kernel", st);
+    prio_check_kernel<<<(unsigned)ceil_div(G, 256), 256, 0, st>>>(d_groups, G, d_cnt, d_redo);
+    PIPNN_LAUNCHED("prio_check_kernel", st);
     size_t tb = cub_bytes;
-    PIPNN_CUDA(cub::DeviceSegmentedSort::SortPairs(cub_tmp, tb, ck, ck2, cv, cv2, (int)NC, G, d_cand_seg,
-                                                   d_cand_seg + 1, st));
+    if (G == 1) {
+      PIPNN_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, ck, ck2, cv, cv2, (int)NC, 0, 64, st));
+    } else {
+      PIPNN_CUDA(cub::DeviceSegmentedSort::SortPairs(cub_tmp, tb, ck, ck2, cv, cv2, (int)NC, G, d_cand_seg,
+                                                     d_cand_seg + 1, st));
+    }
     take_leaders_kernel<<<G, 128, 0, st>>>(d_groups, G, cv2, lead);
     PIPNN_LAUNCHED("take_leaders_kernel", st);
     tb = cub_bytes;
-    PIPNN_CUDA(cub::DeviceSegmentedSort::SortKeys(cub_tmp, tb, lead, lead_sorted, (int)C, G, d_lead_seg,
-                                                  d_lead_seg + 1, st));
-    // ---- 2. nearest f_g leaders of every member (tcgen05 distance tiles + top-f)
+    if (G == 1) {
+      PIPNN_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, lead, lead_sorted, (int)C, 0, 32, st));
+    } else {
+      PIPNN_CUDA(cub::DeviceSegmentedSort::SortKeys(cub_tmp, tb, lead, lead_sorted, (int)C, G, d_lead_seg,
+                                                    d_lead_seg + 1, st));
+    }
+    // ---- 2. nearest f_g leaders of every member (tcgen05 distance tiles + top-f), written directly as
+    // (child = lead_off + leader index, member id) pairs with the child histogram
     std::vector<TileSeg> hA(G), hB(G);
     std::vector<DistSeg> hD(G);
     std::vector<WorkItem> hItA, hItB;
@@ -479,6 +486,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     PIPNN_CUDA(cudaMemcpyAsync(n_it, nits, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
     PIPNN_TRY(gather_tiled(X, mem, tsA, itA, n_it, nItA, TA, nA, c));
     PIPNN_TRY(gather_tiled(X, lead_sorted, tsB, itB, n_it + 1, nItB, TB, nB, c));
+    PIPNN_CUDA(cudaMemsetAsync(ccnt, 0, C * sizeof(uint32_t), st));
     DistTopkArgs da{};
     da.Ta = TA;
     da.Tb = TB;
@@ -488,23 +496,29 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     da.segs = dsegs;
     da.items = itA;
     da.n_items = n_it;
-    da.col_ids = nullptr;
-    da.out_idx = assign;
+    da.col_ids = iota;   // leader index j of group g -> child id lead_off + j
+    da.out_idx = pk;
     da.out_dist = nullptr;
+    da.row_ids = mem;    // member ids
+    da.out_rowid = cv2;
+    da.out_cnt = ccnt;
     da.err = c.err;
     PIPNN_TRY(launch_dist_topk(da, X->dtype == PIPNN_U8, X->metric == PIPNN_MIPS, fmax_l, st));
-    // ---- 3. group-by (stable radix sort of (child, id) pairs in member order)
-    PIPNN_CUDA(cudaMemsetAsync(ccnt, 0, C * sizeof(uint32_t), st));
-    pairs_kernel<<<(unsigned)std::min<int64_t>(ceil_div(M, 256), num_sms() * 64), 256, 0, st>>>(
-        d_groups, d_cbase, G, M, mem, assign, pk, cv2 /*ids*/, ccnt, c.err);
-    PIPNN_LAUNCHED("pairs_kernel", st);
+    // ---- 3. group-by: stable radix sort of the (child, id) pairs, in member order -> every child ascending
     tb = cub_bytes;
     PIPNN_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, pk, pk2, cv2, nxt, (int)Q, 0, bits_for(C), st));
-    // ---- 4. host merge plan
+    // ---- 4. host merge plan (the level's one synchronisation)
     std::vector<uint32_t> hccnt(C), hlead(C);
+    int hredo = 0;
     PIPNN_CUDA(cudaMemcpyAsync(hccnt.data(), ccnt, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     PIPNN_CUDA(cudaMemcpyAsync(hlead.data(), lead_sorted, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    PIPNN_CUDA(cudaMemcpyAsync(&hredo, d_redo, sizeof(int), cudaMemcpyDeviceToHost, st));
     PIPNN_CUDA(cudaStreamSynchronize(st));
+    if (hredo) {
+      if (redo_unfiltered) return fail(PIPNN_ECUDA, "partition: leader selection failed without filter");
+      redo_unfiltered = true;  // exceedingly rare: every member becomes a leader candidate
+      goto level_again;
+    }
     std::vector<int64_t> coff(C + 1, 0);
     for (int64_t j = 0; j < C; ++j) coff[j + 1] = coff[j] + hccnt[j];
     std::vector<HGroup> next;
