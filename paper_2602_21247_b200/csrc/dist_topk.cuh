@@ -115,6 +115,10 @@ __host__ __device__ constexpr int dt_smem_bytes(int Kb, bool u8) {
   return dt_fixed_bytes(Kb, u8) + dt_stages(Kb, u8) * kDtStageBytes;
 }
 
+// Passes per item: 2 (threshold, then exact picks). A single exact pass (U = +inf; every key of the first
+// chunk passes) measured slower even for the partition's K = 2 on B200 (C2: 3.08 vs 2.89 ms partition).
+__host__ __device__ __forceinline__ int dt_passes(int /*k*/) { return 2; }
+
 // Sorted insertion into a register list (ascending; equal keys keep the earlier entry first).
 // Precondition: key < kk[KMAX-1].
 template <typename KT, int KMAX>
@@ -230,7 +234,8 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
           ptx::bulk_g2s(sA + (g * NA + slot) * KCa * 2048, args.Ta + (S.a.pos / 128 + w.rb) * (int64_t)KC * 2048,
                         KCa * 2048, &bar_a_full[g][slot]);
         }
-        for (int t = 0; t < 2 * T; ++t) {
+        const int NT = dt_passes(S.k) * T;
+        for (int t = 0; t < NT; ++t) {
           const int c0 = (t % T) * kDtTileN;
           const uint8_t* srcB = args.Tb + (S.b.pos / 128 + c0 / 128) * (int64_t)KC * 2048;
           for (int ch = 0; ch < nchunks; ++ch, ++sg) {
@@ -255,11 +260,12 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
         const WorkItem w = args.items[it];
         const int ncols = args.segs[w.seg].b.rows;
         const int T = (ncols + kDtTileN - 1) / kDtTileN;
+        const int NT = dt_passes(args.segs[w.seg].k) * T;
         const int slot = (int)(ia % NA);
         if (!ptx::mbar_wait(&bar_a_full[g][slot], (ia / NA) & 1, args.err, DERR_WAIT_TIMEOUT)) return;
         ++ia;
         const uint8_t* a_base = sA + (g * NA + slot) * KCa * 2048;
-        for (int t = 0; t < 2 * T; ++t, ++tc) {
+        for (int t = 0; t < NT; ++t, ++tc) {
           const int c0 = (t % T) * kDtTileN;
           const int Nt = min(kDtTileN, (ncols - c0 + 31) & ~31);
           const uint32_t buf = 2 * g + (tc & 1), use = tc >> 1;
@@ -334,15 +340,16 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
         KT U = kInf;
         int qlen = 0;
         const int diag_chunk = S.self ? (r0 + q * 32) : -1;  // column base of this warp's diagonal chunk
-        for (int t2 = 0; t2 < 2 * T; ++t2, ++tcount) {
-          const bool pass2 = t2 >= T;
-          const int c0 = (pass2 ? t2 - T : t2) * kDtTileN;
+        const int P1 = dt_passes(K) == 2 ? T : 0;  // tiles of pass 1 (none: single exact pass, U = +inf)
+        for (int t2 = 0; t2 < P1 + T; ++t2, ++tcount) {
+          const bool pass2 = t2 >= P1;
+          const int c0 = (pass2 ? t2 - P1 : t2) * kDtTileN;
           const int Nt = min(kDtTileN, (ncols - c0 + 31) & ~31);
           const uint32_t buf = 2 * wg + (tcount & 1), use = tcount >> 1;
           if (!ptx::mbar_wait(&bar_acc_full[buf], use & 1, args.err, DERR_WAIT_TIMEOUT)) return;
           ptx::tc_fence_after();
           const uint32_t taddr = tmem + buf * kDtTileN + ((uint32_t)(q * 32) << 16);
-          if (t2 == T) {
+          if (t2 == P1 && P1 > 0) {
             U = vk[VK - 1];
             if (U8 && U != kInf) U = U + 1;  // key <= U  <=>  key < U + 1
             if (!U8) U = (KT)nextafterf((float)U, __int_as_float(0x7F800000));
