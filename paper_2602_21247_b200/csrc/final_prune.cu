@@ -355,6 +355,20 @@ __device__ __forceinline__ void mma_16x8(int32_t (&acc)[4], const uint32_t (&a)[
   }
 }
 
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 struct GpLayout {
   int Kb, pitch;  // bytes of a staged row (multiple of 32), SMEM row pitch (Kb + 16)
   size_t rows_off, g_off, nrm_off, ids_off, per_warp;
@@ -387,6 +401,17 @@ __device__ __forceinline__ void gp_stage(const void* __restrict__ Xv, int64_t ld
   const int rr = lane / cpr, ch = lane - rr * cpr;
   const bool act = rr < rpp;
   const bool fast = U8 ? ((d & 15) == 0 && (ld & 15) == 0) : ((d & 7) == 0 && (ld & 3) == 0);
+  if (U8 && fast) {
+    // cp.async straight into the tile (16 B per lane, zero fill beyond d and for padding rows)
+    for (int r = rr; r < nrp; r += rpp) {
+      if (!act) break;
+      const bool on = r < nr && ch * 16 < d;
+      const uint8_t* src = on ? (const uint8_t*)Xv + (int64_t)ids[r] * ld + ch * 16 : (const uint8_t*)Xv;
+      cp_async16(rows + (size_t)r * L.pitch + ch * 16, src, on ? 16u : 0u);
+    }
+    cp_async_wait_all();
+    return;
+  }
   for (int r0 = 0; r0 < nrp; r0 += 8 * rpp) {
     uint4 v[8];
 #pragma unroll
@@ -397,14 +422,10 @@ __device__ __forceinline__ void gp_stage(const void* __restrict__ Xv, int64_t ld
         const int64_t id = ids[r];
         if (U8) {
           const uint8_t* src = (const uint8_t*)Xv + id * ld;
-          if (fast) {
-            if (ch * 16 < d) v[j] = __ldg((const uint4*)src + ch);
-          } else {
-            uint32_t w[4] = {0u, 0u, 0u, 0u};
-            for (int t = 0; t < 16; ++t)
-              if (ch * 16 + t < d) w[t >> 2] |= (uint32_t)src[ch * 16 + t] << (8 * (t & 3));
-            v[j] = make_uint4(w[0], w[1], w[2], w[3]);
-          }
+          uint32_t w[4] = {0u, 0u, 0u, 0u};
+          for (int t = 0; t < 16; ++t)
+            if (ch * 16 + t < d) w[t >> 2] |= (uint32_t)src[ch * 16 + t] << (8 * (t & 3));
+          v[j] = make_uint4(w[0], w[1], w[2], w[3]);
         } else {
           const float* src = (const float*)Xv + id * ld;
           float f[8];
@@ -439,7 +460,7 @@ __device__ __forceinline__ void gp_stage(const void* __restrict__ Xv, int64_t ld
 // the lazy scan of P:938-942 (admit i unless an admitted y prunes it) solved as a fixpoint over ballots, no
 // sort: the admission order is the (D, id) order, so an admitted i lands at rank popc(admitted & P_i).
 template <bool U8, bool MIPS, int CP>
-__global__ void __launch_bounds__(256) fp_gram_kernel(const void* __restrict__ Xv, int64_t n, int d, int64_t ld,
+__global__ void __launch_bounds__(256, CP == 32 ? 3 : 1) fp_gram_kernel(const void* __restrict__ Xv, int64_t n, int d, int64_t ld,
                                                       int l_max, const uint64_t* __restrict__ slots,
                                                       const uint32_t* __restrict__ count, int R, int an, int ad,
                                                       uint32_t* __restrict__ nbr_tmp, uint32_t* __restrict__ deg,
@@ -479,33 +500,32 @@ __global__ void __launch_bounds__(256) fp_gram_kernel(const void* __restrict__ X
     __syncwarp();
     gp_stage<U8>(Xv, ld, d, ids, nr, nrp, rows, L, lane);
     __syncwarp();
-    // ---- Gram on tensor cores: 16-row blocks x 8-row blocks, K in 32-byte steps
-    const int nb16 = nrp >> 4, nb8 = nrp >> 3;
+    // ---- Gram on tensor cores: 16-row blocks x 16-row (two 8-row) blocks, K in 32-byte steps; fragments by
+    // ldmatrix (matrix m of x4 = rows +8*(m&1), bytes +16*(m>>1): exactly the a0..a3 / b0,b1 register layout)
+    const int nb16 = nrp >> 4;
+    const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 16;
     for (int bi = 0; bi < nb16; ++bi) {
       int32_t acc[CP / 8][4];
 #pragma unroll
       for (int bj = 0; bj < CP / 8; ++bj) acc[bj][0] = acc[bj][1] = acc[bj][2] = acc[bj][3] = 0;
-      const uint8_t* ra = rows + (size_t)(bi * 16 + g) * L.pitch + t4 * 4;
+      const uint8_t* ra = rows + (size_t)(bi * 16 + lrow) * L.pitch + lcol;
       for (int kb = 0; kb < L.Kb; kb += 32) {
         uint32_t a[4];
-        a[0] = *(const uint32_t*)(ra + kb);
-        a[1] = *(const uint32_t*)(ra + 8 * L.pitch + kb);
-        a[2] = *(const uint32_t*)(ra + kb + 16);
-        a[3] = *(const uint32_t*)(ra + 8 * L.pitch + kb + 16);
+        ldsm_x4(a, ra + kb);
 #pragma unroll
-        for (int bj = 0; bj < CP / 8; ++bj) {
-          if (bj < nb8) {
-            const uint8_t* rb = rows + (size_t)(bj * 8 + g) * L.pitch + t4 * 4 + kb;
-            uint32_t b[2];
-            b[0] = *(const uint32_t*)rb;
-            b[1] = *(const uint32_t*)(rb + 16);
-            mma_16x8<U8>(acc[bj], a, b);
+        for (int bj2 = 0; bj2 < CP / 16; ++bj2) {
+          if (bj2 < nb16) {
+            uint32_t bb[4];
+            ldsm_x4(bb, rows + (size_t)(bj2 * 16 + lrow) * L.pitch + lcol + kb);
+            const uint32_t b0[2] = {bb[0], bb[2]}, b1[2] = {bb[1], bb[3]};
+            mma_16x8<U8>(acc[2 * bj2], a, b0);
+            mma_16x8<U8>(acc[2 * bj2 + 1], a, b1);
           }
         }
       }
 #pragma unroll
       for (int bj = 0; bj < CP / 8; ++bj) {
-        if (bj < nb8) {
+        if (bj < 2 * nb16) {
           const int r = bi * 16 + g, s = bj * 8 + 2 * t4;
           DT* d0 = G + (size_t)r * DS + s;
           DT* d1 = G + (size_t)(r + 8) * DS + s;
