@@ -386,8 +386,59 @@ struct OwnerKeys {
 
 // Fast merge: one warp per owner, all of its keys (reservoir + new, <= 32*E) in registers: bitonic sort,
 // keep the first key of every hash run (bucket minimum, Alg. 3's collision rule), write back sorted by hash.
-// Owners with more keys, more instances than lanes, or more than l_max buckets go to the generic merge.
+// Returns false (nothing written) when more than l_max buckets survive.
 template <int E>
+__device__ __forceinline__ bool merge_owner_regs(int lane, int T, int c, int k, const uint64_t* res_in,
+                                                 const uint32_t* sinst, const uint32_t* sbeg, int ni,
+                                                 const uint64_t* __restrict__ fwd, const uint64_t* __restrict__ rev,
+                                                 const uint32_t* __restrict__ rev_start, int l_max, uint64_t* res,
+                                                 int& B_out) {
+  uint64_t key[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    int idx = e * 32 + lane;
+    uint64_t v = ~0ull;
+    if (idx < T) {
+      if (idx < c) {
+        v = res_in[idx];
+      } else {
+        idx -= c;
+        int j = 0;
+        while (j + 1 < ni && (int)sbeg[j + 1] <= idx) ++j;  // segment j: k forward then rev keys of instance j
+        const int o = idx - (int)sbeg[j];
+        const uint32_t i = sinst[j];
+        v = o < k ? fwd[(int64_t)i * k + o] : rev[(uint64_t)rev_start[i] + (o - k)];
+      }
+    }
+    key[e] = v;
+  }
+  warp_sort_regs<E>(key, lane);
+  bool keep[E];
+  int B = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint64_t up = __shfl_up_sync(0xffffffffu, key[e], 1);
+    const uint64_t last = __shfl_sync(0xffffffffu, key[e > 0 ? e - 1 : 0], 31);  // element 32e - 1
+    const uint64_t prev = lane > 0 ? up : last;
+    const bool first = (e == 0 && lane == 0) || ((prev >> 48) != (key[e] >> 48));
+    keep[e] = key[e] != ~0ull && first;
+    B += __popc(__ballot_sync(0xffffffffu, keep[e]));
+  }
+  if (B > l_max) return false;
+  int base = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t bal = __ballot_sync(0xffffffffu, keep[e]);
+    if (keep[e]) res[base + __popc(bal & ((1u << lane) - 1u))] = key[e];
+    base += __popc(bal);
+  }
+  B_out = B;
+  return true;
+}
+
+// One warp per owner: the owner's instance table (instance id, first flat index of its keys) in SMEM, then
+// the register merge with 32 (common: 2 k f keys) or 64 slots. Owners with more keys, more instances than
+// lanes, or more than l_max buckets go to the generic merge.
 __global__ void __launch_bounds__(256) hp_merge_inst_kernel(int64_t n, int l_max, int k, const uint64_t* __restrict__ inv_start,
                                                             const uint32_t* __restrict__ inv, const uint64_t* __restrict__ fwd,
                                                             const uint64_t* __restrict__ rev,
@@ -395,54 +446,49 @@ __global__ void __launch_bounds__(256) hp_merge_inst_kernel(int64_t n, int l_max
                                                             const uint32_t* __restrict__ rev_cnt,
                                                             uint64_t* __restrict__ slots, uint32_t* __restrict__ count,
                                                             uint32_t* __restrict__ defer, uint32_t* __restrict__ defer_n) {
-  const int lane = threadIdx.x & 31;
+  __shared__ uint32_t s_inst[8][32], s_beg[8][32];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t u = wid; u < n; u += nw) {
     const uint64_t i0 = inv_start[u];
     const int ni = (int)(inv_start[u + 1] - i0);
     if (ni == 0) continue;
+    if (ni > 32) {
+      if (lane == 0) defer[atomicAdd(defer_n, 1u)] = (uint32_t)u;
+      continue;
+    }
     const int c = (int)count[u];
     int sz = 0;
-    if (lane < ni) sz = k + (int)rev_cnt[inv[i0 + lane]];
+    uint32_t inst = 0;
+    if (lane < ni) {
+      inst = inv[i0 + lane];
+      sz = k + (int)rev_cnt[inst];
+    }
+    int x = sz;  // inclusive prefix over the instance segments
 #pragma unroll
-    for (int o = 16; o; o >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, o);
-    const int T = c + sz;
-    if (ni > 32 || T > 32 * E) {
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    const int T = c + __shfl_sync(0xffffffffu, x, 31);
+    if (T > 64) {
       if (lane == 0) defer[atomicAdd(defer_n, 1u)] = (uint32_t)u;
       continue;
     }
+    __syncwarp();
+    s_inst[wl][lane] = inst;
+    s_beg[wl][lane] = (uint32_t)(x - sz);
+    __syncwarp();
     uint64_t* res = slots + u * (int64_t)l_max;
-    OwnerKeys ok{res, c, k, inv + i0, ni, fwd, rev, rev_start, rev_cnt};
-    uint64_t key[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const int idx = e * 32 + lane;
-      key[e] = idx < T ? ok.get(idx) : ~0ull;
-    }
-    warp_sort_regs<E>(key, lane);
-    // bucket minima: first key of each hash run; ~0 keys (missing picks, padding) are never kept
-    bool keep[E];
     int B = 0;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const uint64_t up = __shfl_up_sync(0xffffffffu, key[e], 1);
-      const uint64_t last = __shfl_sync(0xffffffffu, key[e > 0 ? e - 1 : 0], 31);  // element 32e - 1
-      const uint64_t prev = lane > 0 ? up : last;
-      const bool first = (e == 0 && lane == 0) || ((prev >> 48) != (key[e] >> 48));
-      keep[e] = key[e] != ~0ull && first;
-      B += __popc(__ballot_sync(0xffffffffu, keep[e]));
-    }
-    if (B > l_max) {
+    const bool ok = T <= 32 ? merge_owner_regs<1>(lane, T, c, k, res, s_inst[wl], s_beg[wl], ni, fwd, rev, rev_start,
+                                                  l_max, res, B)
+                            : merge_owner_regs<2>(lane, T, c, k, res, s_inst[wl], s_beg[wl], ni, fwd, rev, rev_start,
+                                                  l_max, res, B);
+    if (!ok) {
       if (lane == 0) defer[atomicAdd(defer_n, 1u)] = (uint32_t)u;
       continue;
-    }
-    int base = 0;
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const uint32_t bal = __ballot_sync(0xffffffffu, keep[e]);
-      if (keep[e]) res[base + __popc(bal & ((1u << lane) - 1u))] = key[e];
-      base += __popc(bal);
     }
     if (lane == 0) count[u] = (uint32_t)B;
   }
@@ -562,7 +608,7 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
   // (3) merge per owner (register path), deferred owners through the generic chunked path
   PIPNN_CUDA(cudaMemsetAsync(defer_n, 0, sizeof(uint32_t), c.st));
   const int64_t blocks = std::min<int64_t>(ceil_div(n, 8), (int64_t)num_sms() * 32);
-  hp_merge_inst_kernel<2><<<(unsigned)blocks, 256, 0, c.st>>>(n, l_max, k, g.start, inv, fwd, rev, rev_start, rev_cnt,
+  hp_merge_inst_kernel<<<(unsigned)blocks, 256, 0, c.st>>>(n, l_max, k, g.start, inv, fwd, rev, rev_start, rev_cnt,
                                                                slots, count, defer, defer_n);
   PIPNN_LAUNCHED("hp_merge_inst_kernel", c.st);
   const int cap = merge_cap(l_max);
