@@ -225,29 +225,42 @@ __global__ void __launch_bounds__(256) hp_emit_kernel(const int64_t* __restrict_
                                                       int64_t* __restrict__ n_edges) {
   extern __shared__ __align__(16) uint8_t esm[];
   __shared__ uint32_t tot_sh;
+  __shared__ uint32_t part[256];
   const int64_t b = blockIdx.x;
   const int64_t o0 = leaf_off[b];
   const int s = (int)(leaf_off[b + 1] - o0);
+  const int ms = m | 1;             // SMEM sketch row stride (odd: conflict-free row-per-thread reads)
   uint32_t* ids = (uint32_t*)esm;   // [s]
   uint32_t* rc = ids + s;           // [s] reverse in-degree, then cursor
   uint32_t* rs = rc + s;            // [s] exclusive scan of rc
-  ST* sk = (ST*)(rs + s);           // [s][m] when staged
+  ST* sk = (ST*)(rs + s);           // [s][ms] when staged
   if (threadIdx.x == 0) tot_sh = 0;
   for (int j = threadIdx.x; j < s; j += blockDim.x) {
-    ids[j] = leaf_ids[o0 + j];
+    const uint32_t id = leaf_ids[o0 + j];
+    ids[j] = id;
     rc[j] = 0;
+    if (stage_sk) {
+      const ST* src = S + (int64_t)id * m;
+      ST v[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        if (t < m) v[t] = src[t];  // independent loads, all in flight
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        if (t < m) sk[j * ms + t] = v[t];
+    }
   }
   __syncthreads();
-  if (stage_sk)
-    for (int e = threadIdx.x; e < s * m; e += blockDim.x) {
-      const int j = e / m;
-      sk[e] = S[(int64_t)ids[j] * m + (e - j * m)];
-    }
-  const int P = s * k;
   const uint16_t* cl = cols + o0 * k;
-  for (int e = threadIdx.x; e < P; e += blockDim.x) {
-    const uint16_t q = cl[e];
-    if (q != 0xFFFFu) atomicAdd(&rc[q], 1u);
+  // pass A: reverse in-degree of every member (thread per instance; the k picks of an instance in one go)
+  for (int i = threadIdx.x; i < s; i += blockDim.x) {
+    uint16_t q[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+      if (t < k) q[t] = cl[i * k + t];
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+      if (t < k && q[t] != 0xFFFFu) atomicAdd(&rc[q[t]], 1u);
   }
   __syncthreads();
   // exclusive scan of rc (block-wide, thread-serial chunks + warp scan of chunk sums)
@@ -256,7 +269,6 @@ __global__ void __launch_bounds__(256) hp_emit_kernel(const int64_t* __restrict_
     const int j0 = threadIdx.x * per, j1 = min(s, j0 + per);
     uint32_t sum = 0;
     for (int j = j0; j < j1; ++j) sum += rc[j];
-    __shared__ uint32_t part[256];
     part[threadIdx.x] = sum;
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -288,26 +300,44 @@ __global__ void __launch_bounds__(256) hp_emit_kernel(const int64_t* __restrict_
     rc[j] = 0;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < P; e += blockDim.x) {
-    const int i = e / k;
-    const uint16_t q = cl[e];
-    uint64_t kf = ~0ull;
-    if (q != 0xFFFFu) {
-      const uint32_t pid = ids[i], qid = ids[q];
-      const ST* sp = stage_sk ? sk + (int64_t)i * m : S + (int64_t)pid * m;
-      const ST* sq = stage_sk ? sk + (int64_t)q * m : S + (int64_t)qid * m;
-      uint32_t hf = 0, hr = 0;
-      for (int t = 0; t < m; ++t) {
-        const ST a = sp[t], c = sq[t];
-        hf |= (uint32_t)(c >= a) << t;  // h_p(q): bit t = [S(q)_t >= S(p)_t]
-        hr |= (uint32_t)(a >= c) << t;  // h_q(p)
+  // pass B: both directions of every pick (thread per instance)
+  for (int i = threadIdx.x; i < s; i += blockDim.x) {
+    uint16_t q[16];
+    float D[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+      if (t < k) {
+        q[t] = cl[i * k + t];
+        D[t] = dist[(o0 + i) * k + t];
       }
-      const uint64_t dk = (uint64_t)dist_order_key(dist[o0 * k + e]) << 32;
-      kf = ((uint64_t)hf << 48) | dk | qid;
-      const uint32_t pos = rs[q] + atomicAdd(&rc[q], 1u);
-      rev[rbase + pos] = ((uint64_t)hr << 48) | dk | pid;
+    const uint32_t pid = ids[i];
+    ST sp[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t)
+      if (t < m) sp[t] = stage_sk ? sk[i * ms + t] : S[(int64_t)pid * m + t];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      if (t >= k) break;
+      uint64_t kf = ~0ull;
+      if (q[t] != 0xFFFFu) {
+        const int qq = q[t];
+        const uint32_t qid = ids[qq];
+        uint32_t hf = 0, hr = 0;
+#pragma unroll
+        for (int h = 0; h < 16; ++h) {
+          if (h < m) {
+            const ST a = sp[h], c = stage_sk ? sk[qq * ms + h] : S[(int64_t)qid * m + h];
+            hf |= (uint32_t)(c >= a) << h;  // h_p(q): bit h = [S(q)_h >= S(p)_h]
+            hr |= (uint32_t)(a >= c) << h;  // h_q(p)
+          }
+        }
+        const uint64_t dk = (uint64_t)dist_order_key(D[t]) << 32;
+        kf = ((uint64_t)hf << 48) | dk | qid;
+        const uint32_t pos = rs[qq] + atomicAdd(&rc[qq], 1u);
+        rev[rbase + pos] = ((uint64_t)hr << 48) | dk | pid;
+      }
+      fwd[(o0 + i) * k + t] = kf;
     }
-    fwd[o0 * k + e] = kf;
   }
   if (threadIdx.x == 0) atomicAdd((unsigned long long*)n_edges, 2ull * tot_sh);
 }
@@ -437,7 +467,7 @@ __device__ __forceinline__ bool merge_owner_regs(int lane, int T, int c, int k, 
 }
 
 // One warp per owner: the owner's instance table (instance id, first flat index of its keys) in SMEM, then
-// the register merge with 32 (common: 2 k f keys) or 64 slots. Owners with more keys, more instances than
+// the register merge with 32 (common: 2 k f keys), 64 or 128 slots. Owners with more keys, more instances than
 // lanes, or more than l_max buckets go to the generic merge.
 __global__ void __launch_bounds__(256) hp_merge_inst_kernel(int64_t n, int l_max, int k, const uint64_t* __restrict__ inv_start,
                                                             const uint32_t* __restrict__ inv, const uint64_t* __restrict__ fwd,
@@ -472,7 +502,7 @@ __global__ void __launch_bounds__(256) hp_merge_inst_kernel(int64_t n, int l_max
       if (lane >= o) x += y;
     }
     const int T = c + __shfl_sync(0xffffffffu, x, 31);
-    if (T > 64) {
+    if (T > 128) {
       if (lane == 0) defer[atomicAdd(defer_n, 1u)] = (uint32_t)u;
       continue;
     }
@@ -482,10 +512,10 @@ __global__ void __launch_bounds__(256) hp_merge_inst_kernel(int64_t n, int l_max
     __syncwarp();
     uint64_t* res = slots + u * (int64_t)l_max;
     int B = 0;
-    const bool ok = T <= 32 ? merge_owner_regs<1>(lane, T, c, k, res, s_inst[wl], s_beg[wl], ni, fwd, rev, rev_start,
-                                                  l_max, res, B)
-                            : merge_owner_regs<2>(lane, T, c, k, res, s_inst[wl], s_beg[wl], ni, fwd, rev, rev_start,
-                                                  l_max, res, B);
+    bool ok;
+    if (T <= 32) ok = merge_owner_regs<1>(lane, T, c, k, res, s_inst[wl], s_beg[wl], ni, fwd, rev, rev_start, l_max, res, B);
+    else if (T <= 64) ok = merge_owner_regs<2>(lane, T, c, k, res, s_inst[wl], s_beg[wl], ni, fwd, rev, rev_start, l_max, res, B);
+    else ok = merge_owner_regs<4>(lane, T, c, k, res, s_inst[wl], s_beg[wl], ni, fwd, rev, rev_start, l_max, res, B);
     if (!ok) {
       if (lane == 0) defer[atomicAdd(defer_n, 1u)] = (uint32_t)u;
       continue;
@@ -582,7 +612,7 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
   if (n_inst == 0 || n_leaves == 0) return PIPNN_OK;
   // (1) leaf-local emission of both edge directions
   max_leaf = std::max(1, std::min(max_leaf, 4096));
-  const size_t sk_bytes = (size_t)max_leaf * m * 4;
+  const size_t sk_bytes = (size_t)max_leaf * (m | 1) * 4;
   const int stage_sk = sk_bytes <= 96 * 1024 ? 1 : 0;
   const int smem = (int)((size_t)max_leaf * 12 + (stage_sk ? sk_bytes : 0));
   if (sk_int) {
