@@ -133,6 +133,17 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   uint64_t* slots = ar.take<uint64_t>((size_t)X->n * p->hp.l_max);
   uint32_t* count = ar.take<uint32_t>(X->n);
   int64_t* n_edges_dev = ar.take<int64_t>(1);
+  // float data: one bf16 (RNE) copy of X, made in prep; every later stage gathers its rows (R19)
+  const bool is_float = X->dtype != PIPNN_U8;
+  const int ldb = (int)round_up(X->d, 8);
+  uint16_t* Xb = is_float ? ar.take<uint16_t>((size_t)X->n * ldb) : nullptr;
+  pipnn_points Xbv = *X;
+  if (is_float) {
+    Xbv.data = Xb;
+    Xbv.ld = ldb;
+    Xbv.dtype = kDtypeBf16;
+  }
+  const pipnn_points* XS = is_float ? &Xbv : X;  // the rows the stages read
   const size_t mark = ar.mark();
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tile_ev;
   int64_t leaf_pairs = 0;
@@ -153,15 +164,19 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
     }
     tile_ev.clear();
   };
-  // (a0) sketches
-  pipnn_status s = sketch_impl(X, p->hp.m, p->hp.seed, sketch, ar, c);
+  // (a0) bf16 copy (float data) and sketches
+  if (is_float && !ar.measuring()) {
+    pipnn_status s0 = to_bf16(X, Xb, ldb, c);
+    if (s0 != PIPNN_OK) { cleanup(); return s0; }
+  }
+  pipnn_status s = sketch_impl(XS, p->hp.m, p->hp.seed, sketch, ar, c);
   if (s != PIPNN_OK) { cleanup(); return s; }
   ar.release(mark);
   if (!ar.measuring()) cudaEventRecord(ev[1], st);
   // (a1, a2) partition (Alg. 5)
   int64_t n_leaves = 0, n_inst = 0;
   int depth = 0;
-  s = partition_impl(X, &p->part, leaf_off, bp.leaf_off_cap, leaf_ids, bp.leaf_ids_cap, &n_leaves, &n_inst, &depth,
+  s = partition_impl(XS, &p->part, leaf_off, bp.leaf_off_cap, leaf_ids, bp.leaf_ids_cap, &n_leaves, &n_inst, &depth,
                      ar, c);
   if (s != PIPNN_OK) { cleanup(); return s; }
   ar.release(mark);
@@ -172,7 +187,7 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   const int64_t budget = std::min<int64_t>(bp.leaf_ids_cap / 64 + 1024, (int64_t)1 << 16);
   int max_leaf_h = p->part.c_max;
   if (ar.measuring()) {
-    s = leaf_pick_impl(X, nullptr, nullptr, budget, budget * 128, k, nullptr, dist, ar, c, budget, cols);
+    s = leaf_pick_impl(XS, nullptr, nullptr, budget, budget * 128, k, nullptr, dist, ar, c, budget, cols);
     if (s != PIPNN_OK) { cleanup(); return s; }
   } else if (n_leaves > 0) {
     std::vector<int64_t> off(n_leaves + 1);
@@ -192,7 +207,7 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
         ++b1;
       }
       if (b1 == b0) { cleanup(); return fail(PIPNN_EUNSUPPORTED, "leaf larger than the wave budget"); }
-      s = leaf_pick_impl(X, leaf_off + b0, leaf_ids, b1 - b0, off[b1] - off[b0], k, nullptr, dist, ar, c, budget, cols);
+      s = leaf_pick_impl(XS, leaf_off + b0, leaf_ids, b1 - b0, off[b1] - off[b0], k, nullptr, dist, ar, c, budget, cols);
       if (s != PIPNN_OK) { cleanup(); return s; }
       ar.release(mark);
       b0 = b1;
@@ -210,8 +225,17 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   if (s != PIPNN_OK) { cleanup(); return s; }
   ar.release(mark);
   if (!ar.measuring()) cudaEventRecord(ev[4], st);
-  // (a7, a8) final prune + CSR
-  s = final_prune_impl(X, p->hp.l_max, slots, count, &p->prune, row_ptr, col_idx, ar, c);
+  // (a7, a8) final prune + CSR. Float data (rows larger than L2 at 1M points): points in leaf
+  // order, so the candidate rows of consecutive points overlap (L2 reuse); uint8 rows fit L2 at C2 and
+  // id order measured slightly faster there.
+  uint32_t* order = is_float ? ar.take<uint32_t>(X->n) : nullptr;
+  uint32_t* order_n = is_float ? ar.take<uint32_t>(1) : nullptr;
+  if (is_float) {
+    s = leaf_order(leaf_ids, n_inst, X->n, order, order_n, ar, c);
+    if (s != PIPNN_OK) { cleanup(); return s; }
+  }
+  s = final_prune_impl(X, p->hp.l_max, slots, count, &p->prune, row_ptr, col_idx, ar, c, order, order_n,
+                       is_float ? &Xbv : nullptr);
   if (s != PIPNN_OK) { cleanup(); return s; }
   if (ar.measuring()) return PIPNN_OK;
   PIPNN_CUDA(cudaEventRecord(ev[5], st));

@@ -101,6 +101,11 @@ __host__ __device__ __forceinline__ uint16_t dist_order_key(float D) {
   return (uint16_t)(b ^ ((b & 0x8000u) ? 0xFFFFu : 0x8000u));
 }
 
+// Internal element type: float data already rounded to bf16 (RNE), rows of ld elements, zero padded to ld
+// (ld = round_up(d, 8)). Never an ABI value: pipnn_build makes this copy of float X once (prep) and every
+// later gather reads it (half the bytes of the fp32 rows).
+constexpr int32_t kDtypeBf16 = 2;
+
 inline int num_sms() {
   static int n = 0;
   if (n == 0) {

@@ -395,18 +395,21 @@ __host__ __device__ inline GpLayout gp_layout(int d, bool u8, int CP) {
 // rows; 8 passes (8 independent 16-B loads per lane) are issued before the stores.
 template <bool U8>
 __device__ __forceinline__ void gp_stage(const void* __restrict__ Xv, int64_t ld, int d, const uint32_t* ids, int nr,
-                                         int nrp, uint8_t* rows, const GpLayout& L, int lane) {
+                                         int nrp, uint8_t* rows, const GpLayout& L, int lane, int src_bf16) {
   const int cpr = L.Kb >> 4;  // 16-B chunks per row (<= 32)
   const int rpp = 32 / cpr;   // rows per pass
   const int rr = lane / cpr, ch = lane - rr * cpr;
   const bool act = rr < rpp;
   const bool fast = U8 ? ((d & 15) == 0 && (ld & 15) == 0) : ((d & 7) == 0 && (ld & 3) == 0);
-  if (U8 && fast) {
-    // cp.async straight into the tile (16 B per lane, zero fill beyond d and for padding rows)
+  if ((U8 && fast) || (!U8 && src_bf16)) {
+    // cp.async straight into the tile (16 B per lane, zero fill beyond the row and for padding rows); uint8
+    // rows of ld bytes, or the bf16 copy's rows of ld elements (zero padded, ld a multiple of 8)
+    const int64_t rb = U8 ? ld : 2 * ld;
+    const int lim = U8 ? d : (int)(2 * ld);
     for (int r = rr; r < nrp; r += rpp) {
       if (!act) break;
-      const bool on = r < nr && ch * 16 < d;
-      const uint8_t* src = on ? (const uint8_t*)Xv + (int64_t)ids[r] * ld + ch * 16 : (const uint8_t*)Xv;
+      const bool on = r < nr && ch * 16 < lim;
+      const uint8_t* src = on ? (const uint8_t*)Xv + (int64_t)ids[r] * rb + ch * 16 : (const uint8_t*)Xv;
       cp_async16(rows + (size_t)r * L.pitch + ch * 16, src, on ? 16u : 0u);
     }
     cp_async_wait_all();
@@ -466,7 +469,8 @@ __global__ void __launch_bounds__(256, CP == 32 ? 3 : 1) fp_gram_kernel(const vo
                                                       uint32_t* __restrict__ nbr_tmp, uint32_t* __restrict__ deg,
                                                       const uint32_t* __restrict__ list,
                                                       const uint32_t* __restrict__ list_n,
-                                                      uint32_t* __restrict__ defer, uint32_t* __restrict__ defer_n) {
+                                                      uint32_t* __restrict__ defer, uint32_t* __restrict__ defer_n,
+                                                      int src_bf16) {
   using DT = typename std::conditional<U8, int32_t, float>::type;
   constexpr int E = CP / 32;  // sorted candidates per lane; also the bitmask words per candidate
   extern __shared__ __align__(16) uint8_t gsm[];
@@ -498,7 +502,7 @@ __global__ void __launch_bounds__(256, CP == 32 ? 3 : 1) fp_gram_kernel(const vo
     const int nr = c + 1, nrp = (nr + 15) & ~15;
     for (int t = lane; t < nr; t += 32) ids[t] = t == 0 ? (uint32_t)u : (uint32_t)(res[t - 1] & 0xFFFFFFFFu);
     __syncwarp();
-    gp_stage<U8>(Xv, ld, d, ids, nr, nrp, rows, L, lane);
+    gp_stage<U8>(Xv, ld, d, ids, nr, nrp, rows, L, lane, src_bf16);
     __syncwarp();
     // ---- Gram on tensor cores: 16-row blocks x 16-row (two 8-row) blocks, K in 32-byte steps; fragments by
     // ldmatrix (matrix m of x4 = rows +8*(m&1), bytes +16*(m>>1): exactly the a0..a3 / b0,b1 register layout)
@@ -693,8 +697,10 @@ pipnn_status leaf_order(const uint32_t* leaf_ids, int64_t n_inst, int64_t n, uin
 
 pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* slots, const uint32_t* count,
                               const pipnn_prune_params* p, uint64_t* row_ptr, uint32_t* col_idx, Arena& ar,
-                              const Ctx& c, const uint32_t* order, const uint32_t* order_n) {
+                              const Ctx& c, const uint32_t* order, const uint32_t* order_n, const pipnn_points* Xb) {
   const int64_t n = X->n;
+  const pipnn_points* Xg = Xb ? Xb : X;  // rows the Gram path reads (the bf16 copy of float data when given)
+  const int src_bf16 = Xg->dtype == kDtypeBf16 ? 1 : 0;
   const int R = p->R;
   uint32_t* nbr_tmp = ar.take<uint32_t>((size_t)n * R);
   uint32_t* deg = ar.take<uint32_t>(n + 1);
@@ -729,9 +735,9 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
     PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));                         \
     const int64_t blocks = first_tier ? std::min<int64_t>(ceil_div(n, w), num_sms() * 32) : (int64_t)num_sms() * 4; \
     first_tier = false;                                                                                            \
-    fn<<<(unsigned)blocks, 32 * w, sm, c.st>>>(X->data, n, X->d, X->ld, l_max, slots, count, R, p->alpha_num,      \
+    fn<<<(unsigned)blocks, 32 * w, sm, c.st>>>(Xg->data, n, X->d, Xg->ld, l_max, slots, count, R, p->alpha_num,    \
                                                p->alpha_den, nbr_tmp, deg, in_list, in_n, defer + (T) * n,        \
-                                               defer_n + (T));                                                     \
+                                               defer_n + (T), src_bf16);                                           \
     PIPNN_LAUNCHED("fp_gram_kernel", c.st);                                                                        \
     in_list = defer + (T) * n;                                                                                     \
     in_n = defer_n + (T);                                                                                          \

@@ -39,6 +39,8 @@ pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, cons
                             int64_t n_inst, int k, uint32_t* nbr, float* dist, Arena& ar, const Ctx& c,
                             int64_t max_items = 0, uint16_t* cols = nullptr);
 
+// fp32 -> bf16 copy of float points (kDtypeBf16 rows of ldb = round_up(d, 8) elements).
+pipnn_status to_bf16(const pipnn_points* X, uint16_t* Xb, int ldb, const Ctx& c);
 pipnn_status sketch_impl(const pipnn_points* X, int m, uint64_t seed, void* sketch, Arena& ar, const Ctx& c);
 
 pipnn_status hashprune_impl(int m, int l_max, int64_t n, const void* sketch, bool sk_int, uint64_t* slots,
@@ -57,7 +59,8 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
 // leaf_order); without it every point in id order.
 pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* slots, const uint32_t* count,
                               const pipnn_prune_params* p, uint64_t* row_ptr, uint32_t* col_idx, Arena& ar,
-                              const Ctx& c, const uint32_t* order = nullptr, const uint32_t* order_n = nullptr);
+                              const Ctx& c, const uint32_t* order = nullptr, const uint32_t* order_n = nullptr,
+                              const pipnn_points* Xb = nullptr);
 // Every point once, at its first instance in leaf_ids order (order[0..*order_n)).
 pipnn_status leaf_order(const uint32_t* leaf_ids, int64_t n_inst, int64_t n, uint32_t* order, uint32_t* order_n,
                         Arena& ar, const Ctx& c);

@@ -19,13 +19,14 @@ int tiled_row_bytes(const pipnn_points* X) {
 // Float rows end with the 16-element augment K-step of dist_topk.cuh: (t_hi, t_mid, t_lo, 0...) with
 // t = -||y||^2/2 (L2) or 0 (MIPS), split over three bf16 values; padding rows get t = -1e30 (u8 padding
 // rows get the norm kPadNormU8 instead), so padded columns never enter a top-k.
-template <bool U8>
+template <int SRC>  // 0: uint8, 1: float32, 2: bf16 (kDtypeBf16)
 __global__ void __launch_bounds__(256) gather_tiled_kernel(const void* __restrict__ Xv, int64_t ld, int d, int Kb,
                                                            int mips, const uint32_t* __restrict__ ids,
                                                            const TileSeg* __restrict__ segs,
                                                            const WorkItem* __restrict__ items,
                                                            const int64_t* __restrict__ n_items, uint8_t* __restrict__ T,
                                                            void* __restrict__ nrm, int* err) {
+  constexpr bool U8 = SRC == 0;
   extern __shared__ __align__(16) uint8_t st[];
   if ((int64_t)blockIdx.x >= *n_items) return;
   const WorkItem w = items[blockIdx.x];
@@ -68,6 +69,16 @@ __global__ void __launch_bounds__(256) gather_tiled_kernel(const void* __restric
           ni = __dp4a(out.y, out.y, (uint32_t)ni);
           ni = __dp4a(out.z, out.z, (uint32_t)ni);
           ni = __dp4a(out.w, out.w, (uint32_t)ni);
+        } else if (SRC == 2) {
+          // bf16 rows zero padded to ld (a multiple of 8): 16-B chunks, norm of the bf16 values
+          if (ch * 8 < ld) out = __ldg((const uint4*)((const uint16_t*)Xv + id * ld) + ch);
+          const uint32_t wv[4] = {out.x, out.y, out.z, out.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const float xl = __uint_as_float(wv[t] << 16), xh = __uint_as_float(wv[t] & 0xFFFF0000u);
+            nf = fmaf(xl, xl, nf);
+            nf = fmaf(xh, xh, nf);
+          }
         } else {
           const float* src = (const float*)Xv + id * ld;
           float f[8];
@@ -134,16 +145,16 @@ pipnn_status gather_tiled(const pipnn_points* X, const uint32_t* ids, const Tile
   const int Kb = tiled_row_bytes(X);
   const int smem = 128 * (Kb + 16);
   const int64_t ld = X->ld;
-  if (X->dtype == PIPNN_U8) {
-    PIPNN_CUDA(cudaFuncSetAttribute(gather_tiled_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    gather_tiled_kernel<true><<<(unsigned)max_items, 256, smem, c.st>>>(X->data, ld, X->d, Kb, 0, ids, segs, items,
-                                                                         n_items, T, nrm, c.err);
-  } else {
-    PIPNN_CUDA(cudaFuncSetAttribute(gather_tiled_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    gather_tiled_kernel<false><<<(unsigned)max_items, 256, smem, c.st>>>(X->data, ld, X->d, Kb,
-                                                                          X->metric == PIPNN_MIPS, ids, segs, items,
-                                                                          n_items, T, nrm, c.err);
-  }
+#define GT_LAUNCH(SRC)                                                                                             \
+  do {                                                                                                             \
+    PIPNN_CUDA(cudaFuncSetAttribute(gather_tiled_kernel<SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));  \
+    gather_tiled_kernel<SRC><<<(unsigned)max_items, 256, smem, c.st>>>(X->data, ld, X->d, Kb, X->metric == PIPNN_MIPS, \
+                                                                        ids, segs, items, n_items, T, nrm, c.err);  \
+  } while (0)
+  if (X->dtype == PIPNN_U8) GT_LAUNCH(0);
+  else if (X->dtype == kDtypeBf16) GT_LAUNCH(2);
+  else GT_LAUNCH(1);
+#undef GT_LAUNCH
   PIPNN_LAUNCHED("gather_tiled_kernel", c.st);
   return PIPNN_OK;
 }

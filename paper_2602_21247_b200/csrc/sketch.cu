@@ -1,5 +1,7 @@
 // sketch.cu — hyperplanes H (docs/DETERMINISM.md) and per-point sketches S(x)_i = H_i . x
 // (§3 "Implementation": "pre-compute m-dimensional sketches for each point"; Eq. 1).
+#include <algorithm>
+
 #include "internal.h"
 
 namespace pipnn {
@@ -25,7 +27,7 @@ __device__ __forceinline__ int32_t dp4a_su(uint32_t h_s8x4, uint32_t x_u8x4, int
   return r;
 }
 
-template <bool U8>
+template <int SRC>  // 0: uint8, 1: float32, 2: bf16 (kDtypeBf16)
 __global__ void __launch_bounds__(128) sketch_kernel(const void* __restrict__ Xv, int64_t n, int d, int64_t ld, int m,
                                                      const int8_t* __restrict__ Hg, void* __restrict__ S) {
   extern __shared__ __align__(16) int8_t Hs[];  // [m][dp] with dp = round_up(d, 16), zero padded
@@ -37,6 +39,7 @@ __global__ void __launch_bounds__(128) sketch_kernel(const void* __restrict__ Xv
   __syncthreads();
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (x >= n) return;
+  constexpr bool U8 = SRC == 0;
   if (U8) {
     int32_t acc[16];
 #pragma unroll
@@ -72,11 +75,29 @@ __global__ void __launch_bounds__(128) sketch_kernel(const void* __restrict__ Xv
       }
     }
     int32_t* out = (int32_t*)S + x * m;
-    for (int i = 0; i < m; ++i) out[i] = acc[i];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < m) out[i] = acc[i];
   } else {
     double acc[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+    if (SRC == 2) {
+      const uint16_t* row = (const uint16_t*)Xv + x * ld;  // already bf16, zero padded to ld (multiple of 8)
+      for (int j0 = 0; j0 < d; j0 += 8) {
+        const uint4 q = __ldg((const uint4*)(row + j0));
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          if (j0 + t < d) {
+            const double v = (double)__uint_as_float(((w[t >> 1] >> (16 * (t & 1))) & 0xFFFFu) << 16);
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i < m) acc[i] += (double)Hs[i * dp + j0 + t] * v;
+          }
+        }
+      }
+    } else {
     const float* row = (const float*)Xv + x * ld;
     const bool vec = ((d & 3) == 0) && ((ld & 3) == 0);
     for (int j0 = 0; j0 < d; j0 += 4) {
@@ -96,9 +117,59 @@ __global__ void __launch_bounds__(128) sketch_kernel(const void* __restrict__ Xv
           if (i < m) acc[i] += (double)Hs[i * dp + j0 + t] * v;
       }
     }
+    }
     float* out = (float*)S + x * m;
-    for (int i = 0; i < m; ++i) out[i] = (float)acc[i];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)  // static indices: acc stays in registers
+      if (i < m) out[i] = (float)acc[i];
   }
+}
+
+// fp32 -> bf16 (RNE) copy of float data, rows of ldb = round_up(d, 8) elements zero padded; non-finite input
+// raises DERR_NONFINITE. Thread per 8 output elements (two 16-B loads when aligned, one 16-B store).
+__global__ void to_bf16_kernel(const float* __restrict__ X, int64_t n, int d, int64_t ld, int ldb,
+                               uint16_t* __restrict__ Xb, int* err) {
+  const int cpr = ldb >> 3;
+  const bool vec = (d & 7) == 0 && (ld & 3) == 0;
+  const int64_t total = n * cpr;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r;
+    int ch;
+    if (total < (1ll << 32)) {  // 32-bit division when it fits (it does up to 2^32 chunks)
+      const uint32_t e32 = (uint32_t)e, r32 = e32 / (uint32_t)cpr;
+      r = r32;
+      ch = (int)(e32 - r32 * (uint32_t)cpr);
+    } else {
+      r = e / cpr;
+      ch = (int)(e - r * cpr);
+    }
+    const float* src = X + r * ld + ch * 8;
+    float f[8];
+    if (vec) {
+      const float4 a = __ldg((const float4*)src), b = __ldg((const float4*)src + 1);
+      f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+    } else {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) f[t] = ch * 8 + t < d ? __ldg(src + t) : 0.0f;
+    }
+    bool bad = false;
+    uint32_t w[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      bad |= !isfinite(f[2 * t]) || !isfinite(f[2 * t + 1]);
+      w[t] = (uint32_t)f32_to_bf16_rne(f[2 * t]) | ((uint32_t)f32_to_bf16_rne(f[2 * t + 1]) << 16);
+    }
+    if (bad) atomicExch(err, DERR_NONFINITE);
+    *(uint4*)(Xb + r * ldb + ch * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+pipnn_status to_bf16(const pipnn_points* X, uint16_t* Xb, int ldb, const Ctx& c) {
+  const int64_t work = X->n * (ldb / 8);
+  to_bf16_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(work, 256), num_sms() * 32)), 256, 0,
+                   c.st>>>((const float*)X->data, X->n, X->d, X->ld, ldb, Xb, c.err);
+  PIPNN_LAUNCHED("to_bf16_kernel", c.st);
+  return PIPNN_OK;
 }
 
 pipnn_status sketch_impl(const pipnn_points* X, int m, uint64_t seed, void* sketch, Arena& ar, const Ctx& c) {
@@ -109,15 +180,16 @@ pipnn_status sketch_impl(const pipnn_points* X, int m, uint64_t seed, void* sket
   hyperplane_kernel<<<(unsigned)ceil_div(md, 256), 256, 0, c.st>>>(m, X->d, seed, H);
   PIPNN_LAUNCHED("hyperplane_kernel", c.st);
   const int smem = (int)((int64_t)m * ((X->d + 15) & ~15));
-  if (X->dtype == PIPNN_U8) {
-    if (smem > 48 * 1024)
-      PIPNN_CUDA(cudaFuncSetAttribute(sketch_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    sketch_kernel<true><<<(unsigned)ceil_div(X->n, 128), 128, smem, c.st>>>(X->data, X->n, X->d, X->ld, m, H, sketch);
-  } else {
-    if (smem > 48 * 1024)
-      PIPNN_CUDA(cudaFuncSetAttribute(sketch_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    sketch_kernel<false><<<(unsigned)ceil_div(X->n, 128), 128, smem, c.st>>>(X->data, X->n, X->d, X->ld, m, H, sketch);
-  }
+#define SK_LAUNCH(SRC)                                                                                             \
+  do {                                                                                                             \
+    if (smem > 48 * 1024)                                                                                          \
+      PIPNN_CUDA(cudaFuncSetAttribute(sketch_kernel<SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));     \
+    sketch_kernel<SRC><<<(unsigned)ceil_div(X->n, 128), 128, smem, c.st>>>(X->data, X->n, X->d, X->ld, m, H, sketch); \
+  } while (0)
+  if (X->dtype == PIPNN_U8) SK_LAUNCH(0);
+  else if (X->dtype == kDtypeBf16) SK_LAUNCH(2);
+  else SK_LAUNCH(1);
+#undef SK_LAUNCH
   PIPNN_LAUNCHED("sketch_kernel", c.st);
   return PIPNN_OK;
 }
