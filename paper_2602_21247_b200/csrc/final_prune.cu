@@ -369,14 +369,17 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
+// Per-warp SMEM: a row tile of CP rows x (<= 128 B of K), the Gram [CP][CP+1], norms and ids. K is processed
+// in chunks of 128 B (one chunk for uint8 d <= 128), so the tile size does not grow with d.
 struct GpLayout {
-  int Kb, pitch;  // bytes of a staged row (multiple of 32), SMEM row pitch (Kb + 16)
+  int Kb, Kc, pitch;  // bytes of a staged row (multiple of 32), bytes per K-chunk (<= 128), SMEM row pitch (Kc+16)
   size_t rows_off, g_off, nrm_off, ids_off, per_warp;
 };
 __host__ __device__ inline GpLayout gp_layout(int d, bool u8, int CP) {
   GpLayout L;
   L.Kb = u8 ? (d + 31) / 32 * 32 : (d + 15) / 16 * 32;
-  L.pitch = L.Kb + 16;
+  L.Kc = L.Kb < 128 ? L.Kb : 128;
+  L.pitch = L.Kc + 16;
   size_t o = 0;
   L.rows_off = o;
   o += (size_t)CP * L.pitch;
@@ -390,28 +393,28 @@ __host__ __device__ inline GpLayout gp_layout(int d, bool u8, int CP) {
   return L;
 }
 
-// Stage rows ids[0..nr) into the tile as 16-B chunks (u8 bytes / bf16 RNE of the fp32 coordinates); chunks
-// beyond d and rows nr..nrp-1 are zero. Lane -> (row rr of a pass, chunk ch) is fixed; a pass covers 32/cpr
-// rows; 8 passes (8 independent 16-B loads per lane) are issued before the stores.
+// Stage bytes [kc0, kc0 + Kc) of rows ids[0..nr) into the tile as 16-B chunks (u8 bytes / bf16 coordinates);
+// bytes beyond the row and rows nr..nrp-1 are zero. Lane -> (row rr of a pass, chunk ch) is fixed.
 template <bool U8>
 __device__ __forceinline__ void gp_stage(const void* __restrict__ Xv, int64_t ld, int d, const uint32_t* ids, int nr,
-                                         int nrp, uint8_t* rows, const GpLayout& L, int lane, int src_bf16) {
-  const int cpr = L.Kb >> 4;  // 16-B chunks per row (<= 32)
+                                         int nrp, uint8_t* rows, const GpLayout& L, int lane, int src_bf16, int kc0) {
+  const int cpr = L.Kc >> 4;  // 16-B chunks per row and K-chunk (<= 8)
   const int rpp = 32 / cpr;   // rows per pass
   const int rr = lane / cpr, ch = lane - rr * cpr;
   const bool act = rr < rpp;
+  const int cb = kc0 + ch * 16;  // byte offset of this lane's chunk in the staged row
   const bool fast = U8 ? ((d & 15) == 0 && (ld & 15) == 0) : ((d & 7) == 0 && (ld & 3) == 0);
   if ((U8 && fast) || (!U8 && src_bf16)) {
     // cp.async straight into the tile (16 B per lane, zero fill beyond the row and for padding rows); uint8
     // rows of ld bytes, or the bf16 copy's rows of ld elements (zero padded, ld a multiple of 8)
     const int64_t rb = U8 ? ld : 2 * ld;
     const int lim = U8 ? d : (int)(2 * ld);
-    for (int r = rr; r < nrp; r += rpp) {
-      if (!act) break;
-      const bool on = r < nr && ch * 16 < lim;
-      const uint8_t* src = on ? (const uint8_t*)Xv + (int64_t)ids[r] * rb + ch * 16 : (const uint8_t*)Xv;
-      cp_async16(rows + (size_t)r * L.pitch + ch * 16, src, on ? 16u : 0u);
-    }
+    if (act)
+      for (int r = rr; r < nrp; r += rpp) {
+        const bool on = r < nr && cb < lim;
+        const uint8_t* src = on ? (const uint8_t*)Xv + (int64_t)ids[r] * rb + cb : (const uint8_t*)Xv;
+        cp_async16(rows + (size_t)r * L.pitch + ch * 16, src, on ? 16u : 0u);
+      }
     cp_async_wait_all();
     return;
   }
@@ -427,18 +430,19 @@ __device__ __forceinline__ void gp_stage(const void* __restrict__ Xv, int64_t ld
           const uint8_t* src = (const uint8_t*)Xv + id * ld;
           uint32_t w[4] = {0u, 0u, 0u, 0u};
           for (int t = 0; t < 16; ++t)
-            if (ch * 16 + t < d) w[t >> 2] |= (uint32_t)src[ch * 16 + t] << (8 * (t & 3));
+            if (cb + t < d) w[t >> 2] |= (uint32_t)src[cb + t] << (8 * (t & 3));
           v[j] = make_uint4(w[0], w[1], w[2], w[3]);
         } else {
           const float* src = (const float*)Xv + id * ld;
+          const int e0 = cb >> 1;  // first coordinate of the chunk
           float f[8];
-          if (fast && ch * 8 < d) {
-            const float4 a = __ldg((const float4*)(src + ch * 8));
-            const float4 b = __ldg((const float4*)(src + ch * 8 + 4));
+          if (fast && e0 < d) {
+            const float4 a = __ldg((const float4*)(src + e0));
+            const float4 b = __ldg((const float4*)(src + e0 + 4));
             f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
           } else {
 #pragma unroll
-            for (int t = 0; t < 8; ++t) f[t] = (ch * 8 + t < d) ? __ldg(src + ch * 8 + t) : 0.0f;
+            for (int t = 0; t < 8; ++t) f[t] = (e0 + t < d) ? __ldg(src + e0 + t) : 0.0f;
           }
           uint32_t w[4];
 #pragma unroll
@@ -502,42 +506,56 @@ __global__ void __launch_bounds__(256, CP == 32 ? 3 : 1) fp_gram_kernel(const vo
     const int nr = c + 1, nrp = (nr + 15) & ~15;
     for (int t = lane; t < nr; t += 32) ids[t] = t == 0 ? (uint32_t)u : (uint32_t)(res[t - 1] & 0xFFFFFFFFu);
     __syncwarp();
-    gp_stage<U8>(Xv, ld, d, ids, nr, nrp, rows, L, lane, src_bf16);
-    __syncwarp();
-    // ---- Gram on tensor cores: 16-row blocks x 16-row (two 8-row) blocks, K in 32-byte steps; fragments by
-    // ldmatrix (matrix m of x4 = rows +8*(m&1), bytes +16*(m>>1): exactly the a0..a3 / b0,b1 register layout)
+    // ---- Gram on tensor cores, K in chunks of <= 128 B staged per chunk: 16-row blocks x 16-row (two 8-row)
+    // blocks, 32-byte K-steps; fragments by ldmatrix (matrix m of x4 = rows +8*(m&1), bytes +16*(m>>1): exactly
+    // the a0..a3 / b0,b1 register layout); partial sums of later chunks are added to G in SMEM
     const int nb16 = nrp >> 4;
     const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 16;
-    for (int bi = 0; bi < nb16; ++bi) {
-      int32_t acc[CP / 8][4];
+    for (int kc0 = 0; kc0 < L.Kb; kc0 += L.Kc) {
+      const int kcn = min(L.Kc, L.Kb - kc0);
+      __syncwarp();
+      gp_stage<U8>(Xv, ld, d, ids, nr, nrp, rows, L, lane, src_bf16, kc0);
+      __syncwarp();
+      for (int bi = 0; bi < nb16; ++bi) {
+        int32_t acc[CP / 8][4];
 #pragma unroll
-      for (int bj = 0; bj < CP / 8; ++bj) acc[bj][0] = acc[bj][1] = acc[bj][2] = acc[bj][3] = 0;
-      const uint8_t* ra = rows + (size_t)(bi * 16 + lrow) * L.pitch + lcol;
-      for (int kb = 0; kb < L.Kb; kb += 32) {
-        uint32_t a[4];
-        ldsm_x4(a, ra + kb);
+        for (int bj = 0; bj < CP / 8; ++bj) acc[bj][0] = acc[bj][1] = acc[bj][2] = acc[bj][3] = 0;
+        const uint8_t* ra = rows + (size_t)(bi * 16 + lrow) * L.pitch + lcol;
+        for (int kb = 0; kb < kcn; kb += 32) {
+          uint32_t a[4];
+          ldsm_x4(a, ra + kb);
 #pragma unroll
-        for (int bj2 = 0; bj2 < CP / 16; ++bj2) {
-          if (bj2 < nb16) {
-            uint32_t bb[4];
-            ldsm_x4(bb, rows + (size_t)(bj2 * 16 + lrow) * L.pitch + lcol + kb);
-            const uint32_t b0[2] = {bb[0], bb[2]}, b1[2] = {bb[1], bb[3]};
-            mma_16x8<U8>(acc[2 * bj2], a, b0);
-            mma_16x8<U8>(acc[2 * bj2 + 1], a, b1);
+          for (int bj2 = 0; bj2 < CP / 16; ++bj2) {
+            if (bj2 < nb16) {
+              uint32_t bb[4];
+              ldsm_x4(bb, rows + (size_t)(bj2 * 16 + lrow) * L.pitch + lcol + kb);
+              const uint32_t b0[2] = {bb[0], bb[2]}, b1[2] = {bb[1], bb[3]};
+              mma_16x8<U8>(acc[2 * bj2], a, b0);
+              mma_16x8<U8>(acc[2 * bj2 + 1], a, b1);
+            }
           }
         }
-      }
 #pragma unroll
-      for (int bj = 0; bj < CP / 8; ++bj) {
-        if (bj < 2 * nb16) {
-          const int r = bi * 16 + g, s = bj * 8 + 2 * t4;
-          DT* d0 = G + (size_t)r * DS + s;
-          DT* d1 = G + (size_t)(r + 8) * DS + s;
-          if (U8) {
-            d0[0] = acc[bj][0]; d0[1] = acc[bj][1]; d1[0] = acc[bj][2]; d1[1] = acc[bj][3];
-          } else {
-            d0[0] = __int_as_float(acc[bj][0]); d0[1] = __int_as_float(acc[bj][1]);
-            d1[0] = __int_as_float(acc[bj][2]); d1[1] = __int_as_float(acc[bj][3]);
+        for (int bj = 0; bj < CP / 8; ++bj) {
+          if (bj < 2 * nb16) {
+            const int r = bi * 16 + g, s = bj * 8 + 2 * t4;
+            DT* d0 = G + (size_t)r * DS + s;
+            DT* d1 = G + (size_t)(r + 8) * DS + s;
+            if (U8) {
+              if (kc0 == 0) {
+                d0[0] = acc[bj][0]; d0[1] = acc[bj][1]; d1[0] = acc[bj][2]; d1[1] = acc[bj][3];
+              } else {
+                d0[0] += acc[bj][0]; d0[1] += acc[bj][1]; d1[0] += acc[bj][2]; d1[1] += acc[bj][3];
+              }
+            } else {
+              if (kc0 == 0) {
+                d0[0] = __int_as_float(acc[bj][0]); d0[1] = __int_as_float(acc[bj][1]);
+                d1[0] = __int_as_float(acc[bj][2]); d1[1] = __int_as_float(acc[bj][3]);
+              } else {
+                d0[0] += __int_as_float(acc[bj][0]); d0[1] += __int_as_float(acc[bj][1]);
+                d1[0] += __int_as_float(acc[bj][2]); d1[1] += __int_as_float(acc[bj][3]);
+              }
+            }
           }
         }
       }
