@@ -19,6 +19,8 @@
 //      (b) the next level's subproblems (children larger than C_max, key mix(K_g, l + 1)).
 // At the end, leaf sizes -> exclusive scan -> leaf_off, and the staged leaves are compacted into leaf_ids.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include <vector>
 
@@ -174,6 +176,42 @@ __global__ void leaf_compact_kernel(int64_t nl, const int64_t* __restrict__ leaf
     for (int64_t i = threadIdx.x; i < len; i += blockDim.x) out[s + i] = staging[d + i];
   }
 }
+
+// Host -> device copies of the per-depth plan go through pinned staging memory: a copy from pageable memory
+// synchronises the stream first, which would serialise the host planning with every kernel of the level.
+// Two thread-local arenas: one for the level's plan (reused after the level's synchronisation), one for the
+// leaf jobs (reused after the next level's synchronisation). Growing synchronises the stream first.
+struct PinnedArena {
+  uint8_t* base = nullptr;
+  size_t cap = 0, used = 0;
+  ~PinnedArena() {
+    if (base) cudaFreeHost(base);
+  }
+  cudaError_t copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return cudaSuccess;
+    const size_t need = (used + bytes + 255) & ~(size_t)255;
+    if (need > cap) {
+      cudaError_t e = cudaStreamSynchronize(st);  // every pending copy from this arena has completed
+      if (e != cudaSuccess) return e;
+      if (base) cudaFreeHost(base);
+      base = nullptr;
+      cap = std::max<size_t>(2 * cap, std::max<size_t>(need, (size_t)1 << 20));
+      used = 0;
+      e = cudaHostAlloc((void**)&base, cap, cudaHostAllocDefault);
+      if (e != cudaSuccess) {
+        base = nullptr;
+        cap = 0;
+        return e;
+      }
+    }
+    uint8_t* p = base + used;
+    used = (used + bytes + 255) & ~(size_t)255;
+    std::memcpy(p, src, bytes);
+    return cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, st);
+  }
+  void reset() { used = 0; }
+};
+static thread_local PinnedArena g_pin_level, g_pin_jobs;
 
 // ------------------------------------------------------------------ host helpers
 static int64_t leaders_of(int64_t sz, const pipnn_partition_params* p) {
@@ -344,8 +382,9 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
   auto flush_jobs = [&](const uint32_t* src) -> pipnn_status {
     if (jobs.empty()) return PIPNN_OK;
     if ((int64_t)jobs.size() > cp.J || (int64_t)parts.size() > cp.J) return fail(PIPNN_ECAPACITY, "partition: job capacity");
-    PIPNN_CUDA(cudaMemcpyAsync(d_jobs, jobs.data(), jobs.size() * sizeof(LeafJob), cudaMemcpyHostToDevice, st));
-    PIPNN_CUDA(cudaMemcpyAsync(d_parts, parts.data(), parts.size() * sizeof(LeafPart), cudaMemcpyHostToDevice, st));
+    g_pin_jobs.reset();  // its previous copies completed at the last synchronisation
+    PIPNN_CUDA(g_pin_jobs.copy(d_jobs, jobs.data(), jobs.size() * sizeof(LeafJob), st));
+    PIPNN_CUDA(g_pin_jobs.copy(d_parts, parts.data(), parts.size() * sizeof(LeafPart), st));
     leaf_job_kernel<<<(unsigned)jobs.size(), 256, 0, st>>>(d_jobs, (int)jobs.size(), d_parts, src, staging, leaf_size);
     PIPNN_LAUNCHED("leaf_job_kernel", st);
     // (host->device copies from pageable memory have consumed jobs/parts when they return)
@@ -373,9 +412,16 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
   }
   PIPNN_TRY(flush_jobs(memA));
 
+  static const bool dbg_timing = [] {
+    const char* e = std::getenv("PIPNN_DEBUG_TIMING");
+    return e && e[0] == '1';
+  }();
+  auto wall = [] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
   while (!open.empty()) {
     const int G = (int)open.size();
     if (G > cp.G) return fail(PIPNN_ECAPACITY, "partition: open-group capacity");
+    const double t_level0 = dbg_timing ? wall() : 0.0;
+    double t_sync0 = 0.0, t_sync1 = 0.0;
     // ---- host plan of the level
     std::vector<PGroup> hg(G);
     std::vector<int64_t> cb(G);
@@ -411,6 +457,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     std::vector<int64_t> cand_seg(G + 1, 0), lead_seg(G + 1, 0);
     bool redo_unfiltered = false;
   level_again:
+    g_pin_level.reset();  // the previous level's (or attempt's) copies completed at its synchronisation
     for (int g = 0; g < G; ++g) {
       PGroup& q = hg[g];
       if (redo_unfiltered) q.thr = ~0ull;
@@ -421,10 +468,10 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
       lead_seg[g + 1] = lead_seg[g] + q.l;
     }
     const int64_t NC = cand_seg[G];
-    PIPNN_CUDA(cudaMemcpyAsync(d_groups, hg.data(), G * sizeof(PGroup), cudaMemcpyHostToDevice, st));
-    PIPNN_CUDA(cudaMemcpyAsync(d_cbase, cb.data(), G * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    PIPNN_CUDA(cudaMemcpyAsync(d_cand_seg, cand_seg.data(), (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    PIPNN_CUDA(cudaMemcpyAsync(d_lead_seg, lead_seg.data(), (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    PIPNN_CUDA(g_pin_level.copy(d_groups, hg.data(), G * sizeof(PGroup), st));
+    PIPNN_CUDA(g_pin_level.copy(d_cbase, cb.data(), G * sizeof(int64_t), st));
+    PIPNN_CUDA(g_pin_level.copy(d_cand_seg, cand_seg.data(), (G + 1) * sizeof(int64_t), st));
+    PIPNN_CUDA(g_pin_level.copy(d_lead_seg, lead_seg.data(), (G + 1) * sizeof(int64_t), st));
     PIPNN_CUDA(cudaMemsetAsync(d_cnt, 0, G * sizeof(uint32_t), st));
     PIPNN_CUDA(cudaMemsetAsync(d_redo, 0, sizeof(int), st));
     PIPNN_CUDA(cudaMemsetAsync(ck, 0xFF, NC * sizeof(uint64_t), st));
@@ -433,6 +480,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     PIPNN_LAUNCHED("prio_kernel", st);
     prio_check_kernel<<<(unsigned)ceil_div(G, 256), 256, 0, st>>>(d_groups, G, d_cnt, d_redo);
     PIPNN_LAUNCHED("prio_check_kernel", st);
+    const double t_prio = dbg_timing ? wall() : 0.0;
     size_t tb = cub_bytes;
     if (G == 1) {
       PIPNN_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, ck, ck2, cv, cv2, (int)NC, 0, 64, st));
@@ -449,6 +497,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
       PIPNN_CUDA(cub::DeviceSegmentedSort::SortKeys(cub_tmp, tb, lead, lead_sorted, (int)C, G, d_lead_seg,
                                                     d_lead_seg + 1, st));
     }
+    const double t_leaders = dbg_timing ? wall() : 0.0;
     // ---- 2. nearest f_g leaders of every member (tcgen05 distance tiles + top-f), written directly as
     // (child = lead_off + leader index, member id) pairs with the child histogram
     std::vector<TileSeg> hA(G), hB(G);
@@ -478,14 +527,16 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     if (posA > cp.rowsA || posB > cp.rowsB) return fail(PIPNN_ECAPACITY, "partition: tiled capacity");
     const int64_t nItA = (int64_t)hItA.size(), nItB = (int64_t)hItB.size();
     const int64_t nits[2] = {nItA, nItB};
-    PIPNN_CUDA(cudaMemcpyAsync(tsA, hA.data(), G * sizeof(TileSeg), cudaMemcpyHostToDevice, st));
-    PIPNN_CUDA(cudaMemcpyAsync(tsB, hB.data(), G * sizeof(TileSeg), cudaMemcpyHostToDevice, st));
-    PIPNN_CUDA(cudaMemcpyAsync(dsegs, hD.data(), G * sizeof(DistSeg), cudaMemcpyHostToDevice, st));
-    PIPNN_CUDA(cudaMemcpyAsync(itA, hItA.data(), nItA * sizeof(WorkItem), cudaMemcpyHostToDevice, st));
-    PIPNN_CUDA(cudaMemcpyAsync(itB, hItB.data(), nItB * sizeof(WorkItem), cudaMemcpyHostToDevice, st));
-    PIPNN_CUDA(cudaMemcpyAsync(n_it, nits, 2 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    PIPNN_CUDA(g_pin_level.copy(tsA, hA.data(), G * sizeof(TileSeg), st));
+    PIPNN_CUDA(g_pin_level.copy(tsB, hB.data(), G * sizeof(TileSeg), st));
+    PIPNN_CUDA(g_pin_level.copy(dsegs, hD.data(), G * sizeof(DistSeg), st));
+    PIPNN_CUDA(g_pin_level.copy(itA, hItA.data(), nItA * sizeof(WorkItem), st));
+    PIPNN_CUDA(g_pin_level.copy(itB, hItB.data(), nItB * sizeof(WorkItem), st));
+    PIPNN_CUDA(g_pin_level.copy(n_it, nits, 2 * sizeof(int64_t), st));
+    const double t_plan2 = dbg_timing ? wall() : 0.0;
     PIPNN_TRY(gather_tiled(X, mem, tsA, itA, n_it, nItA, TA, nA, c));
     PIPNN_TRY(gather_tiled(X, lead_sorted, tsB, itB, n_it + 1, nItB, TB, nB, c));
+    const double t_gather = dbg_timing ? wall() : 0.0;
     PIPNN_CUDA(cudaMemsetAsync(ccnt, 0, C * sizeof(uint32_t), st));
     DistTopkArgs da{};
     da.Ta = TA;
@@ -504,6 +555,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     da.out_cnt = ccnt;
     da.err = c.err;
     PIPNN_TRY(launch_dist_topk(da, X->dtype == PIPNN_U8, X->metric == PIPNN_MIPS, fmax_l, st));
+    const double t_dist = dbg_timing ? wall() : 0.0;
     // ---- 3. group-by: stable radix sort of the (child, id) pairs, in member order -> every child ascending
     tb = cub_bytes;
     PIPNN_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, pk, pk2, cv2, nxt, (int)Q, 0, bits_for(C), st));
@@ -513,7 +565,9 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     PIPNN_CUDA(cudaMemcpyAsync(hccnt.data(), ccnt, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     PIPNN_CUDA(cudaMemcpyAsync(hlead.data(), lead_sorted, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     PIPNN_CUDA(cudaMemcpyAsync(&hredo, d_redo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    if (dbg_timing) t_sync0 = wall();
     PIPNN_CUDA(cudaStreamSynchronize(st));
+    if (dbg_timing) t_sync1 = wall();
     if (hredo) {
       if (redo_unfiltered) return fail(PIPNN_ECUDA, "partition: leader selection failed without filter");
       redo_unfiltered = true;  // exceedingly rare: every member becomes a leader candidate
@@ -586,6 +640,10 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     }
     if (staged > cp.L || n_leaves > cp.leaves - 1) return fail(PIPNN_ECAPACITY, "partition: leaf capacity");
     PIPNN_TRY(flush_jobs(nxt));
+    if (dbg_timing)
+      std::fprintf(stderr, "[pipnn] depth %d: groups %d members %lld | enqueue %.0f us (prio %.0f leaders %.0f plan %.0f gather %.0f dist %.0f sort %.0f), wait %.0f us, host plan %.0f us\n",
+                   depth, G, (long long)M, t_sync0 - t_level0, t_prio - t_level0, t_leaders - t_prio, t_plan2 - t_leaders,
+                   t_gather - t_plan2, t_dist - t_gather, t_sync0 - t_dist, t_sync1 - t_sync0, wall() - t_sync1);
     // next level: subproblems live in `nxt`; ping-pong the member buffers
     open.swap(next);
     std::swap(mem, nxt);
@@ -595,7 +653,8 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
   PIPNN_CUDA(cudaMemsetAsync(leaf_size + n_leaves, 0, sizeof(int64_t), st));
   size_t tb = cub_bytes;
   PIPNN_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, leaf_size, leaf_off, (int)(n_leaves + 1), st));
-  PIPNN_CUDA(cudaMemcpyAsync(leaf_dst, h_leaf_dst.data(), n_leaves * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  g_pin_level.reset();
+  PIPNN_CUDA(g_pin_level.copy(leaf_dst, h_leaf_dst.data(), n_leaves * sizeof(int64_t), st));
   if (n_leaves > 0) {
     leaf_compact_kernel<<<(unsigned)std::min<int64_t>(n_leaves, 65535), 256, 0, st>>>(n_leaves, leaf_dst, leaf_off,
                                                                                          staging, leaf_ids);
