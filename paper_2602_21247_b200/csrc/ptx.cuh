@@ -56,6 +56,22 @@ __device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity, int* e
   return false;
 }
 
+// Bounded wait with back-off (__nanosleep) for roles whose waits are not latency critical (producers, MMA
+// issuers waiting for free buffers): a spinning warp would take issue slots from the epilogue warps of its
+// sub-partition.
+__device__ __forceinline__ bool mbar_wait_sleep(uint64_t* bar, uint32_t parity, int* err_flag, int code) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ns = 32;
+  for (uint32_t it = 0; it < (1u << 22); ++it) {
+    if (mbar_try_wait(a, parity)) return true;
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+    if ((it & 255u) == 255u && err_flag && *(volatile int*)err_flag != 0) return false;
+  }
+  if (err_flag) atomicExch(err_flag, code);
+  return false;
+}
+
 // ---------------------------------------------------------------- bulk async copy (global -> shared)
 // 1-D bulk copy through the TMA engine; completes `bytes` of transaction count on `bar`.
 // dst/src 16-B aligned, bytes a multiple of 16.
