@@ -1,10 +1,15 @@
 // dist_topk.cu — instantiations + launcher of the distance-tile / top-k kernel (dist_topk.cuh).
+#include <cstdlib>
+
 #include "dist_topk.cuh"
 
 namespace pipnn {
 
 template <bool U8, bool MIPS, int KMAX>
-static pipnn_status launch_one(const DistTopkArgs& a, cudaStream_t st) {
+static pipnn_status launch_one(const DistTopkArgs& a0, cudaStream_t st) {
+  DistTopkArgs a = a0;
+  const char* dbg_env = std::getenv("PIPNN_DEBUG_EPI");  // experiment hook (read per launch)
+  a.dbg = dbg_env ? std::atoi(dbg_env) : 0;
   const int smem = dt_smem_bytes(a.Kb, U8);
   if (dt_stages(a.Kb, U8) < 2) return fail(PIPNN_EUNSUPPORTED, "dist_topk: row too long for the SMEM pipeline");
   auto* fn = dist_topk_kernel<U8, MIPS, KMAX>;

@@ -77,6 +77,7 @@ struct DistTopkArgs {
   const uint32_t* row_ids; // with out_rowid: id of local row i = row_ids[a.id_off + i]
   uint32_t* out_rowid;     // nullable: the row's id next to every output slot (same layout)
   uint32_t* out_cnt;       // nullable: out_cnt[pick id] += 1 for every valid pick (group-by histogram)
+  int dbg;                 // experiment hook (PIPNN_DEBUG_EPI): 1 = epilogue skips all tile processing, 2 = skips pass 2
   int* err;
 };
 
@@ -354,45 +355,49 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
             if (U8 && U != kInf) U = U + 1;  // key <= U  <=>  key < U + 1
             if (!U8) U = (KT)nextafterf((float)U, __int_as_float(0x7F800000));
           }
-          if (!pass2) {
-            for (int j0 = 0; j0 < Nt; j0 += 32) {
-              // ---- pass 1: group minima of 16 keys, inserted into the value list
+          if (args.dbg == 1 || (args.dbg == 2 && pass2)) {
+          } else if (!pass2) {
+            // ---- pass 1: group minima of 16 keys, inserted into the value list; 64 columns per TMEM load
+            // (one load wait per 64 columns; the tile's column count is a multiple of 32, padding columns of a
+            // 64-column load beyond Nt hold another tile's stale values and are masked to +inf)
+            for (int j0 = 0; j0 < Nt; j0 += 64) {
               const int col0 = c0 + j0;
-              int4 nb4[8];
+              const bool two = j0 + 32 < Nt;
+              int4 nb4[16];
               if (U8) {
                 const int4* p4 = reinterpret_cast<const int4*>((const int32_t*)args.nb + S.b.pos + col0);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) nb4[u] = __ldg(p4 + u);
+                for (int u = 0; u < 16; ++u) nb4[u] = (u < 8 || two) ? __ldg(p4 + u) : make_int4(0, 0, 0, 0);
               }
-              uint32_t v[32];
-              ptx::tmem_ld32(taddr + j0, v);
+              uint32_t v[64];
+              ptx::tmem_ld64(taddr + j0, v);
               ptx::tmem_ld_wait();
-              KT key[32];
-              if (U8) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                  key[4 * u + 0] = nb4[u].x - 2 * (int32_t)v[4 * u + 0];
-                  key[4 * u + 1] = nb4[u].y - 2 * (int32_t)v[4 * u + 1];
-                  key[4 * u + 2] = nb4[u].z - 2 * (int32_t)v[4 * u + 2];
-                  key[4 * u + 3] = nb4[u].w - 2 * (int32_t)v[4 * u + 3];
+              for (int gq = 0; gq < 4; ++gq) {
+                KT k16[16];
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                  const int c = 16 * gq + jj;
+                  if (U8) {
+                    const int nbv = (c & 3) == 0 ? nb4[c >> 2].x : (c & 3) == 1 ? nb4[c >> 2].y
+                                    : (c & 3) == 2 ? nb4[c >> 2].z : nb4[c >> 2].w;
+                    k16[jj] = nbv - 2 * (int32_t)v[c];
+                  } else {
+                    k16[jj] = __uint_as_float(v[c]);
+                  }
                 }
-              } else {
-#pragma unroll
-                for (int jj = 0; jj < 32; ++jj) key[jj] = __uint_as_float(v[jj]);
-              }
-#pragma unroll
-              for (int gq = 0; gq < 2; ++gq) {
-                const KT* k8 = key + 16 * gq;
                 KT gm;
                 if (U8) {
-                  gm = min(min(min(k8[0], k8[1]), min(k8[2], k8[3])), min(min(k8[4], k8[5]), min(k8[6], k8[7])));
-                  gm = min(gm, min(min(min(k8[8], k8[9]), min(k8[10], k8[11])),
-                                   min(min(k8[12], k8[13]), min(k8[14], k8[15]))));
+                  gm = min(min(min(k16[0], k16[1]), min(k16[2], k16[3])), min(min(k16[4], k16[5]), min(k16[6], k16[7])));
+                  gm = min(gm, min(min(min(k16[8], k16[9]), min(k16[10], k16[11])),
+                                   min(min(k16[12], k16[13]), min(k16[14], k16[15]))));
                 } else {
-                  gm = fminf(fminf(fminf(k8[0], k8[1]), fminf(k8[2], k8[3])), fminf(fminf(k8[4], k8[5]), fminf(k8[6], k8[7])));
-                  gm = fminf(gm, fminf(fminf(fminf(k8[8], k8[9]), fminf(k8[10], k8[11])),
-                                       fminf(fminf(k8[12], k8[13]), fminf(k8[14], k8[15]))));
+                  gm = fminf(fminf(fminf(k16[0], k16[1]), fminf(k16[2], k16[3])),
+                             fminf(fminf(k16[4], k16[5]), fminf(k16[6], k16[7])));
+                  gm = fminf(gm, fminf(fminf(fminf(k16[8], k16[9]), fminf(k16[10], k16[11])),
+                                       fminf(fminf(k16[12], k16[13]), fminf(k16[14], k16[15]))));
                 }
+                if (gq >= 2 && !two) gm = kInf;
 #pragma unroll
                 for (int t = VK - 1; t > 0; --t) {
                   if (U8) vk[t] = max(vk[t - 1], min(vk[t], gm));
