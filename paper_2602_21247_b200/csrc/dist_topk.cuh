@@ -116,9 +116,13 @@ __host__ __device__ constexpr int dt_smem_bytes(int Kb, bool u8) {
   return dt_fixed_bytes(Kb, u8) + dt_stages(Kb, u8) * kDtStageBytes;
 }
 
-// Passes per item: 2 (threshold, then exact picks). A single exact pass (U = +inf; every key of the first
-// chunk passes) measured slower even for the partition's K = 2 on B200 (C2: 3.08 vs 2.89 ms partition).
-__host__ __device__ __forceinline__ int dt_passes(int /*k*/) { return 2; }
+// Passes per item: 2 (threshold, then exact picks). A single exact pass through the queue (U = +inf; every
+// key of the first chunk passes) measured slower even for the partition's K = 2 (C2: 3.08 vs 2.89 ms
+// partition). Segments of <= 32 columns with K <= 4 and no self exclusion (the partition below depth 0: a
+// handful of leaders) take a direct single pass instead: all 32 keys of the one chunk go through the
+// branch-free (key, column) insertion network.
+__host__ __device__ __forceinline__ bool dt_direct(int k, int ncols, int self) { return ncols <= 32 && k <= 4 && !self; }
+__host__ __device__ __forceinline__ int dt_passes(int k, int ncols, int self) { return dt_direct(k, ncols, self) ? 1 : 2; }
 
 // Sorted insertion into a register list (ascending; equal keys keep the earlier entry first).
 // Precondition: key < kk[KMAX-1].
@@ -235,7 +239,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
           ptx::bulk_g2s(sA + (g * NA + slot) * KCa * 2048, args.Ta + (S.a.pos / 128 + w.rb) * (int64_t)KC * 2048,
                         KCa * 2048, &bar_a_full[g][slot]);
         }
-        const int NT = dt_passes(S.k) * T;
+        const int NT = dt_passes(S.k, S.b.rows, S.self) * T;
         for (int t = 0; t < NT; ++t) {
           const int c0 = (t % T) * kDtTileN;
           const uint8_t* srcB = args.Tb + (S.b.pos / 128 + c0 / 128) * (int64_t)KC * 2048;
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
         const WorkItem w = args.items[it];
         const int ncols = args.segs[w.seg].b.rows;
         const int T = (ncols + kDtTileN - 1) / kDtTileN;
-        const int NT = dt_passes(args.segs[w.seg].k) * T;
+        const int NT = dt_passes(args.segs[w.seg].k, ncols, args.segs[w.seg].self) * T;
         const int slot = (int)(ia % NA);
         if (!ptx::mbar_wait(&bar_a_full[g][slot], (ia / NA) & 1, args.err, DERR_WAIT_TIMEOUT)) return;
         ++ia;
@@ -341,7 +345,8 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
         KT U = kInf;
         int qlen = 0;
         const int diag_chunk = S.self ? (r0 + q * 32) : -1;  // column base of this warp's diagonal chunk
-        const int P1 = dt_passes(K) == 2 ? T : 0;  // tiles of pass 1 (none: single exact pass, U = +inf)
+        const bool direct = KMAX <= 4 && dt_direct(K, ncols, S.self);
+        const int P1 = direct ? 0 : T;  // tiles of pass 1 (none: direct single pass)
         for (int t2 = 0; t2 < P1 + T; ++t2, ++tcount) {
           const bool pass2 = t2 >= P1;
           const int c0 = (pass2 ? t2 - P1 : t2) * kDtTileN;
@@ -356,6 +361,30 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
             if (!U8) U = (KT)nextafterf((float)U, __int_as_float(0x7F800000));
           }
           if (args.dbg == 1 || (args.dbg == 2 && pass2)) {
+          } else if (direct) {
+            // ---- direct single pass (one chunk of <= 32 columns, K <= 4): every key through the insertion
+            // network (columns ascending, strict: ties keep the smaller column)
+            int4 nb4[8];
+            if (U8) {
+              const int4* p4 = reinterpret_cast<const int4*>((const int32_t*)args.nb + S.b.pos + c0);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) nb4[u] = __ldg(p4 + u);
+            }
+            uint32_t v[32];
+            ptx::tmem_ld32(taddr, v);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < 32; ++jj) {
+              KT key;
+              if (U8) {
+                const int nbv = (jj & 3) == 0 ? nb4[jj >> 2].x : (jj & 3) == 1 ? nb4[jj >> 2].y
+                                : (jj & 3) == 2 ? nb4[jj >> 2].z : nb4[jj >> 2].w;
+                key = nbv - 2 * (int32_t)v[jj];
+              } else {
+                key = __uint_as_float(v[jj]);
+              }
+              if (key < kk[KMAX - 1]) topk_insert<KT, KMAX>(kk, ii, key, (uint32_t)(c0 + jj));
+            }
           } else if (!pass2) {
             // ---- pass 1: group minima of 16 keys, inserted into the value list; 64 columns per TMEM load
             // (one load wait per 64 columns; the tile's column count is a multiple of 32, padding columns of a
