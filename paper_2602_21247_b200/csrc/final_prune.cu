@@ -671,6 +671,253 @@ __global__ void __launch_bounds__(256, CP == 32 ? 3 : 1) fp_gram_kernel(const vo
   }
 }
 
+// ------------------------------------------------------------------ cooperative tiers (CP = 64, 128)
+// Staging by a group of nt threads (thread t of the group): the same chunk layout as gp_stage.
+template <bool U8>
+__device__ __forceinline__ void gp_stage_group(const void* __restrict__ Xv, int64_t ld, int d, const uint32_t* ids,
+                                               int nr, int nrp, uint8_t* rows, const GpLayout& L, int t, int nt,
+                                               int src_bf16, int kc0) {
+  const int cpr = L.Kc >> 4;
+  const int rpp = nt / cpr;
+  const int rr = t / cpr, ch = t - rr * cpr;
+  const bool act = rr < rpp;
+  const int cb = kc0 + ch * 16;
+  const bool fast = U8 ? ((d & 15) == 0 && (ld & 15) == 0) : ((d & 7) == 0 && (ld & 3) == 0);
+  if ((U8 && fast) || (!U8 && src_bf16)) {
+    const int64_t rb = U8 ? ld : 2 * ld;
+    const int lim = U8 ? d : (int)(2 * ld);
+    if (act)
+      for (int r = rr; r < nrp; r += rpp) {
+        const bool on = r < nr && cb < lim;
+        const uint8_t* src = on ? (const uint8_t*)Xv + (int64_t)ids[r] * rb + cb : (const uint8_t*)Xv;
+        cp_async16(rows + (size_t)r * L.pitch + ch * 16, src, on ? 16u : 0u);
+      }
+    cp_async_wait_all();
+    return;
+  }
+  if (!act) return;
+  for (int r = rr; r < nrp; r += rpp) {
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (r < nr) {
+      const int64_t id = ids[r];
+      if (U8) {
+        const uint8_t* src = (const uint8_t*)Xv + id * ld;
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        for (int q = 0; q < 16; ++q)
+          if (cb + q < d) w[q >> 2] |= (uint32_t)src[cb + q] << (8 * (q & 3));
+        v = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+        const float* src = (const float*)Xv + id * ld;
+        const int e0 = cb >> 1;
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float a = e0 + 2 * q < d ? __ldg(src + e0 + 2 * q) : 0.0f;
+          const float b = e0 + 2 * q + 1 < d ? __ldg(src + e0 + 2 * q + 1) : 0.0f;
+          w[q] = (uint32_t)f32_to_bf16_rne(a) | ((uint32_t)f32_to_bf16_rne(b) << 16);
+        }
+        v = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    *(uint4*)(rows + (size_t)r * L.pitch + ch * 16) = v;
+  }
+}
+
+// One point per CTA of W = CP/32 warps (the larger reservoirs): the warps split the Gram bands, warp w owns
+// candidates 32w .. 32w+31 (one per lane), and the fixpoint of the lazy scan runs over shared admitted /
+// rejected masks with a CTA barrier per round. Same arithmetic and order rules as fp_gram_kernel.
+template <bool U8, bool MIPS, int CP>
+__global__ void __launch_bounds__(CP) fp_coop_kernel(const void* __restrict__ Xv, int64_t n, int d, int64_t ld,
+                                                     int l_max, const uint64_t* __restrict__ slots,
+                                                     const uint32_t* __restrict__ count, int R, int an, int ad,
+                                                     uint32_t* __restrict__ nbr_tmp, uint32_t* __restrict__ deg,
+                                                     const uint32_t* __restrict__ list,
+                                                     const uint32_t* __restrict__ list_n,
+                                                     uint32_t* __restrict__ defer, uint32_t* __restrict__ defer_n,
+                                                     int src_bf16) {
+  using DT = typename std::conditional<U8, int32_t, float>::type;
+  constexpr int W = CP / 32;
+  extern __shared__ __align__(16) uint8_t csm[];
+  __shared__ uint64_t skeys[CP];
+  __shared__ uint32_t sKA[W], sKR[W];
+  __shared__ int s_done;
+  const GpLayout L = gp_layout(d, U8, CP);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint8_t* rows = csm + L.rows_off;
+  DT* G = (DT*)(csm + L.g_off);
+  DT* nrm = (DT*)(csm + L.nrm_off);
+  uint32_t* ids = (uint32_t*)(csm + L.ids_off);
+  const int DS = CP + 1;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int64_t n_iter = list ? (int64_t)*list_n : n;
+  for (int64_t it = blockIdx.x; it < n_iter; it += gridDim.x) {
+    const int64_t u = list ? (int64_t)list[it] : it;
+    const int c = (int)count[u];
+    if (c > CP - 1) {
+      if (tid == 0) defer[atomicAdd(defer_n, 1u)] = (uint32_t)u;
+      continue;
+    }
+    uint32_t* out = nbr_tmp + u * (int64_t)R;
+    if (c == 0) {
+      if (tid == 0) deg[u] = 0;
+      continue;
+    }
+    const uint64_t* res = slots + u * (int64_t)l_max;
+    const int nr = c + 1, nrp = (nr + 15) & ~15;
+    __syncthreads();  // the previous point's SMEM is free
+    for (int t = tid; t < nr; t += CP) ids[t] = t == 0 ? (uint32_t)u : (uint32_t)(res[t - 1] & 0xFFFFFFFFu);
+    __syncthreads();
+    // ---- Gram (bands of 16 rows split over the warps), K in chunks of <= 128 B
+    const int nb16 = nrp >> 4;
+    const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 16;
+    for (int kc0 = 0; kc0 < L.Kb; kc0 += L.Kc) {
+      const int kcn = min(L.Kc, L.Kb - kc0);
+      gp_stage_group<U8>(Xv, ld, d, ids, nr, nrp, rows, L, tid, CP, src_bf16, kc0);
+      __syncthreads();
+      for (int bi = warp; bi < nb16; bi += W) {
+        int32_t acc[CP / 8][4];
+#pragma unroll
+        for (int bj = 0; bj < CP / 8; ++bj) acc[bj][0] = acc[bj][1] = acc[bj][2] = acc[bj][3] = 0;
+        const uint8_t* ra = rows + (size_t)(bi * 16 + lrow) * L.pitch + lcol;
+        for (int kb = 0; kb < kcn; kb += 32) {
+          uint32_t a[4];
+          ldsm_x4(a, ra + kb);
+#pragma unroll
+          for (int bj2 = 0; bj2 < CP / 16; ++bj2) {
+            if (bj2 < nb16) {
+              uint32_t bb[4];
+              ldsm_x4(bb, rows + (size_t)(bj2 * 16 + lrow) * L.pitch + lcol + kb);
+              const uint32_t b0[2] = {bb[0], bb[2]}, b1[2] = {bb[1], bb[3]};
+              mma_16x8<U8>(acc[2 * bj2], a, b0);
+              mma_16x8<U8>(acc[2 * bj2 + 1], a, b1);
+            }
+          }
+        }
+#pragma unroll
+        for (int bj = 0; bj < CP / 8; ++bj) {
+          if (bj < 2 * nb16) {
+            const int r = bi * 16 + g, sc = bj * 8 + 2 * t4;
+            DT* d0 = G + (size_t)r * DS + sc;
+            DT* d1 = G + (size_t)(r + 8) * DS + sc;
+            DT x0, x1, x2, x3;
+            if (U8) {
+              x0 = acc[bj][0]; x1 = acc[bj][1]; x2 = acc[bj][2]; x3 = acc[bj][3];
+            } else {
+              x0 = __int_as_float(acc[bj][0]); x1 = __int_as_float(acc[bj][1]);
+              x2 = __int_as_float(acc[bj][2]); x3 = __int_as_float(acc[bj][3]);
+            }
+            if (kc0 == 0) {
+              d0[0] = x0; d0[1] = x1; d1[0] = x2; d1[1] = x3;
+            } else {
+              d0[0] += x0; d0[1] += x1; d1[0] += x2; d1[1] += x3;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    for (int r = tid; r < nr; r += CP) nrm[r] = MIPS ? (DT)0 : G[(size_t)r * DS + r];
+    __syncthreads();
+    auto Dof = [&](int r, int sc, DT nr_, DT ns_) -> DT {
+      const DT gg = G[(size_t)r * DS + sc];
+      if (MIPS) return -gg;
+      if (U8) return nr_ + ns_ - 2 * gg;
+      return fmaxf(nr_ + ns_ - 2.0f * gg, 0.0f);
+    };
+    // ---- candidate i = tid (warp w, lane l): key (D(u,v), v), threshold ad * D(u, v)
+    const int i = tid;
+    uint64_t key = ~0ull;
+    DT ni = 0;
+    uint32_t thr_i = 0;
+    float thr_f = 0.0f;
+    if (i < c) {
+      ni = nrm[i + 1];
+      const DT Du = Dof(0, i + 1, nrm[0], ni);
+      key = ((uint64_t)(U8 ? (uint32_t)Du : f_ord((float)Du)) << 32) | ids[i + 1];
+      if (U8) thr_i = (uint32_t)ad * (uint32_t)Du;
+      else thr_f = (float)ad * (float)Du;
+    }
+    skeys[i] = key;
+    __syncthreads();
+    uint32_t Pm[W], M[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) Pm[w] = M[w] = 0u;
+    for (int y = 0; y < c; ++y) {
+      const uint64_t ky = skeys[y];
+      const DT ny = nrm[y + 1];
+      const bool prec = ky < key;
+      const DT Dyi = Dof(y + 1, i + 1, ny, ni);
+      bool p;
+      if (U8) p = (uint32_t)an * (uint32_t)Dyi < thr_i;
+      else p = (float)an * (float)Dyi < thr_f;
+      const uint32_t bit = 1u << (y & 31);
+#pragma unroll
+      for (int w = 0; w < W; ++w)
+        if (w == (y >> 5) && prec) {
+          Pm[w] |= bit;
+          if (p) M[w] |= bit;
+        }
+    }
+    // ---- fixpoint over shared admitted / rejected masks
+    if (tid < W) {
+      const int valid = min(32, max(0, c - 32 * tid));
+      sKA[tid] = 0u;
+      sKR[tid] = valid == 32 ? 0u : ~((1u << valid) - 1u);
+    }
+    __syncthreads();
+    for (int round = 0; round < c; ++round) {
+      uint32_t KA[W], KR[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        KA[w] = sKA[w];
+        KR[w] = sKR[w];
+      }
+      uint32_t myKA = 0u, myKR = 0u;  // (static register indices: no local-memory arrays)
+#pragma unroll
+      for (int w = 0; w < W; ++w)
+        if (w == warp) {
+          myKA = KA[w];
+          myKR = KR[w];
+        }
+      const bool undecided = !((myKA | myKR) >> lane & 1u);
+      bool hit = false, open = false;
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        hit |= (M[w] & KA[w]) != 0u;
+        open |= (M[w] & ~KR[w]) != 0u;
+      }
+      const uint32_t adm = __ballot_sync(0xffffffffu, undecided && !hit && !open);
+      const uint32_t rej = __ballot_sync(0xffffffffu, undecided && hit);
+      __syncthreads();  // everyone has read the masks of this round
+      if (lane == 0) {
+        sKA[warp] = myKA | adm;
+        sKR[warp] = myKR | rej;
+      }
+      if (tid == 0) s_done = 1;
+      __syncthreads();
+      if (lane == 0 && (sKA[warp] | sKR[warp]) != 0xFFFFFFFFu) s_done = 0;
+      __syncthreads();
+      if (s_done) break;
+    }
+    // ---- output
+    uint32_t KA[W], myKA = 0u;
+    int na = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      KA[w] = sKA[w];
+      na += __popc(KA[w]);
+      if (w == warp) myKA = KA[w];
+    }
+    if (myKA >> lane & 1u) {
+      int rank = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) rank += __popc(KA[w] & Pm[w]);
+      if (rank < R) out[rank] = (uint32_t)(key & 0xFFFFFFFFu);
+    }
+    if (tid == 0) deg[u] = (uint32_t)min(na, R);
+  }
+}
+
 __global__ void csr_copy_kernel(int64_t n, int R, const uint32_t* __restrict__ nbr_tmp, const uint32_t* __restrict__ deg,
                                 const uint64_t* __restrict__ row_ptr, uint32_t* __restrict__ col_idx) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -760,11 +1007,25 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
     in_list = defer + (T) * n;                                                                                     \
     in_n = defer_n + (T);                                                                                          \
   } while (0)
+#define GP_COOP(U, M, CPV, T)                                                                                      \
+  do {                                                                                                             \
+    const GpLayout GL = gp_layout(X->d, U, CPV);                                                                   \
+    const int sm = (int)GL.per_warp;                                                                               \
+    auto* fn = fp_coop_kernel<U, M, CPV>;                                                                          \
+    PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));                         \
+    const int per_sm = std::max(1, std::min(2048 / CPV, (int)((227 * 1024) / (sm + 2048))));                       \
+    fn<<<(unsigned)(num_sms() * per_sm), CPV, sm, c.st>>>(Xg->data, n, X->d, Xg->ld, l_max, slots, count, R,       \
+                                                          p->alpha_num, p->alpha_den, nbr_tmp, deg, in_list, in_n,  \
+                                                          defer + (T) * n, defer_n + (T), src_bf16);                \
+    PIPNN_LAUNCHED("fp_coop_kernel", c.st);                                                                        \
+    in_list = defer + (T) * n;                                                                                     \
+    in_n = defer_n + (T);                                                                                          \
+  } while (0)
 #define GP_ALL(U, M)                                                                                               \
   do {                                                                                                             \
     GP_TIER(U, M, 32, 0);                                                                                          \
-    if (l_max > 31) GP_TIER(U, M, 64, 1);                                                                          \
-    if (l_max > 63) GP_TIER(U, M, 128, 2);                                                                         \
+    if (l_max > 31) GP_COOP(U, M, 64, 1);                                                                          \
+    if (l_max > 63) GP_COOP(U, M, 128, 2);                                                                         \
     if (l_max > 127) {                                                                                             \
       auto* fn = final_prune_kernel<U, M>;                                                                         \
       PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));                    \
@@ -778,6 +1039,7 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
     else if (mips) GP_ALL(false, true);
     else GP_ALL(false, false);
 #undef GP_ALL
+#undef GP_COOP
 #undef GP_TIER
   } else {
     // final_prune = 0: the R nearest reservoir entries, generic kernel
