@@ -1,6 +1,7 @@
 // api.cu — the C ABI (include/pipnn.h): validation, workspace sizing, stream plumbing, stage timing.
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -181,6 +182,30 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   if (s != PIPNN_OK) { cleanup(); return s; }
   ar.release(mark);
   if (ar.measuring()) n_inst = bp.leaf_ids_cap;  // size the later stages at their upper bounds
+  if (!ar.measuring() && std::getenv("PIPNN_DEBUG_CHECK")) {
+    // debug: host-side check of the partition output (sorted unique ids < n, sizes <= C_max, coverage)
+    std::vector<int64_t> ho(n_leaves + 1);
+    std::vector<uint32_t> hi(n_inst);
+    cudaMemcpy(ho.data(), leaf_off, (n_leaves + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost);
+    cudaMemcpy(hi.data(), leaf_ids, n_inst * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+    std::vector<uint8_t> cov(X->n, 0);
+    int64_t bad = 0;
+    for (int64_t b = 0; b < n_leaves; ++b) {
+      const int64_t s0 = ho[b], s1 = ho[b + 1];
+      if (s1 < s0 || s1 - s0 > p->part.c_max) ++bad;
+      for (int64_t i = s0; i < s1; ++i) {
+        if (hi[i] >= (uint64_t)X->n || (i > s0 && hi[i] <= hi[i - 1])) {
+          ++bad;
+          break;
+        }
+        cov[hi[i]] = 1;
+      }
+    }
+    int64_t uncovered = 0;
+    for (int64_t i = 0; i < X->n; ++i) uncovered += !cov[i];
+    std::fprintf(stderr, "[pipnn] partition check: leaves %lld instances %lld bad %lld uncovered %lld\n",
+                 (long long)n_leaves, (long long)n_inst, (long long)bad, (long long)uncovered);
+  }
   if (!ar.measuring()) cudaEventRecord(ev[2], st);
   // (a3, a4) leaf distance tiles + fused pick, in waves of at most `budget` 128-row blocks so
   // the tiled leaf buffer stays bounded (one wave at 1M points).

@@ -65,6 +65,14 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
 pipnn_status leaf_order(const uint32_t* leaf_ids, int64_t n_inst, int64_t n, uint32_t* order, uint32_t* order_n,
                         Arena& ar, const Ctx& c);
 
+// Device carving of whole subtrees below depth 0 (partition_subtree.cu): which subproblems fit, and the launch.
+bool subtree_fits(const pipnn_points* X, const pipnn_partition_params* p, int64_t size, int depth);
+size_t subtree_group_bytes();
+pipnn_status subtree_launch(const pipnn_points* X, const pipnn_partition_params* p, const void* groups, int n_groups,
+                            const uint32_t* mem, uint32_t* staging, int64_t stage_cap, unsigned long long* stage_cursor,
+                            int64_t* leaf_dst, int64_t* leaf_size, int64_t leaf_cap, unsigned long long* leaf_count,
+                            int* work, int* err, int* max_depth, cudaStream_t st);
+
 pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params* p, int64_t* leaf_off,
                             int64_t leaf_off_cap, uint32_t* leaf_ids, int64_t leaf_ids_cap, int64_t* n_leaves_h,
                             int64_t* n_inst_h, int* depth_h, Arena& ar, const Ctx& c);
