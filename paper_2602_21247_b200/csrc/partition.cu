@@ -680,6 +680,8 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
         else keep.push_back(h);
       }
       if (!dg.empty()) {
+        // largest subproblems first (the CTAs take groups in this order): the longest serial subtrees start early
+        std::stable_sort(dg.begin(), dg.end(), [](const DevGroup& a, const DevGroup& b) { return a.size > b.size; });
         // the members live in `nxt`, which the level after next overwrites: stream order runs this first
         PIPNN_CUDA(g_pin_jobs.copy(dev_groups, dg.data(), dg.size() * sizeof(DevGroup), st));
         PIPNN_CUDA(cudaMemsetAsync(dev_work, 0, sizeof(int), st));
