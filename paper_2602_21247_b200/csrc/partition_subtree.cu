@@ -18,7 +18,7 @@
 namespace pipnn {
 
 constexpr int kStThreads = 256;
-constexpr int kStMaxMembers = 6144;   // ids per ping-pong buffer
+constexpr int kStMaxMembers = 4096;   // ids per ping-pong buffer
 constexpr int kStMaxLeaders = 64;
 constexpr int kStMaxCand = 512;       // leader-priority candidates
 constexpr int kStMaxStack = 256;
@@ -64,7 +64,6 @@ __host__ __device__ inline size_t st_smem_bytes(int d, bool u8) {
          + (size_t)kStMaxMembers                           // assignment (child index per member)
          + (size_t)kStMaxCand * 16                         // candidate (priority, id) + leader scratch
          + (size_t)kStMaxLeaders * st_row_bytes(d, u8)     // leader rows
-         + (size_t)kStUnion * 4                            // union / sort scratch
          + (size_t)kStMaxStack * sizeof(StEntry)           // DFS stack
          + (size_t)kStMaxLeaders * (kStThreads / 32) * 4   // per-warp child counts
          + 8192;                                           // small arrays
@@ -85,8 +84,7 @@ __global__ void __launch_bounds__(kStThreads, 2) subtree_kernel(const SubtreeArg
   uint64_t* ck = (uint64_t*)(asg + kStMaxMembers);
   uint32_t* cv = (uint32_t*)(ck + kStMaxCand);
   uint8_t* lrows = (uint8_t*)(cv + 2 * kStMaxCand);
-  uint32_t* uni = (uint32_t*)(lrows + (size_t)kStMaxLeaders * rb);
-  StEntry* stack = (StEntry*)(uni + kStUnion);
+  StEntry* stack = (StEntry*)(lrows + (size_t)kStMaxLeaders * rb);
   uint32_t* wcnt = (uint32_t*)(stack + kStMaxStack);            // [kStMaxLeaders][nwarps]
   uint32_t* lead = wcnt + kStMaxLeaders * (kStThreads / 32);    // [64] leader ids, ascending
   uint32_t* coff = lead + 64;                                   // [65] child offsets in dst
@@ -394,7 +392,9 @@ __global__ void __launch_bounds__(kStThreads, 2) subtree_kernel(const SubtreeArg
         s_nact = nact;
       }
       __syncthreads();
-      // ---- execute the leaf actions
+      // ---- execute the leaf actions (merged leaves are built in the subproblem's source range, free now
+      // that its members are scattered into dst; a merged leaf never holds more than the subproblem)
+      uint32_t* uni = bufs + E.buf * kStMaxMembers + E.a;
       const int nact = s_nact;
       __syncthreads();  // every thread has read the action count
       for (int a = 0; a < nact; ++a) {
@@ -516,7 +516,7 @@ pipnn_status subtree_launch(const pipnn_points* X, const pipnn_partition_params*
   a.n = X->n;
   const size_t smem = subtree_smem(X);
   PIPNN_CUDA(cudaFuncSetAttribute(subtree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  subtree_kernel<<<(unsigned)std::min(n_groups, 2 * num_sms()), kStThreads, smem, st>>>(a);
+  subtree_kernel<<<(unsigned)std::min(n_groups, 3 * num_sms()), kStThreads, smem, st>>>(a);
   PIPNN_LAUNCHED("subtree_kernel", st);
   return PIPNN_OK;
 }
