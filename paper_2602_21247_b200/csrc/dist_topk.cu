@@ -10,11 +10,15 @@ static pipnn_status launch_one(const DistTopkArgs& a0, cudaStream_t st) {
   DistTopkArgs a = a0;
   const char* dbg_env = std::getenv("PIPNN_DEBUG_EPI");  // experiment hook (read per launch)
   a.dbg = dbg_env ? std::atoi(dbg_env) : 0;
-  const int smem = dt_smem_bytes(a.Kb, U8);
-  if (dt_stages(a.Kb, U8) < 2) return fail(PIPNN_EUNSUPPORTED, "dist_topk: row too long for the SMEM pipeline");
+  // threshold-pass tiles: any column subset gives a valid bound; fewer tiles trade pass-1 work for a few more
+  // pass-2 candidates (measured on C2: 3 tiles for leaves, 2 for the partition's K <= 4)
+  const char* p1_env = std::getenv(KMAX <= 4 ? "PIPNN_P1_PART" : "PIPNN_P1");
+  a.p1cap = p1_env ? std::max(1, std::atoi(p1_env)) : (KMAX <= 4 ? 2 : (U8 ? 3 : 64));
+  const DtGeom g = dt_geom(a.Kb, !U8);
+  if (g.stages < 2) return fail(PIPNN_EUNSUPPORTED, "dist_topk: row too long for the SMEM pipeline");
   auto* fn = dist_topk_kernel<U8, MIPS, KMAX>;
-  PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  fn<<<num_sms(), kDtThreads, smem, st>>>(a);
+  PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem));
+  fn<<<num_sms(), kDtThreads, g.smem, st>>>(a);
   PIPNN_LAUNCHED("dist_topk_kernel", st);
   return PIPNN_OK;
 }
@@ -40,3 +44,10 @@ pipnn_status launch_dist_topk(const DistTopkArgs& a, bool u8, bool mips, int kma
 }
 
 }  // namespace pipnn
+
+// Experiment hook: copy out and clear the pipeline wait profile (PIPNN_DEBUG_EPI bit 64).
+extern "C" __attribute__((visibility("default"))) int pipnn_debug_dt_prof(unsigned long long* out16) {
+  if (cudaMemcpyFromSymbol(out16, pipnn::g_dt_prof, 16 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+  static const unsigned long long zero[16] = {};
+  return cudaMemcpyToSymbol(pipnn::g_dt_prof, zero, sizeof(zero)) == cudaSuccess ? 0 : 1;
+}

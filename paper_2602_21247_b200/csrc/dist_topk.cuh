@@ -77,13 +77,14 @@ struct DistTopkArgs {
   const uint32_t* row_ids; // with out_rowid: id of local row i = row_ids[a.id_off + i]
   uint32_t* out_rowid;     // nullable: the row's id next to every output slot (same layout)
   uint32_t* out_cnt;       // nullable: out_cnt[pick id] += 1 for every valid pick (group-by histogram)
-  int dbg;                 // experiment hook (PIPNN_DEBUG_EPI): 1 = epilogue skips all tile processing, 2 = skips pass 2
+  int p1cap;               // max column tiles of the threshold pass (>= 1)
+  int dbg;                 // experiment hook (PIPNN_DEBUG_EPI): low bits 1 = epilogue skips all tile processing,
+                           // 2 = skips pass 2; bit 64 = wait profile (pipnn_debug_dt_prof)
   int* err;
 };
 
-constexpr int kDtMaxStages = 8;
+constexpr int kDtMaxStages = 16;                    // B ring stages (both pipelines)
 constexpr int kDtTileN = 128;                       // columns per tile (one TMEM accumulator)
-constexpr int kDtStageBytes = 128 * 128;            // one B K-chunk: 128 columns x 128 B of K
 constexpr int kDtThreads = 384;
 constexpr int kTopkMax = 16;                        // max K (k, or the partition fanout)
 constexpr int kQCap = 16;                           // per-row candidate queue (SMEM) between drains
@@ -91,29 +92,37 @@ constexpr int kStgPitch = 36;                       // words per row of the key 
 constexpr int32_t kPadNormU8 = 0x3FFFFFFF;          // norm of a padding row: key far above any real key
 constexpr float kPadKey = 1e30f;                    // float: column term of a padding row
 
-// dynamic SMEM: A block per warpgroup [2][KCa planes][128 rows][16 B] | B ring [NS][16 KB] |
+// dynamic SMEM: A block per warpgroup [2][NA][KCa planes][128 rows][16 B] | B ring [stages][ppc planes] |
 //               key staging per warpgroup [128][kStgPitch] | queues key [kQCap][128] + col u16 [kQCap][128] |
-//               ones tile (float augment)
+//               A-side augment tile (2 planes)
 constexpr int kDtStgBytes = 128 * kStgPitch * 4;
 constexpr int kDtQBytes = kQCap * 128 * 6;
 constexpr int kDtSmemBudget = 227 * 1024 - 1024;
-__host__ __device__ constexpr int dt_a_planes(int Kb, bool u8) { return u8 ? Kb / 16 : Kb / 16 - 2; }
-// A slots per warpgroup: 2 (the next item's A block loads while the current item runs) when that still leaves
-// room for 4 B stages, else 1
-__host__ __device__ constexpr int dt_fixed_bytes_na(int Kb, bool u8, int na) {
-  return 2 * na * dt_a_planes(Kb, u8) * 2048 + 2 * kDtStgBytes + 2 * kDtQBytes + 4096;
-}
-__host__ __device__ constexpr int dt_a_slots(int Kb, bool u8) {
-  return dt_fixed_bytes_na(Kb, u8, 2) + 4 * kDtStageBytes <= kDtSmemBudget ? 2 : 1;
-}
-__host__ __device__ constexpr int dt_fixed_bytes(int Kb, bool u8) { return dt_fixed_bytes_na(Kb, u8, dt_a_slots(Kb, u8)); }
-__host__ __device__ constexpr int dt_stages(int Kb, bool u8) {
-  return (kDtSmemBudget - dt_fixed_bytes(Kb, u8)) / kDtStageBytes > kDtMaxStages
-             ? kDtMaxStages
-             : (kDtSmemBudget - dt_fixed_bytes(Kb, u8)) / kDtStageBytes;
-}
-__host__ __device__ constexpr int dt_smem_bytes(int Kb, bool u8) {
-  return dt_fixed_bytes(Kb, u8) + dt_stages(Kb, u8) * kDtStageBytes;
+// Plane geometry of a tiled buffer with Kb bytes per row: KCs planes per 128-row block (its stride), of which
+// KCm hold coordinates (float: the last 2 are the augment step that folds the column term into the MMA);
+// all KCs are multiplied, a tile's planes arriving in nchunks chunks of <= ppc planes.
+struct DtGeom {
+  int KCs, KCm, KCuse, nchunks, ppc, stage_bytes, KCa, NA, stages, smem;
+};
+__host__ __device__ inline DtGeom dt_geom(int Kb, bool fold) {
+  DtGeom g;
+  g.KCs = Kb / 16;
+  g.KCm = fold ? g.KCs - 2 : g.KCs;
+  g.KCuse = g.KCs;
+  g.nchunks = (g.KCuse + 9) / 10;  // <= 10 planes (160 B of K) per chunk: one chunk per tile up to K = 160 B
+  g.ppc = ((g.KCuse + g.nchunks - 1) / g.nchunks + 1) & ~1;
+  g.stage_bytes = g.ppc * 2048;
+  g.KCa = g.KCm;
+  const int rest = 2 * kDtStgBytes + 2 * kDtQBytes + 4096;
+  // 2 A slots per warpgroup (the next item's A block loads while the current item runs) when that still
+  // leaves room for 4 B stages, else 1
+  g.NA = 2 * 2 * g.KCa * 2048 + rest + 4 * g.stage_bytes <= kDtSmemBudget ? 2 : 1;
+  const int fixed = 2 * g.NA * g.KCa * 2048 + rest;
+  g.stages = (kDtSmemBudget - fixed) / g.stage_bytes;
+  if (g.stages > kDtMaxStages) g.stages = kDtMaxStages;
+  g.stages &= ~1;
+  g.smem = fixed + g.stages * g.stage_bytes;
+  return g;
 }
 
 // Passes per item: 2 (threshold, then exact picks). A single exact pass through the queue (U = +inf; every
@@ -122,7 +131,11 @@ __host__ __device__ constexpr int dt_smem_bytes(int Kb, bool u8) {
 // handful of leaders) take a direct single pass instead: all 32 keys of the one chunk go through the
 // branch-free (key, column) insertion network.
 __host__ __device__ __forceinline__ bool dt_direct(int k, int ncols, int self) { return ncols <= 32 && k <= 4 && !self; }
-__host__ __device__ __forceinline__ int dt_passes(int k, int ncols, int self) { return dt_direct(k, ncols, self) ? 1 : 2; }
+// Tiles of the threshold pass: the first min(T, p1cap) column tiles (any column subset gives a valid bound).
+__host__ __device__ __forceinline__ int dt_p1(int k, int ncols, int self, int p1cap) {
+  const int T = (ncols + 127) / 128;
+  return dt_direct(k, ncols, self) ? 0 : (T < p1cap ? T : p1cap);
+}
 
 // Sorted insertion into a register list (ascending; equal keys keep the earlier entry first).
 // Precondition: key < kk[KMAX-1].
@@ -157,6 +170,10 @@ __device__ __forceinline__ void topk_drain(KT (&kk)[KMAX], uint16_t (&ii)[KMAX],
   qlen = 0;
 }
 
+// Pipeline profile (experiment hook, PIPNN_DEBUG_EPI bit 64): clock64 cycles spent in each wait, per role,
+// summed over the grid; read and cleared by pipnn_debug_dt_prof (dist_topk.cu).
+static __device__ unsigned long long g_dt_prof[16];
+
 template <bool U8, bool MIPS, int KMAX>
 __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopkArgs args) {
   using KT = typename std::conditional<U8, int32_t, float>::type;
@@ -168,18 +185,21 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int Kb = args.Kb;
-  const int KC = Kb >> 4;                // 16-B K planes per row (incl. the 2 augment planes for float)
-  const int KCm = kFold ? KC - 2 : KC;   // planes of the coordinates themselves
-  const int nchunks = (KC + 7) >> 3;     // K-chunks of <= 8 planes (128 B) per tile
-  const int NS = dt_stages(Kb, U8) / 2;  // B stages per warpgroup pipeline
-  const int KCa = dt_a_planes(Kb, U8);   // == KCm: the A planes held in SMEM
-  const int NA = dt_a_slots(Kb, U8);     // A slots per warpgroup
+  const DtGeom GM = dt_geom(args.Kb, kFold);
+  const int KCs = GM.KCs;                // planes per 128-row block of the tiled buffers (block stride)
+  const int KCm = GM.KCm;                // planes of the coordinates themselves
+  const int KCu = GM.KCuse;              // planes multiplied per tile (incl. the augment step when folded)
+  const int nchunks = GM.nchunks;        // K-chunks of <= ppc planes per tile
+  const int ppc = GM.ppc;
+  const int SB = GM.stage_bytes;
+  const int NS = GM.stages / 2;          // B stages per warpgroup pipeline
+  const int KCa = GM.KCa;                // == KCm: the A planes held in SMEM
+  const int NA = GM.NA;                  // A slots per warpgroup
   uint8_t* sA = smem;                    // [2 warpgroups][NA][KCa][128][16]
-  uint8_t* ring = sA + 2 * NA * KCa * 2048;  // [2 warpgroups][NS][16 KB]
-  uint8_t* stg_base = ring + dt_stages(Kb, U8) * kDtStageBytes;
+  uint8_t* ring = sA + 2 * NA * KCa * 2048;  // [2 warpgroups][NS][SB]
+  uint8_t* stg_base = ring + GM.stages * SB;
   uint8_t* q_base = stg_base + 2 * kDtStgBytes;
-  uint8_t* sOnes = q_base + 2 * kDtQBytes;  // float: [2 planes][128 rows][16 B] A-side augment
+  uint8_t* sOnes = q_base + 2 * kDtQBytes;  // [2 planes][128 rows][16 B] A-side augment
 
   if (kFold) {
     // constant A-side augment tile: row = (1, 1, 1, 0, ...) in bf16
@@ -213,6 +233,16 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
   ptx::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
   const int64_t n_items = *args.n_items;
+  const bool prof = (args.dbg & 64) != 0;
+  unsigned long long pw[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  const unsigned long long t_start = clock64();
+#define PWAIT(slot, bar, par, err, code)                                                  \
+  [&]() {                                                                                 \
+    const unsigned long long t0_ = prof ? clock64() : 0ull;                               \
+    const bool ok_ = ptx::mbar_wait((bar), (par), (err), (code));                         \
+    if (prof) pw[slot] += clock64() - t0_;                                                \
+    return ok_;                                                                           \
+  }()
 
   // Two independent pipelines, one per epilogue warpgroup g: producer warp g, MMA warp 2 + g, TMEM
   // accumulators 2g and 2g + 1, its own A slots and B ring. Warpgroup g takes the CTA's items
@@ -223,7 +253,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
     const int g = warp;
     if (lane == 0) [&]() {
       uint32_t sg = 0, ia = 0;
-      uint8_t* my_ring = ring + g * NS * kDtStageBytes;
+      uint8_t* my_ring = ring + g * NS * SB;
       for (int64_t it = (int64_t)blockIdx.x + (int64_t)g * gridDim.x; it < n_items; it += 2 * (int64_t)gridDim.x) {
         const WorkItem w = args.items[it];
         const DistSeg S = args.segs[w.seg];
@@ -234,70 +264,102 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
           const int slot = (int)(ia % NA);
           const uint32_t ph = (ia / NA) & 1;
           ++ia;
-          if (!ptx::mbar_wait(&bar_a_empty[g][slot], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
+          if (!PWAIT(0, &bar_a_empty[g][slot], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
           ptx::mbar_arrive_expect_tx(&bar_a_full[g][slot], (uint32_t)(KCa * 2048));
-          ptx::bulk_g2s(sA + (g * NA + slot) * KCa * 2048, args.Ta + (S.a.pos / 128 + w.rb) * (int64_t)KC * 2048,
+          ptx::bulk_g2s(sA + (g * NA + slot) * KCa * 2048, args.Ta + (S.a.pos / 128 + w.rb) * (int64_t)KCs * 2048,
                         KCa * 2048, &bar_a_full[g][slot]);
         }
-        const int NT = dt_passes(S.k, S.b.rows, S.self) * T;
-        for (int t = 0; t < NT; ++t) {
-          const int c0 = (t % T) * kDtTileN;
-          const uint8_t* srcB = args.Tb + (S.b.pos / 128 + c0 / 128) * (int64_t)KC * 2048;
+        const int p1 = dt_p1(S.k, S.b.rows, S.self, args.p1cap);
+        for (int t = 0; t < p1 + T; ++t) {
+          const int c0 = (t < p1 ? t : t - p1) * kDtTileN;
+          const uint8_t* srcB = args.Tb + (S.b.pos / 128 + c0 / 128) * (int64_t)KCs * 2048;
           for (int ch = 0; ch < nchunks; ++ch, ++sg) {
             const int s = sg % NS;
             const uint32_t ph = (sg / NS) & 1;
-            if (!ptx::mbar_wait(&bar_empty[g][s], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
-            const int kc0 = ch * 8, kc1 = min(KC, kc0 + 8);
+            if (!PWAIT(1, &bar_empty[g][s], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
+            const int kc0 = ch * ppc, kc1 = min(KCu, kc0 + ppc);
             ptx::mbar_arrive_expect_tx(&bar_full[g][s], (uint32_t)((kc1 - kc0) * 2048));
-            ptx::bulk_g2s(my_ring + s * kDtStageBytes, srcB + (int64_t)kc0 * 2048, (kc1 - kc0) * 2048,
+            ptx::bulk_g2s(my_ring + s * SB, srcB + (int64_t)kc0 * 2048, (kc1 - kc0) * 2048,
                           &bar_full[g][s]);
           }
         }
       }
+      if (prof) {
+        atomicAdd(&g_dt_prof[0], pw[0]);
+        atomicAdd(&g_dt_prof[1], pw[1]);
+        atomicAdd(&g_dt_prof[2], clock64() - t_start);
+      }
     }();
   } else if (warp < 4) {
-    // ------------------------------------------------------------ MMA issuer of pipeline g (one lane)
+    // ------------------------------------------------------------ MMA issuer of pipeline g
+    // The whole warp runs the loop (converged, so descriptors and counters stay warp-uniform and live in
+    // uniform registers); one elected lane issues the tcgen05.mma / commit instructions. Descriptors of
+    // consecutive 16-B K planes differ by 2048 B = 128 in the descriptor's address field.
     const int g = warp - 2;
-    if (lane == 0) [&]() {
+    [&]() {
       uint32_t sg = 0, ia = 0, tc = 0;
-      const uint8_t* my_ring = ring + g * NS * kDtStageBytes;
+      const uint32_t ring_u32 = ptx::smem_u32(ring + g * NS * SB);
+      const uint64_t ones_desc = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(sOnes), 2048, 128);
       for (int64_t it = (int64_t)blockIdx.x + (int64_t)g * gridDim.x; it < n_items; it += 2 * (int64_t)gridDim.x) {
+        const unsigned long long ti0 = prof ? clock64() : 0ull;
         const WorkItem w = args.items[it];
-        const int ncols = args.segs[w.seg].b.rows;
+        const DistSeg Sg = args.segs[w.seg];
+        const int ncols = Sg.b.rows;
         const int T = (ncols + kDtTileN - 1) / kDtTileN;
-        const int NT = dt_passes(args.segs[w.seg].k, ncols, args.segs[w.seg].self) * T;
+        const int p1 = dt_p1(Sg.k, ncols, Sg.self, args.p1cap);
+        const int NT = p1 + T;
         const int slot = (int)(ia % NA);
-        if (!ptx::mbar_wait(&bar_a_full[g][slot], (ia / NA) & 1, args.err, DERR_WAIT_TIMEOUT)) return;
+        if (prof) pw[7] += clock64() - ti0;
+        if (!PWAIT(4, &bar_a_full[g][slot], (ia / NA) & 1, args.err, DERR_WAIT_TIMEOUT)) return;
         ++ia;
-        const uint8_t* a_base = sA + (g * NA + slot) * KCa * 2048;
+        const uint64_t a_desc = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(sA + (g * NA + slot) * KCa * 2048), 2048, 128);
         for (int t = 0; t < NT; ++t, ++tc) {
-          const int c0 = (t % T) * kDtTileN;
+          const int c0 = (t < p1 ? t : t - p1) * kDtTileN;
           const int Nt = min(kDtTileN, (ncols - c0 + 31) & ~31);
           const uint32_t buf = 2 * g + (tc & 1), use = tc >> 1;
-          if (!ptx::mbar_wait(&bar_acc_empty[buf], (use & 1) ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
+          if (!PWAIT(5, &bar_acc_empty[buf], (use & 1) ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
+          const unsigned long long tt0 = prof ? clock64() : 0ull;
+          const unsigned long long w6 = pw[6];
           ptx::tc_fence_after();
           // float: negate B (bit 14), so the accumulator is -x.y + (column term)
           const uint32_t idesc = U8 ? ptx::idesc_u8_s32(128, Nt) : (ptx::idesc_bf16_f32(128, Nt) | (1u << 14));
           const uint32_t dtm = tmem + buf * kDtTileN;
           for (int ch = 0; ch < nchunks; ++ch, ++sg) {
             const int s = sg % NS;
-            if (!ptx::mbar_wait(&bar_full[g][s], (sg / NS) & 1, args.err, DERR_WAIT_TIMEOUT)) return;
+            if (!PWAIT(6, &bar_full[g][s], (sg / NS) & 1, args.err, DERR_WAIT_TIMEOUT)) return;
             ptx::tc_fence_after();
-            const int kc0 = ch * 8, kc1 = min(KC, kc0 + 8);
-            const uint8_t* st = my_ring + s * kDtStageBytes;
-            for (int kc = kc0; kc < kc1; kc += 2) {
-              const uint8_t* a_src = (kFold && kc >= KCm) ? sOnes + (kc - KCm) * 2048 : a_base + kc * 2048;
-              const uint64_t ad = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(a_src), 2048, 128);
-              const uint64_t bd = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(st + (kc - kc0) * 2048), 2048, 128);
-              const uint32_t acc = (ch > 0 || kc > kc0) ? 1u : 0u;
-              if (U8) ptx::mma_i8(dtm, ad, bd, idesc, acc);
-              else ptx::mma_bf16(dtm, ad, bd, idesc, acc);
+            const int kc0 = ch * ppc, kc1 = min(KCu, kc0 + ppc);
+            const uint64_t b_desc = ptx::smem_desc_kmajor_noswz(ring_u32 + s * SB, 2048, 128);
+            const unsigned long long tm0 = prof ? clock64() : 0ull;
+            if (ptx::elect_one()) {
+              for (int kc = kc0; kc < kc1; kc += 2) {
+                const bool augk = kFold && kc >= KCm;
+                const uint64_t ad = augk ? ones_desc + (uint64_t)((kc - KCm) * 128) : a_desc + (uint64_t)(kc * 128);
+                const uint64_t bd = b_desc + (uint64_t)((kc - kc0) * 128);
+                const uint32_t acc = (ch > 0 || kc > kc0) ? 1u : 0u;
+                if (U8) ptx::mma_i8(dtm, ad, bd, idesc, acc);
+                else ptx::mma_bf16(dtm, ad, bd, idesc, acc);
+              }
+              ptx::mma_commit(&bar_empty[g][s]);
             }
-            ptx::mma_commit(&bar_empty[g][s]);
+            __syncwarp();
+            if (prof) pw[2] += clock64() - tm0;
           }
-          ptx::mma_commit(&bar_acc_full[buf]);
+          if (ptx::elect_one()) ptx::mma_commit(&bar_acc_full[buf]);
+          __syncwarp();
+          if (prof) pw[3] += clock64() - tt0 - (pw[6] - w6);
         }
-        ptx::mma_commit(&bar_a_empty[g][slot]);  // all of the item's MMAs issued: release its A block
+        if (ptx::elect_one()) ptx::mma_commit(&bar_a_empty[g][slot]);  // the item's MMAs issued: free its A
+        __syncwarp();
+      }
+      if (prof && lane == 0) {
+        atomicAdd(&g_dt_prof[4], pw[4]);
+        atomicAdd(&g_dt_prof[5], pw[5]);
+        atomicAdd(&g_dt_prof[6], pw[6]);
+        atomicAdd(&g_dt_prof[7], clock64() - t_start);
+        atomicAdd(&g_dt_prof[12], pw[3]);
+        atomicAdd(&g_dt_prof[14], pw[2]);
+        atomicAdd(&g_dt_prof[13], pw[7]);
       }
     }();
   } else {
@@ -327,6 +389,8 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
         const DistSeg S = args.segs[w.seg];
         const int r0 = w.rb * 128;
         const int row = r0 + tid;
+        // the row's own norm, needed only at the output: loaded now, in flight during the tiles
+        const KT na_row = (!MIPS && row < S.a.rows) ? ((const KT*)args.na)[S.a.pos + row] : (KT)0;
         const int K = S.k;
         const int K1 = K + (S.self ? 1 : 0);
         const int ncols = S.b.rows;
@@ -346,13 +410,13 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
         int qlen = 0;
         const int diag_chunk = S.self ? (r0 + q * 32) : -1;  // column base of this warp's diagonal chunk
         const bool direct = KMAX <= 4 && dt_direct(K, ncols, S.self);
-        const int P1 = direct ? 0 : T;  // tiles of pass 1 (none: direct single pass)
+        const int P1 = dt_p1(K, ncols, S.self, args.p1cap);  // tiles of pass 1 (none: direct single pass)
         for (int t2 = 0; t2 < P1 + T; ++t2, ++tcount) {
           const bool pass2 = t2 >= P1;
           const int c0 = (pass2 ? t2 - P1 : t2) * kDtTileN;
           const int Nt = min(kDtTileN, (ncols - c0 + 31) & ~31);
           const uint32_t buf = 2 * wg + (tcount & 1), use = tcount >> 1;
-          if (!ptx::mbar_wait(&bar_acc_full[buf], use & 1, args.err, DERR_WAIT_TIMEOUT)) return;
+          if (!PWAIT(8, &bar_acc_full[buf], use & 1, args.err, DERR_WAIT_TIMEOUT)) return;
           ptx::tc_fence_after();
           const uint32_t taddr = tmem + buf * kDtTileN + ((uint32_t)(q * 32) << 16);
           if (t2 == P1 && P1 > 0) {
@@ -360,7 +424,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
             if (U8 && U != kInf) U = U + 1;  // key <= U  <=>  key < U + 1
             if (!U8) U = (KT)nextafterf((float)U, __int_as_float(0x7F800000));
           }
-          if (args.dbg == 1 || (args.dbg == 2 && pass2)) {
+          if ((args.dbg & 15) == 1 || ((args.dbg & 15) == 2 && pass2)) {
           } else if (direct) {
             // ---- direct single pass (one chunk of <= 32 columns, K <= 4): every key through the insertion
             // network (columns ascending, strict: ties keep the smaller column)
@@ -504,11 +568,11 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&bar_acc_empty[buf]);
         }
+        const unsigned long long t_out = prof ? clock64() : 0ull;
         topk_drain<KT, KMAX>(kk, ii, qlen, my_qk, my_qc);
         if (row < S.a.rows) {
           const int64_t obase = S.out_off + (int64_t)row * S.ostride;
-          KT na = 0;
-          if (!MIPS) na = ((const KT*)args.na)[S.a.pos + row];
+          const KT na = na_row;
           int o = 0;
 #pragma unroll
           for (int t = 0; t < KMAX; ++t) {
@@ -538,6 +602,13 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
             if (args.out_dist) args.out_dist[obase + o] = __int_as_float(0x7F800000);
           }
         }
+        if (prof) pw[9] += clock64() - t_out;
+      }
+      if (prof && tid == 0) {
+        atomicAdd(&g_dt_prof[11], pw[9]);
+        atomicAdd(&g_dt_prof[8], pw[8]);
+        atomicAdd(&g_dt_prof[9], clock64() - t_start);
+        atomicAdd(&g_dt_prof[10], (unsigned long long)tcount);
       }
     }();
   }

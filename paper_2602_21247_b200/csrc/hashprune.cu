@@ -252,15 +252,50 @@ __global__ void __launch_bounds__(256) hp_emit_kernel(const int64_t* __restrict_
   }
   __syncthreads();
   const uint16_t* cl = cols + o0 * k;
+  // A reverse edge q -> p (carrying D(p, q)) is dropped when q's own pick list already holds p with the same D
+  // bit for bit: q's forward edge q -> p is then the identical key (same bucket h_q(p), same dist, same id),
+  // and a duplicate insert is idempotent (Alg. 3). Mutual picks are common, so this halves many merges.
+  const float* dl = dist + o0 * k;
+  uint16_t* dup = (uint16_t*)(sk + (stage_sk ? s * ms : 0));  // [s] bit t: pick t's reverse edge is a duplicate
+  auto mutual = [&](int p_local, int q_local, float Dpq) -> bool {
+    int hit = -1;
+    if (k == 8) {  // one 16-B load of q's picks
+      const uint4 v = *reinterpret_cast<const uint4*>(cl + q_local * 8);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if ((w[j] & 0xFFFFu) == (uint32_t)p_local) hit = 2 * j;
+        if ((w[j] >> 16) == (uint32_t)p_local) hit = 2 * j + 1;
+      }
+    } else {
+      for (int t = 0; t < k; ++t)
+        if (cl[q_local * k + t] == (uint16_t)p_local) hit = t;
+    }
+    return hit >= 0 && __float_as_uint(dl[q_local * k + hit]) == __float_as_uint(Dpq);
+  };
+  __shared__ uint32_t picks_sh;
+  if (threadIdx.x == 0) picks_sh = 0;
+  __syncthreads();
   // pass A: reverse in-degree of every member (thread per instance; the k picks of an instance in one go)
   for (int i = threadIdx.x; i < s; i += blockDim.x) {
     uint16_t q[16];
+    float D[16];
 #pragma unroll
     for (int t = 0; t < 16; ++t)
-      if (t < k) q[t] = cl[i * k + t];
+      if (t < k) {
+        q[t] = cl[i * k + t];
+        D[t] = dl[i * k + t];
+      }
+    uint32_t np = 0, dm = 0;
 #pragma unroll
     for (int t = 0; t < 16; ++t)
-      if (t < k && q[t] != 0xFFFFu) atomicAdd(&rc[q[t]], 1u);
+      if (t < k && q[t] != 0xFFFFu) {
+        ++np;
+        if (mutual(i, q[t], D[t])) dm |= 1u << t;
+        else atomicAdd(&rc[q[t]], 1u);
+      }
+    dup[i] = (uint16_t)dm;
+    if (np) atomicAdd(&picks_sh, np);
   }
   __syncthreads();
   // exclusive scan of rc (block-wide, thread-serial chunks + warp scan of chunk sums)
@@ -311,6 +346,7 @@ __global__ void __launch_bounds__(256) hp_emit_kernel(const int64_t* __restrict_
         D[t] = dist[(o0 + i) * k + t];
       }
     const uint32_t pid = ids[i];
+    const uint32_t dm = dup[i];
     ST sp[16];
 #pragma unroll
     for (int t = 0; t < 16; ++t)
@@ -333,13 +369,15 @@ __global__ void __launch_bounds__(256) hp_emit_kernel(const int64_t* __restrict_
         }
         const uint64_t dk = (uint64_t)dist_order_key(D[t]) << 32;
         kf = ((uint64_t)hf << 48) | dk | qid;
-        const uint32_t pos = rs[qq] + atomicAdd(&rc[qq], 1u);
-        rev[rbase + pos] = ((uint64_t)hr << 48) | dk | pid;
+        if (!((dm >> t) & 1u)) {
+          const uint32_t pos = rs[qq] + atomicAdd(&rc[qq], 1u);
+          rev[rbase + pos] = ((uint64_t)hr << 48) | dk | pid;
+        }
       }
       fwd[(o0 + i) * k + t] = kf;
     }
   }
-  if (threadIdx.x == 0) atomicAdd((unsigned long long*)n_edges, 2ull * tot_sh);
+  if (threadIdx.x == 0) atomicAdd((unsigned long long*)n_edges, 2ull * picks_sh);  // streamed edges: both directions
 }
 
 // point -> instances (inverse of leaf_ids): counting sort; the order inside a point's list is irrelevant.
@@ -614,7 +652,7 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
   max_leaf = std::max(1, std::min(max_leaf, 4096));
   const size_t sk_bytes = (size_t)max_leaf * (m | 1) * 4;
   const int stage_sk = sk_bytes <= 96 * 1024 ? 1 : 0;
-  const int smem = (int)((size_t)max_leaf * 12 + (stage_sk ? sk_bytes : 0));
+  const int smem = (int)((size_t)max_leaf * 14 + (stage_sk ? sk_bytes : 0));
   if (sk_int) {
     PIPNN_CUDA(cudaFuncSetAttribute(hp_emit_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     hp_emit_kernel<int32_t><<<(unsigned)n_leaves, 256, smem, c.st>>>(leaf_off, leaf_ids, k, cols, dist,

@@ -140,9 +140,9 @@ __global__ void __launch_bounds__(256) gather_tiled_kernel(const void* __restric
 }
 
 pipnn_status gather_tiled(const pipnn_points* X, const uint32_t* ids, const TileSeg* segs, const WorkItem* items,
-                          const int64_t* n_items, int64_t max_items, uint8_t* T, void* nrm, const Ctx& c) {
+                          const int64_t* n_items, int64_t max_items, uint8_t* T, void* nrm, const Ctx& c, int Kb) {
   if (max_items <= 0) return PIPNN_OK;
-  const int Kb = tiled_row_bytes(X);
+  if (Kb <= 0) Kb = tiled_row_bytes(X);
   const int smem = 128 * (Kb + 16);
   const int64_t ld = X->ld;
 #define GT_LAUNCH(SRC)                                                                                             \
@@ -233,7 +233,7 @@ pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, cons
   if (n_leaves == 0 || n_inst == 0) return PIPNN_OK;
   PIPNN_CUDA(cudaMemcpy2DAsync(tsegs, sizeof(TileSeg), segs, sizeof(DistSeg), sizeof(TileSeg), (size_t)n_leaves,
                                cudaMemcpyDeviceToDevice, c.st));
-  PIPNN_TRY(gather_tiled(X, leaf_ids, tsegs, items, n_items, max_items, T, nrm, c));
+  PIPNN_TRY(gather_tiled(X, leaf_ids, tsegs, items, n_items, max_items, T, nrm, c, Kb));
   DistTopkArgs a{};
   a.Ta = T;
   a.Tb = T;

@@ -120,3 +120,26 @@ def test_leaf_pick_u8_large_distances_bit_exact():
     ok = onbr != UINT32_MAX
     # the ABI's dist is float32: the exact integer D rounded to nearest (pipnn.h)
     assert np.array_equal(dist[ok], odist[ok].astype(np.float32))
+
+
+def test_leaf_pick_u8_wide_norm_range_bit_exact():
+    # leaves whose squared norms span up to ~8e6 next to narrow ones (ranking keys ||y||^2 - 2 x.y over a wide
+    # range, with near-zero rows): picks and distances stay exact
+    rng = np.random.default_rng(21)
+    narrow = np.clip(rng.normal(128, 20, size=(2000, 128)).round(), 0, 255).astype(np.uint8)
+    scale = rng.uniform(0.0, 1.0, size=(2000, 1))
+    wide = np.clip((scale * rng.integers(0, 256, size=(2000, 128))).round(), 0, 255).astype(np.uint8)
+    X = np.concatenate([narrow, wide])
+    nrm = (X.astype(np.int64) ** 2).sum(1)
+    leaves = []
+    for lo, hi, size in [(0, 2000, 1024), (0, 2000, 300), (2000, 4000, 1024), (2000, 4000, 129), (0, 4000, 700)]:
+        leaves.append(np.sort(rng.choice(np.arange(lo, hi), size=size, replace=False)).astype(np.uint32))
+    off = np.concatenate([[0], np.cumsum([len(l) for l in leaves])]).astype(np.int64)
+    ids = np.concatenate(leaves)
+    spans = [nrm[l].max() - nrm[l].min() for l in leaves]
+    assert min(spans) < 2e6 < max(spans)  # narrow and wide leaves
+    nbr, dist = run_gpu(X, "l2", off, ids, 8)
+    onbr, odist = O.leaf_pick(O.Dataset(X), off, ids, 8)
+    assert np.array_equal(nbr, onbr)
+    ok = onbr != UINT32_MAX
+    assert np.array_equal(dist[ok], odist[ok].astype(np.float32))
