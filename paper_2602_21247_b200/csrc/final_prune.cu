@@ -1,17 +1,25 @@
 // final_prune.cu — final RobustPrune of every reservoir and the CSR write-out (§4.3, P:568-570;
-// Alg. 2 P:227-248 in its lazy form P:938-942), one warp per point u (fp_gram_kernel):
+// Alg. 2 P:227-248 in its lazy form P:938-942). Per point u:
 //   1. rows = u and its c reservoir candidates, staged in shared memory (uint8 bytes, or the bf16 RNE
 //      coordinates of float rows: the path precision of DESIGN.md R19/R24);
 //   2. the (c+1)x(c+1) Gram on the tensor cores with warp-level MMAs (u8 x u8 -> s32, exact; bf16 -> f32);
 //      D(r,s) = G_rr + G_ss - 2 G_rs (L2), -G_rs (MIPS);
-//   3. lane per candidate: bitmasks of the candidates that precede it in the (D(u,.), id) order (DESIGN.md
-//      R4) and of those that would prune it (alpha_num*D(y,c) < alpha_den*D(u,c)); the lazy scan (admit c
-//      unless an admitted y prunes it; stop at R) is solved as a fixpoint over warp ballots — no sort.
-//   Tiers by reservoir occupancy (<= 31, <= 63, <= 127 candidates; larger reservoirs take the generic
-//   final_prune_kernel), so the common case runs many warps per SM with small tiles.
+//   3. prune bitmasks (alpha_num*D(y,c) < alpha_den*D(u,c)) and the (D(u,.), id) order (R4);
+//   4. the lazy scan: admit c unless an admitted earlier y prunes it; stop at R.
+// Tiers by reservoir occupancy, each a kernel shaped for its size:
+//   <= 31 candidates : one warp per point — fp_gram_kernel (uint8: Gram in SMEM, fixpoint over ballots) or
+//                      fp_warp_kernel (float: Gram in registers, masks from the MMA fragments, warp bitonic
+//                      sort, sequential scan over shuffles);
+//   <= 63            : fp_coop_kernel (uint8: a CTA of 2 warps, Gram in SMEM) or fp_band_kernel<64> (float);
+//   <= 127, <= 191   : fp_band_kernel (a warp per 16-row Gram band, masks from the fragments, a scan warp
+//                      that ranks and scans while the band warps start the next point);
+//   larger           : the generic final_prune_kernel.
 // final_prune = 0 (keep the R nearest reservoir entries) uses the generic kernel.
 // Then row_ptr = exclusive scan of the degrees and a coalesced copy into col_idx.
 #include <cub/cub.cuh>
+
+#include <cstdio>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -359,6 +367,11 @@ __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void ldsm_x4_s(uint32_t (&r)[4], uint32_t saddr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(saddr));
 }
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
@@ -918,6 +931,557 @@ __global__ void __launch_bounds__(CP) fp_coop_kernel(const void* __restrict__ Xv
   }
 }
 
+// ------------------------------------------------------------------ warp tier (<= 31 candidates)
+// One warp per point, everything in registers but the staged rows: lane t <-> Gram index t (0 = u, 1..c the
+// candidates). The 32x32 Gram (two 16-row bands x four 8-column blocks of mma.sync fragments) stays in the
+// accumulators; each thread forms the prune bits an*D(y,r) < ad*D(u,r) of its four rows r, ORs them over the
+// quad, and lane i collects its row M_i with one shuffle per (band, half). Lanes rank their candidates by
+// (D(u,.), id) and the lazy scan resolves the single batch in sorted order over ballots.
+struct WarpLayout {
+  int Kb, pitch;
+  size_t per_warp;
+};
+__host__ __device__ inline WarpLayout warp_layout(int d, bool u8) {
+  WarpLayout L;
+  L.Kb = u8 ? (d + 31) / 32 * 32 : (d + 15) / 16 * 32;
+  L.pitch = L.Kb + 16;
+  L.per_warp = ((size_t)32 * L.pitch + 2 * 32 * 4 + 32 * 4 + 127) & ~(size_t)127;  // rows | nrm, g0 | perm
+  return L;
+}
+
+template <bool U8, bool MIPS>
+__global__ void __launch_bounds__(256, 3) fp_warp_kernel(const void* __restrict__ Xv, int64_t n, int d, int64_t ld,
+                                                        int l_max, const uint64_t* __restrict__ slots,
+                                                        const uint32_t* __restrict__ count, int R, int an, int ad,
+                                                        uint32_t* __restrict__ nbr_tmp, uint32_t* __restrict__ deg,
+                                                        const uint32_t* __restrict__ list,
+                                                        const uint32_t* __restrict__ list_n,
+                                                        uint32_t* __restrict__ defer, uint32_t* __restrict__ defer_n,
+                                                        int src_bf16) {
+  using DT = typename std::conditional<U8, int32_t, float>::type;
+  extern __shared__ __align__(16) uint8_t wsm[];
+  const WarpLayout WL = warp_layout(d, U8);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  uint8_t* rows = wsm + (size_t)warp * WL.per_warp;
+  DT* nrm = (DT*)(rows + (size_t)32 * WL.pitch);
+  DT* g0 = nrm + 32;
+  uint32_t* perm = (uint32_t*)(g0 + 32);
+  const int g = lane >> 2, t4 = lane & 3;
+  const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 16;
+  const int cpr = WL.Kb >> 4;  // 16-B chunks per staged row (<= 32)
+  const int rpp = 32 / cpr, rr = lane / cpr, ch = lane - (lane / cpr) * cpr;
+  const bool act_stage = rr < rpp;
+  const bool fast = U8 ? ((d & 15) == 0 && (ld & 15) == 0) : (src_bf16 != 0);
+  const int64_t rowbytes = U8 ? ld : (src_bf16 ? 2 * ld : 4 * ld);
+  const int lim = U8 ? d : (src_bf16 ? (int)(2 * ld) : 2 * d);  // staged bytes that come from the source row
+  auto Dof = [](DT gg, DT na_, DT nb_) -> DT {
+    if (MIPS) return -gg;
+    if (U8) return na_ + nb_ - 2 * gg;
+    return fmaxf(na_ + nb_ - 2.0f * gg, 0.0f);
+  };
+  auto val = [](int32_t x) -> DT {
+    if (U8) return (DT)x;
+    return (DT)__int_as_float(x);
+  };
+  const int64_t n_iter = list ? (int64_t)*list_n : n;
+  for (int64_t it = (int64_t)blockIdx.x * wpb + warp; it < n_iter; it += (int64_t)gridDim.x * wpb) {
+    const int64_t u = list ? (int64_t)list[it] : it;
+    const int c = (int)count[u];
+    if (c > 31) {
+      if (lane == 0) defer[atomicAdd(defer_n, 1u)] = (uint32_t)u;
+      continue;
+    }
+    if (c == 0) {
+      if (lane == 0) deg[u] = 0;
+      continue;
+    }
+    const int nr = c + 1, nrp = (nr + 15) & ~15;
+    const uint32_t my_id = lane == 0 ? (uint32_t)u : (lane <= c ? (uint32_t)(slots[u * (int64_t)l_max + lane - 1] & 0xFFFFFFFFu) : 0u);
+    // ---- stage rows 0..nrp-1 (zero beyond nr and beyond the source row), 16-B chunks; lane -> (row rr of
+    // a pass of rpp rows, chunk ch) fixed
+    __syncwarp();
+    if (fast) {
+      const uint32_t dst0 = (uint32_t)__cvta_generic_to_shared(rows + (size_t)rr * WL.pitch + ch * 16);
+      const uint32_t dstep = (uint32_t)(rpp * WL.pitch);
+      const uint8_t* src0 = (const uint8_t*)Xv + ch * 16;
+      const bool col_on = act_stage && ch * 16 < lim;
+      uint32_t dst = dst0;
+      for (int r = rr; r - rr < nrp; r += rpp, dst += dstep) {
+        const uint32_t rid = __shfl_sync(0xffffffffu, my_id, r & 31);
+        if (act_stage && r < nrp) {
+          const bool on = col_on && r < nr;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
+                       "l"(src0 + (on ? (int64_t)rid * rowbytes : 0)), "r"(on ? 16u : 0u)
+                       : "memory");
+        }
+      }
+    } else {
+      for (int r0 = 0; r0 < nrp; r0 += rpp) {
+        const int r = r0 + rr;
+        const uint32_t rid = __shfl_sync(0xffffffffu, my_id, r & 31);
+        if (act_stage && r < nrp) {
+          const int cb = ch * 16;
+          uint4 v = make_uint4(0u, 0u, 0u, 0u);
+          if (r < nr && cb < lim) {
+            if (U8) {
+              const uint8_t* src = (const uint8_t*)Xv + (int64_t)rid * ld;
+              uint32_t w[4] = {0u, 0u, 0u, 0u};
+              for (int t = 0; t < 16; ++t)
+                if (cb + t < d) w[t >> 2] |= (uint32_t)src[cb + t] << (8 * (t & 3));
+              v = make_uint4(w[0], w[1], w[2], w[3]);
+            } else {
+              const float* src = (const float*)Xv + (int64_t)rid * ld;
+              const int e0 = cb >> 1;
+              uint32_t w[4];
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const float a = e0 + 2 * t < d ? __ldg(src + e0 + 2 * t) : 0.0f;
+                const float b = e0 + 2 * t + 1 < d ? __ldg(src + e0 + 2 * t + 1) : 0.0f;
+                w[t] = (uint32_t)f32_to_bf16_rne(a) | ((uint32_t)f32_to_bf16_rne(b) << 16);
+              }
+              v = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+          *(uint4*)(rows + (size_t)r * WL.pitch + cb) = v;
+        }
+      }
+    }
+    if (fast) cp_async_wait_all();
+    __syncwarp();
+    // ---- Gram: bands b = 0 (rows 0-15) and 1 (rows 16-31, when nrp = 32), column blocks of 8
+    const bool two = nrp > 16;
+    int32_t acc[2][4][4];
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int bj = 0; bj < 4; ++bj) acc[b][bj][0] = acc[b][bj][1] = acc[b][bj][2] = acc[b][bj][3] = 0;
+    {
+      const uint32_t r0a = (uint32_t)__cvta_generic_to_shared(rows + (size_t)lrow * WL.pitch + lcol);
+      const uint32_t bstep = 16u * (uint32_t)WL.pitch;
+      if (two) {
+        for (int kb = 0; kb < WL.Kb; kb += 32) {
+          uint32_t a0[4], a1[4], b0r[4], b1r[4];
+          ldsm_x4_s(a0, r0a + kb);
+          ldsm_x4_s(a1, r0a + bstep + kb);
+          b0r[0] = a0[0]; b0r[1] = a0[1]; b0r[2] = a0[2]; b0r[3] = a0[3];  // rows 0-15 as B
+          b1r[0] = a1[0]; b1r[1] = a1[1]; b1r[2] = a1[2]; b1r[3] = a1[3];  // rows 16-31 as B
+          const uint32_t c0[2] = {b0r[0], b0r[2]}, c1[2] = {b0r[1], b0r[3]};
+          const uint32_t c2[2] = {b1r[0], b1r[2]}, c3[2] = {b1r[1], b1r[3]};
+          mma_16x8<U8>(acc[0][0], a0, c0);
+          mma_16x8<U8>(acc[0][1], a0, c1);
+          mma_16x8<U8>(acc[0][2], a0, c2);
+          mma_16x8<U8>(acc[0][3], a0, c3);
+          mma_16x8<U8>(acc[1][0], a1, c0);
+          mma_16x8<U8>(acc[1][1], a1, c1);
+          mma_16x8<U8>(acc[1][2], a1, c2);
+          mma_16x8<U8>(acc[1][3], a1, c3);
+        }
+      } else {
+        for (int kb = 0; kb < WL.Kb; kb += 32) {
+          uint32_t a0[4];
+          ldsm_x4_s(a0, r0a + kb);
+          const uint32_t c0[2] = {a0[0], a0[2]}, c1[2] = {a0[1], a0[3]};
+          mma_16x8<U8>(acc[0][0], a0, c0);
+          mma_16x8<U8>(acc[0][1], a0, c1);
+        }
+      }
+    }
+    // ---- norms (the Gram diagonal; row r = 16b + 8h + g sits at column block 2b + h, offset g) and row 0
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (2 * t4 + e == g) nrm[16 * b + 8 * h + g] = val(acc[b][2 * b + h][2 * h + e]);
+    if (g == 0) {
+#pragma unroll
+      for (int bj = 0; bj < 4; ++bj) {
+        g0[8 * bj + 2 * t4] = val(acc[0][bj][0]);
+        g0[8 * bj + 2 * t4 + 1] = val(acc[0][bj][1]);
+      }
+    }
+    __syncwarp();
+    // ---- lane i: key (D(u,i), id) and threshold ad*D(u,i)
+    const DT n_me = MIPS ? (DT)0 : nrm[lane];
+    const DT n_u = MIPS ? (DT)0 : nrm[0];
+    const DT Du = Dof(g0[lane], n_u, n_me);
+    const bool cand_ok = lane >= 1 && lane <= c;
+    const uint64_t key = cand_ok ? (((uint64_t)(U8 ? (uint32_t)Du : f_ord((float)Du)) << 32) | my_id) : ~0ull;
+    DT thr_me;
+    if (U8) thr_me = (DT)((uint32_t)ad * (uint32_t)Du);
+    else thr_me = (DT)((float)ad * (float)Du);
+    // ---- prune bits of rows r = 16b + 8h + g, columns y = 8bj + 2t4 + e
+    DT nyv[4][2];
+#pragma unroll
+    for (int bj = 0; bj < 4; ++bj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) nyv[bj][e] = MIPS ? (DT)0 : __shfl_sync(0xffffffffu, n_me, 8 * bj + 2 * t4 + e);
+    const uint32_t ymask = ((c >= 31) ? 0xFFFFFFFFu : ((2u << c) - 1u)) & ~1u;  // candidates 1..c
+    uint32_t mrow[2][2] = {{0u, 0u}, {0u, 0u}};
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      if (b == 1 && !two) break;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 16 * b + 8 * h + g;
+        const DT nr_ = MIPS ? (DT)0 : __shfl_sync(0xffffffffu, n_me, r);
+        const DT th = __shfl_sync(0xffffffffu, thr_me, r);
+        uint32_t w = 0u;
+#pragma unroll
+        for (int bj = 0; bj < 4; ++bj) {
+          if (bj >= 2 && !two) break;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const DT D = Dof(val(acc[b][bj][2 * h + e]), nr_, nyv[bj][e]);
+            bool pr;
+            if (U8) pr = (uint32_t)an * (uint32_t)D < (uint32_t)th;
+            else pr = (float)an * (float)D < (float)th;
+            w |= (pr ? 1u : 0u) << (8 * bj + 2 * t4 + e);
+          }
+        }
+        w |= __shfl_xor_sync(0xffffffffu, w, 1);
+        w |= __shfl_xor_sync(0xffffffffu, w, 2);
+        mrow[b][h] = w & ymask & ~(1u << r);
+      }
+    }
+    // lane i <- M_i from the quad holding row i (b = i >> 4, h = (i >> 3) & 1, g = i & 7)
+    uint32_t Mi = 0u;
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t v = __shfl_sync(0xffffffffu, mrow[b][h], 4 * (lane & 7));
+        if ((lane >> 4) == b && ((lane >> 3) & 1) == h) Mi = v;
+      }
+    // ---- bitonic sort of (key, Gram index) over the warp: lane k ends with the k-th candidate (keys are
+    // distinct; non-candidates carry ~0 and sort last)
+    uint64_t sk = key;
+    int i = lane;
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const uint64_t ok = __shfl_xor_sync(0xffffffffu, sk, stride);
+        const int oi = __shfl_xor_sync(0xffffffffu, i, stride);
+        const bool up = (lane & size) == 0;           // ascending block
+        const bool lower = (lane & stride) == 0;      // this lane keeps the smaller of the pair when up
+        const bool take = (lower == up) ? (ok < sk) : (ok > sk);
+        if (take) {
+          sk = ok;
+          i = oi;
+        }
+      }
+    }
+    // ---- lazy scan in sorted order: lane k holds the k-th candidate's Gram index and prune mask; the
+    // admitted set (Gram-index bits) is updated once per step
+    const bool inb = lane < c;
+    const uint32_t Mk = __shfl_sync(0xffffffffu, Mi, i);
+    uint32_t adm = 0u, admS = 0u;
+    for (int k = 0; k < c; ++k) {
+      const uint32_t mk = __shfl_sync(0xffffffffu, Mk, k);
+      const int ik = __shfl_sync(0xffffffffu, i, k);
+      if ((mk & adm) == 0u) {
+        adm |= 1u << ik;
+        admS |= 1u << k;
+      }
+    }
+    const uint32_t id_i = __shfl_sync(0xffffffffu, my_id, i);
+    const int pos = __popc(admS & ((1u << lane) - 1u));
+    if (((admS >> lane) & 1u) && pos < R) nbr_tmp[u * (int64_t)R + pos] = id_i;
+    if (lane == 0) deg[u] = (uint32_t)min(__popc(admS), R);
+  }
+}
+
+// ------------------------------------------------------------------ band tiers (CP = 64, 128, 192)
+// One point per CTA pass: CP/16 "band" warps and one "scan" warp. Band warp b owns the 16-row band b of the
+// (c+1)x(c+1) Gram, whole rows staged once (no K chunks, so the accumulators stay in registers and the Gram
+// never goes to SMEM). From its fragments each thread forms the prune bits of its two rows r
+// (an*D(y,r) < ad*D(u,r), every y: in the scan only earlier y can act) and ORs them over the quad into 32-bit
+// words M[r]. The scan warp ranks the candidates by (D(u,.), id) and runs the lazy scan 32
+// candidates at a time (a lane per candidate, pruned by the admitted set A or by an earlier admitted candidate
+// of its batch, resolved over ballots) while the band warps already work on the next point: ids, keys and M
+// are double buffered and handed over with named barriers (READY[b]: band -> scan, FREE[b]: scan -> band).
+struct BandLayout {
+  int Kb, pitch;
+  size_t rows_off, m_off, key_off, nrm_off, g0_off, thr_off, ids_off, perm_off, bytes;
+};
+__host__ __device__ inline BandLayout band_layout(int d, bool u8, int CP) {
+  BandLayout L;
+  L.Kb = u8 ? (d + 31) / 32 * 32 : (d + 15) / 16 * 32;
+  L.pitch = L.Kb + 16;  // odd multiple of 16 B: conflict-free ldmatrix rows
+  size_t o = 0;
+  L.rows_off = o;
+  o += (size_t)CP * L.pitch;
+  L.m_off = o;  // [2][CP][CP/32]
+  o += (size_t)2 * CP * (CP / 32) * 4;
+  L.key_off = o;  // [2][CP]
+  o += (size_t)2 * CP * 8;
+  L.nrm_off = o;
+  o += (size_t)CP * 4;
+  L.g0_off = o;
+  o += (size_t)CP * 4;
+  L.thr_off = o;
+  o += (size_t)CP * 4;
+  L.ids_off = o;  // [2][CP]
+  o += (size_t)2 * CP * 4;
+  L.perm_off = o;
+  o += (size_t)CP * 4;
+  L.bytes = (o + 127) & ~(size_t)127;
+  return L;
+}
+__device__ __forceinline__ void named_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <bool U8, bool MIPS, int CP>
+__global__ void __launch_bounds__(2 * CP + 32, CP <= 64 ? 4 : (CP <= 128 ? 2 : 1)) fp_band_kernel(const void* __restrict__ Xv, int64_t n, int d, int64_t ld,
+                                                       int l_max, const uint64_t* __restrict__ slots,
+                                                       const uint32_t* __restrict__ count, int R, int an, int ad,
+                                                       uint32_t* __restrict__ nbr_tmp, uint32_t* __restrict__ deg,
+                                                       const uint32_t* __restrict__ list,
+                                                       const uint32_t* __restrict__ list_n,
+                                                       uint32_t* __restrict__ defer, uint32_t* __restrict__ defer_n,
+                                                       int src_bf16) {
+  using DT = typename std::conditional<U8, int32_t, float>::type;
+  constexpr int NW = CP / 16;  // band warps
+  constexpr int NB_T = 32 * NW;  // band threads
+  constexpr int W = CP / 32;   // mask words per row
+  constexpr int NB = CP / 8;   // 8-column fragments per band
+  constexpr int kBarBand = 1, kBarReady = 2, kBarFree = 4;  // named barriers (0 = __syncthreads)
+  extern __shared__ __align__(16) uint8_t bsm[];
+  const BandLayout BL = band_layout(d, U8, CP);
+  GpLayout L;  // full-row staging view for gp_stage_group
+  L.Kb = BL.Kb;
+  L.Kc = BL.Kb;
+  L.pitch = BL.pitch;
+  uint8_t* rows = bsm + BL.rows_off;
+  uint32_t* Mb = (uint32_t*)(bsm + BL.m_off);
+  uint64_t* skeyb = (uint64_t*)(bsm + BL.key_off);
+  DT* nrm = (DT*)(bsm + BL.nrm_off);
+  DT* g0 = (DT*)(bsm + BL.g0_off);
+  DT* thr = (DT*)(bsm + BL.thr_off);
+  uint32_t* idsb = (uint32_t*)(bsm + BL.ids_off);
+  uint32_t* perm = (uint32_t*)(bsm + BL.perm_off);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t n_iter = list ? (int64_t)*list_n : n;
+  int p = 0;  // points handed over so far (buffer = p & 1)
+  if (warp < NW) {
+    // ================================================================ band warps
+    const int g = lane >> 2, t4 = lane & 3;
+    const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 16;
+    auto Dof = [](DT gg, DT na_, DT nb_) -> DT {
+      if (MIPS) return -gg;
+      if (U8) return na_ + nb_ - 2 * gg;
+      return fmaxf(na_ + nb_ - 2.0f * gg, 0.0f);
+    };
+    auto val = [](int32_t x) -> DT {
+      if (U8) return (DT)x;
+      return (DT)__int_as_float(x);
+    };
+    for (int64_t it = blockIdx.x; it < n_iter; it += gridDim.x) {
+      const int64_t u = list ? (int64_t)list[it] : it;
+      const int c = (int)count[u];
+      if (c > CP - 1) {
+        if (tid == 0) defer[atomicAdd(defer_n, 1u)] = (uint32_t)u;
+        continue;
+      }
+      if (c == 0) {
+        if (tid == 0) deg[u] = 0;
+        continue;
+      }
+      const int bsel = p & 1;
+      uint32_t* ids = idsb + bsel * CP;
+      uint32_t* M = Mb + bsel * CP * W;
+      uint64_t* skey = skeyb + bsel * CP;
+      if (p >= 2) named_sync(kBarFree + bsel, NB_T + 32);  // the scan of point p-2 released this buffer
+      const uint64_t* res = slots + u * (int64_t)l_max;
+      const int nr = c + 1, nrp = (nr + 15) & ~15;
+      named_sync(kBarBand, NB_T);  // the previous point's rows / nrm / g0 / thr are no longer read
+      for (int t = tid; t < nr; t += NB_T) ids[t] = t == 0 ? (uint32_t)u : (uint32_t)(res[t - 1] & 0xFFFFFFFFu);
+      named_sync(kBarBand, NB_T);
+      gp_stage_group<U8>(Xv, ld, d, ids, nr, nrp, rows, L, tid, NB_T, src_bf16, 0);
+      named_sync(kBarBand, NB_T);
+      // ---- Gram band of this warp (rows 16*warp .. +15), every column block (rows beyond nrp hold stale
+      // bytes; their columns are never read), K = the whole row
+      const bool act = warp * 16 < nrp;
+      int32_t acc[NB][4];
+#pragma unroll
+      for (int bj = 0; bj < NB; ++bj) acc[bj][0] = acc[bj][1] = acc[bj][2] = acc[bj][3] = 0;
+      if (act) {
+        const uint32_t ra = (uint32_t)__cvta_generic_to_shared(rows + (size_t)(warp * 16 + lrow) * L.pitch + lcol);
+        const uint32_t rb = (uint32_t)__cvta_generic_to_shared(rows + (size_t)lrow * L.pitch + lcol);
+        const uint32_t bstep = 16u * (uint32_t)L.pitch;
+        for (int kb = 0; kb < L.Kb; kb += 32) {
+          uint32_t a[4];
+          ldsm_x4_s(a, ra + kb);
+#pragma unroll
+          for (int bj2 = 0; bj2 < CP / 16; ++bj2) {
+            uint32_t bb[4];
+            ldsm_x4_s(bb, rb + bj2 * bstep + kb);
+            const uint32_t b0[2] = {bb[0], bb[2]}, b1[2] = {bb[1], bb[3]};
+            mma_16x8<U8>(acc[2 * bj2], a, b0);
+            mma_16x8<U8>(acc[2 * bj2 + 1], a, b1);
+          }
+        }
+      }
+      const int r0 = warp * 16 + g, r1 = r0 + 8;
+      // ---- row 0 of the Gram (u against every candidate) and the squared norms (from the staged rows)
+      if (warp == 0 && g == 0) {
+#pragma unroll
+        for (int bj = 0; bj < NB; ++bj) {
+          g0[bj * 8 + 2 * t4] = val(acc[bj][0]);
+          g0[bj * 8 + 2 * t4 + 1] = val(acc[bj][1]);
+        }
+      }
+      if (!MIPS) {
+        for (int r = tid; r < nr; r += NB_T) {
+          const uint4* rw = reinterpret_cast<const uint4*>(rows + (size_t)r * L.pitch);
+          int32_t si = 0;
+          float sf = 0.0f;
+          for (int q = 0; q < (L.Kb >> 4); ++q) {
+            const uint4 v4 = rw[q];
+            const uint32_t wv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              if (U8) {
+                si = (int32_t)__dp4a(wv[e], wv[e], (uint32_t)si);
+              } else {
+                const float lo = __uint_as_float(wv[e] << 16), hi = __uint_as_float(wv[e] & 0xFFFF0000u);
+                sf = fmaf(lo, lo, sf);
+                sf = fmaf(hi, hi, sf);
+              }
+            }
+          }
+          if (U8) nrm[r] = (DT)si;
+          else nrm[r] = (DT)sf;
+        }
+      }
+      named_sync(kBarBand, NB_T);
+      // ---- keys (D(u,y), id) and thresholds ad*D(u,y) of the candidates y = 1..c
+      for (int y = tid + 1; y <= c; y += NB_T) {
+        const DT ny = MIPS ? (DT)0 : nrm[y];
+        const DT Du = Dof(g0[y], MIPS ? (DT)0 : nrm[0], ny);
+        skey[y] = ((uint64_t)(U8 ? (uint32_t)Du : f_ord((float)Du)) << 32) | ids[y];
+        if (U8) thr[y] = (DT)((uint32_t)ad * (uint32_t)Du);
+        else thr[y] = (DT)((float)ad * (float)Du);
+      }
+      named_sync(kBarBand, NB_T);
+      // ---- prune bits of rows r0, r1 (Gram indices; candidates are 1..c), OR-reduced over the quad
+      if (act) {
+        const DT n0 = (MIPS || r0 > c) ? (DT)0 : nrm[r0], n1 = (MIPS || r1 > c) ? (DT)0 : nrm[r1];
+        const DT th0 = (r0 >= 1 && r0 <= c) ? thr[r0] : (DT)0, th1 = (r1 >= 1 && r1 <= c) ? thr[r1] : (DT)0;
+        uint32_t w0[W], w1[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) w0[k] = w1[k] = 0u;
+#pragma unroll
+        for (int bj = 0; bj < NB; ++bj) {
+          if (bj * 8 < nrp) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int y = bj * 8 + 2 * t4 + e;
+              if (y >= 1 && y <= c) {
+                const DT ny = MIPS ? (DT)0 : nrm[y];
+                const DT D0 = Dof(val(acc[bj][e]), n0, ny), D1 = Dof(val(acc[bj][2 + e]), n1, ny);
+                bool p0, p1;
+                if (U8) {
+                  p0 = (uint32_t)an * (uint32_t)D0 < (uint32_t)th0;
+                  p1 = (uint32_t)an * (uint32_t)D1 < (uint32_t)th1;
+                } else {
+                  p0 = (float)an * (float)D0 < (float)th0;
+                  p1 = (float)an * (float)D1 < (float)th1;
+                }
+                const uint32_t bit = 1u << ((bj & 3) * 8 + 2 * t4 + e);
+                if (p0 && y != r0) w0[bj >> 2] |= bit;
+                if (p1 && y != r1) w1[bj >> 2] |= bit;
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+          w0[k] |= __shfl_xor_sync(0xffffffffu, w0[k], 1);
+          w0[k] |= __shfl_xor_sync(0xffffffffu, w0[k], 2);
+          w1[k] |= __shfl_xor_sync(0xffffffffu, w1[k], 1);
+          w1[k] |= __shfl_xor_sync(0xffffffffu, w1[k], 2);
+        }
+        if (t4 == 0) {
+#pragma unroll
+          for (int k = 0; k < W; ++k) {
+            if (r0 <= c) M[r0 * W + k] = w0[k];
+            if (r1 <= c) M[r1 * W + k] = w1[k];
+          }
+        }
+      }
+      __threadfence_block();
+      named_arrive(kBarReady + bsel, NB_T + 32);  // ids, keys and M of point p are complete
+      ++p;
+    }
+  } else {
+    // ================================================================ scan warp
+    for (int64_t it = blockIdx.x; it < n_iter; it += gridDim.x) {
+      const int64_t u = list ? (int64_t)list[it] : it;
+      const int c = (int)count[u];
+      if (c > CP - 1 || c == 0) continue;
+      const int bsel = p & 1;
+      const uint32_t* ids = idsb + bsel * CP;
+      const uint32_t* M = Mb + bsel * CP * W;
+      const uint64_t* skey = skeyb + bsel * CP;
+      named_sync(kBarReady + bsel, NB_T + 32);
+      // ---- rank of every candidate in the (D(u,.), id) order (keys are distinct: ids are)
+      for (int y = lane + 1; y <= c; y += 32) {
+        const uint64_t ky = skey[y];
+        int rank = 0;
+        for (int z = 1; z <= c; ++z) rank += skey[z] < ky ? 1 : 0;
+        perm[rank] = (uint32_t)y;
+      }
+      __syncwarp();
+      // ---- lazy scan, 32 candidates per step
+      uint32_t* out = nbr_tmp + u * (int64_t)R;
+      uint32_t A[W];
+#pragma unroll
+      for (int k = 0; k < W; ++k) A[k] = 0u;
+      int na = 0;
+      for (int b0 = 0; b0 < c && na < R; b0 += 32) {
+        const bool inb = b0 + lane < c;
+        const int i = inb ? (int)perm[b0 + lane] : 0;
+        const uint32_t* Mi = M + i * W;
+        bool hitA = false;
+#pragma unroll
+        for (int k = 0; k < W; ++k) hitA |= ((inb ? Mi[k] : 0u) & A[k]) != 0u;
+        // intra-batch pruners: bit k = candidate at batch position k (< lane) prunes me
+        uint32_t intra = 0u;
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+          const int ik = __shfl_sync(0xffffffffu, i, k);
+          if (k < lane && inb && ((Mi[ik >> 5] >> (ik & 31)) & 1u)) intra |= 1u << k;
+        }
+        const uint32_t cand = __ballot_sync(0xffffffffu, inb && !hitA);
+        uint32_t adm = 0u;
+        for (int k = 0; k < 32; ++k) {
+          const uint32_t ik_intra = __shfl_sync(0xffffffffu, intra, k);
+          if (((cand >> k) & 1u) && (ik_intra & adm) == 0u) adm |= 1u << k;
+        }
+        const bool me = (adm >> lane) & 1u;
+        const int pos = na + __popc(adm & ((1u << lane) - 1u));
+        if (me && pos < R) out[pos] = ids[i];
+        na += __popc(adm);
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+          A[k] |= __reduce_or_sync(0xffffffffu, (me && (i >> 5) == k) ? (1u << (i & 31)) : 0u);
+      }
+      if (lane == 0) deg[u] = (uint32_t)min(na, R);
+      __syncwarp();
+      named_arrive(kBarFree + bsel, NB_T + 32);  // buffer bsel may be refilled (point p + 2)
+      ++p;
+    }
+  }
+}
+
 __global__ void csr_copy_kernel(int64_t n, int R, const uint32_t* __restrict__ nbr_tmp, const uint32_t* __restrict__ deg,
                                 const uint64_t* __restrict__ row_ptr, uint32_t* __restrict__ col_idx) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -969,8 +1533,8 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
   const int R = p->R;
   uint32_t* nbr_tmp = ar.take<uint32_t>((size_t)n * R);
   uint32_t* deg = ar.take<uint32_t>(n + 1);
-  uint32_t* defer = ar.take<uint32_t>((size_t)3 * n);
-  uint32_t* defer_n = ar.take<uint32_t>(4);
+  uint32_t* defer = ar.take<uint32_t>((size_t)4 * n);
+  uint32_t* defer_n = ar.take<uint32_t>(5);
   size_t tmp_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, (const uint32_t*)nullptr, (uint64_t*)nullptr, (int)(n + 1));
   void* tmp = ar.take<uint8_t>(tmp_bytes);
@@ -979,7 +1543,7 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
   if (R > 256) return fail(PIPNN_EUNSUPPORTED, "R > 256");
   const bool u8 = X->dtype == PIPNN_U8, mips = X->metric == PIPNN_MIPS;
   PIPNN_CUDA(cudaMemsetAsync(deg + n, 0, sizeof(uint32_t), c.st));
-  PIPNN_CUDA(cudaMemsetAsync(defer_n, 0, 4 * sizeof(uint32_t), c.st));
+  PIPNN_CUDA(cudaMemsetAsync(defer_n, 0, 5 * sizeof(uint32_t), c.st));
   const size_t pair_bytes = (size_t)kFpStage * (kFpStage - 1) * 2;  // u16 (i, j) pairs of the generic kernel
   int cap1 = l_max;
   FpLayout L1 = fp_layout(X->d, u8, l_max, cap1);
@@ -990,6 +1554,8 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
     const uint32_t* in_list = order;  // nullptr: points in id order
     const uint32_t* in_n = order_n;
     bool first_tier = true;
+    static const bool band = std::getenv("PIPNN_FP_COOP") == nullptr;  // experiment hook: old cooperative tiers
+    static const bool gram32 = std::getenv("PIPNN_FP_GRAM32") != nullptr;  // experiment hook: old warp tier
 #define GP_TIER(U, M, CPV, T)                                                                                      \
   do {                                                                                                             \
     const GpLayout GL = gp_layout(X->d, U, CPV);                                                                   \
@@ -1021,12 +1587,44 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
     in_list = defer + (T) * n;                                                                                     \
     in_n = defer_n + (T);                                                                                          \
   } while (0)
+#define GP_BAND(U, M, CPV, T)                                                                                      \
+  do {                                                                                                             \
+    const BandLayout BL = band_layout(X->d, U, CPV);                                                               \
+    const int sm = (int)BL.bytes;                                                                                  \
+    auto* fn = fp_band_kernel<U, M, CPV>;                                                                          \
+    PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));                         \
+    const int per_sm = std::max(1, std::min(2048 / (2 * CPV + 32), (int)((227 * 1024) / (sm + 1024))));            \
+    fn<<<(unsigned)(num_sms() * per_sm), 2 * CPV + 32, sm, c.st>>>(Xg->data, n, X->d, Xg->ld, l_max, slots, count, R, \
+                                                              p->alpha_num, p->alpha_den, nbr_tmp, deg, in_list,    \
+                                                              in_n, defer + (T) * n, defer_n + (T), src_bf16);      \
+    PIPNN_LAUNCHED("fp_band_kernel", c.st);                                                                        \
+    in_list = defer + (T) * n;                                                                                     \
+    in_n = defer_n + (T);                                                                                          \
+  } while (0)
+#define GP_WARP(U, M)                                                                                              \
+  do {                                                                                                             \
+    const WarpLayout WL = warp_layout(X->d, U);                                                                    \
+    int w = (int)std::min<size_t>(8, (200 * 1024) / WL.per_warp);                                                  \
+    if (w < 1) return fail(PIPNN_EUNSUPPORTED, "final prune: row too large for the warp tile");                   \
+    const int sm = (int)(w * WL.per_warp);                                                                         \
+    auto* fn = fp_warp_kernel<U, M>;                                                                               \
+    PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));                         \
+    const int64_t blocks = std::min<int64_t>(ceil_div(n, w), num_sms() * 32);                                      \
+    first_tier = false;                                                                                            \
+    fn<<<(unsigned)blocks, 32 * w, sm, c.st>>>(Xg->data, n, X->d, Xg->ld, l_max, slots, count, R, p->alpha_num,    \
+                                               p->alpha_den, nbr_tmp, deg, in_list, in_n, defer, defer_n,          \
+                                               src_bf16);                                                          \
+    PIPNN_LAUNCHED("fp_warp_kernel", c.st);                                                                        \
+    in_list = defer;                                                                                               \
+    in_n = defer_n;                                                                                                \
+  } while (0)
 #define GP_ALL(U, M)                                                                                               \
   do {                                                                                                             \
-    GP_TIER(U, M, 32, 0);                                                                                          \
-    if (l_max > 31) GP_COOP(U, M, 64, 1);                                                                          \
-    if (l_max > 63) GP_COOP(U, M, 128, 2);                                                                         \
-    if (l_max > 127) {                                                                                             \
+    if (gram32 || (U)) GP_TIER(U, M, 32, 0); else GP_WARP(U, M);                                                   \
+    if (l_max > 31) { if (band && !(U)) GP_BAND(U, M, 64, 1); else GP_COOP(U, M, 64, 1); }                         \
+    if (l_max > 63) { if (band) GP_BAND(U, M, 128, 2); else GP_COOP(U, M, 128, 2); }                               \
+    if (l_max > 127 && band && band_layout(X->d, U, 192).bytes <= 200 * 1024) GP_BAND(U, M, 192, 3);             \
+    if (l_max > (band && band_layout(X->d, U, 192).bytes <= 200 * 1024 ? 191 : 127)) {                            \
       auto* fn = final_prune_kernel<U, M>;                                                                         \
       PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));                    \
       fn<<<(unsigned)(num_sms() * 2), 32, smem1, c.st>>>(X->data, n, X->d, X->ld, l_max, slots, count, R,          \
@@ -1038,8 +1636,21 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
     if (u8) GP_ALL(true, false);
     else if (mips) GP_ALL(false, true);
     else GP_ALL(false, false);
+    static const bool dbg_timing = [] {
+      const char* e = std::getenv("PIPNN_DEBUG_TIMING");
+      return e && e[0] == '1';
+    }();
+    if (dbg_timing) {  // tier sizes (points with <= 31 / <= 63 / <= 127 / more candidates)
+      uint32_t hd[4] = {0, 0, 0, 0};
+      PIPNN_CUDA(cudaMemcpyAsync(hd, defer_n, sizeof(hd), cudaMemcpyDeviceToHost, c.st));
+      PIPNN_CUDA(cudaStreamSynchronize(c.st));
+      std::fprintf(stderr, "[pipnn] final prune tiers: <=31 %lld, <=63 %u, <=127 %u, >127 %u\n",
+                   (long long)(n - hd[0]), hd[0] - hd[1], hd[1] - hd[2], hd[2]);
+    }
 #undef GP_ALL
 #undef GP_COOP
+#undef GP_BAND
+#undef GP_WARP
 #undef GP_TIER
   } else {
     // final_prune = 0: the R nearest reservoir entries, generic kernel
