@@ -12,6 +12,9 @@
 // Segments longer than the warp's SMEM capacity are merged in chunks (exact by the same lemma).
 #include <cub/cub.cuh>
 
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 #include "internal.h"
 
 namespace pipnn {
@@ -686,6 +689,31 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
                                                                               rev_start, rev_cnt, slots, count, defer,
                                                                               defer_n);
   PIPNN_LAUNCHED("hp_merge_inst_generic_kernel", c.st);
+  static const bool dbg_timing = [] {
+    const char* e = std::getenv("PIPNN_DEBUG_TIMING");
+    return e && e[0] == '1';
+  }();
+  if (dbg_timing) {
+    uint32_t hd = 0;
+    PIPNN_CUDA(cudaMemcpyAsync(&hd, defer_n, sizeof(hd), cudaMemcpyDeviceToHost, c.st));
+    PIPNN_CUDA(cudaStreamSynchronize(c.st));
+    std::vector<uint32_t> dl(hd);
+    std::vector<uint64_t> st(n + 1);
+    if (hd) PIPNN_CUDA(cudaMemcpy(dl.data(), defer, hd * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    PIPNN_CUDA(cudaMemcpy(st.data(), g.start, (n + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> rc(n_inst), ivv(n_inst);
+    PIPNN_CUDA(cudaMemcpy(rc.data(), rev_cnt, n_inst * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    PIPNN_CUDA(cudaMemcpy(ivv.data(), inv, n_inst * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    int64_t tsum = 0, tmax = 0;
+    for (uint32_t u : dl) {
+      int64_t T = 0;
+      for (uint64_t j = st[u]; j < st[u + 1]; ++j) T += k + rc[ivv[j]];
+      tsum += T;
+      tmax = std::max(tmax, T);
+    }
+    std::fprintf(stderr, "[pipnn] hashprune: %u owners deferred to the generic merge, keys mean %.0f max %lld\n", hd,
+                 hd ? (double)tsum / hd : 0.0, (long long)tmax);
+  }
   return PIPNN_OK;
 }
 

@@ -13,129 +13,104 @@ int tiled_row_bytes(const pipnn_points* X) {
 }
 
 // ------------------------------------------------------------------ gather
-// One CTA per (segment, 128-row block). Phase 1: 16-B vector loads of the source rows (a lane group per row)
-// into a row-major SMEM staging tile (fp32 -> bf16 RNE for float data) + the row's squared norm. Phase 2: the
-// tile is written block-major as [K/16][128][16 B] planes: the whole 128-row block is contiguous.
+// One CTA of 4 warps per (segment, 128-row block); lane = row (warp w: rows 32w..32w+31 of the block). Each
+// lane walks its row in 16-B chunks (fp32 -> bf16 RNE for float data; consecutive chunks of a row share L1
+// sectors) and stores chunk kc of its row at plane kc of the block-major layout [K/16][128][16 B]: a warp's
+// stores of one plane are 512 contiguous bytes. The row's squared norm accumulates in the lane (int32 exact
+// for uint8, fp32 of the bf16 values for float). No shared memory, no block barrier.
 // Float rows end with the 16-element augment K-step of dist_topk.cuh: (t_hi, t_mid, t_lo, 0...) with
 // t = -||y||^2/2 (L2) or 0 (MIPS), split over three bf16 values; padding rows get t = -1e30 (u8 padding
 // rows get the norm kPadNormU8 instead), so padded columns never enter a top-k.
 template <int SRC>  // 0: uint8, 1: float32, 2: bf16 (kDtypeBf16)
-__global__ void __launch_bounds__(256) gather_tiled_kernel(const void* __restrict__ Xv, int64_t ld, int d, int Kb,
+__global__ void __launch_bounds__(128) gather_tiled_kernel(const void* __restrict__ Xv, int64_t ld, int d, int Kb,
                                                            int mips, const uint32_t* __restrict__ ids,
                                                            const TileSeg* __restrict__ segs,
                                                            const WorkItem* __restrict__ items,
                                                            const int64_t* __restrict__ n_items, uint8_t* __restrict__ T,
                                                            void* __restrict__ nrm, int* err) {
   constexpr bool U8 = SRC == 0;
-  extern __shared__ __align__(16) uint8_t st[];
   if ((int64_t)blockIdx.x >= *n_items) return;
   const WorkItem w = items[blockIdx.x];
   const TileSeg S = segs[w.seg];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pitch = Kb + 16;  // staging row pitch (bank-conflict-free 16-B column reads)
-  const int r0 = w.rb * 128;
-  const int ldm = U8 ? Kb : (Kb - 32) / 2;  // elements of the coordinate part
-  // Phase 1: a group of L = Kb/16 (uint8) or ldm/8 (float) lanes per row, one 16-B destination chunk per
-  // lane (16 bytes, or 8 floats -> 8 bf16), loaded with 16-B vector loads when the row is aligned; the
-  // row's squared norm by a shuffle reduction inside the lane group (int32 exact / fp32 of the bf16 values).
-  const int cpr = U8 ? (Kb >> 4) : (ldm >> 3);  // 16-B destination chunks per row (<= 32)
-  int L = 1;
-  while (L < cpr) L <<= 1;  // lanes per row (power of two, <= 32)
-  const int rpw = 32 / L;   // rows per warp step
-  const int sub = lane / L, ch = lane % L;
+  const int r = threadIdx.x;  // row within the 128-row block
+  const int local = w.rb * 128 + r;
+  const bool valid = local < S.rows;
+  const int KC = Kb >> 4;
+  const int ldm = U8 ? Kb : (Kb - 32) / 2;      // elements of the coordinate part (float: bf16 elements)
+  const int ncc = U8 ? KC : (ldm >> 3);          // 16-B chunks holding coordinates
+  uint8_t* dst = T + (S.pos / 128 + w.rb) * (int64_t)KC * 2048 + r * 16;
+  const int64_t id = valid ? (ids ? (int64_t)ids[S.id_off + local] : (S.id_off + local)) : 0;
+  int32_t ni = 0;
+  float nf = 0.0f;
+  bool bad = false;
   const bool vec = U8 ? ((d & 15) == 0 && (ld & 15) == 0) : ((d & 3) == 0 && (ld & 3) == 0);
-  for (int rbase = warp * rpw; rbase < 128; rbase += 8 * rpw) {
-    const int r = rbase + sub;
-    const int local = r0 + r;
-    uint8_t* srow = st + r * pitch;
-    const bool valid = local < S.rows;
-    int ni = 0;
-    float nf = 0.0f;
-    if (ch < cpr) {
-      uint4 out = make_uint4(0u, 0u, 0u, 0u);
-      if (valid) {
-        const int64_t id = ids ? (int64_t)ids[S.id_off + local] : (S.id_off + local);
-        if (U8) {
-          const uint8_t* src = (const uint8_t*)Xv + id * ld;
-          if (vec) {
-            if (ch * 16 < d) out = __ldg((const uint4*)src + ch);
-          } else {
-            uint32_t wv[4] = {0u, 0u, 0u, 0u};
-            for (int t = 0; t < 16; ++t)
-              if (ch * 16 + t < d) wv[t >> 2] |= (uint32_t)src[ch * 16 + t] << (8 * (t & 3));
-            out = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-          }
-          ni = __dp4a(out.x, out.x, 0u);
-          ni = __dp4a(out.y, out.y, (uint32_t)ni);
-          ni = __dp4a(out.z, out.z, (uint32_t)ni);
-          ni = __dp4a(out.w, out.w, (uint32_t)ni);
-        } else if (SRC == 2) {
-          // bf16 rows zero padded to ld (a multiple of 8): 16-B chunks, norm of the bf16 values
-          if (ch * 8 < ld) out = __ldg((const uint4*)((const uint16_t*)Xv + id * ld) + ch);
-          const uint32_t wv[4] = {out.x, out.y, out.z, out.w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float xl = __uint_as_float(wv[t] << 16), xh = __uint_as_float(wv[t] & 0xFFFF0000u);
-            nf = fmaf(xl, xl, nf);
-            nf = fmaf(xh, xh, nf);
-          }
+#pragma unroll 4
+  for (int kc = 0; kc < ncc; ++kc) {
+    uint4 out = make_uint4(0u, 0u, 0u, 0u);
+    if (valid) {
+      if (U8) {
+        const uint8_t* src = (const uint8_t*)Xv + id * ld;
+        if (vec) {
+          if (kc * 16 < d) out = __ldg((const uint4*)src + kc);
         } else {
-          const float* src = (const float*)Xv + id * ld;
-          float f[8];
-          if (vec && ch * 8 + 8 <= d) {
-            const float4 a = __ldg((const float4*)(src + ch * 8));
-            const float4 b = __ldg((const float4*)(src + ch * 8 + 4));
-            f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
-          } else {
-#pragma unroll
-            for (int t = 0; t < 8; ++t) f[t] = ch * 8 + t < d ? __ldg(src + ch * 8 + t) : 0.0f;
-          }
-          bool bad = false;
-          uint32_t wv[4];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const uint16_t lo = f32_to_bf16_rne(f[2 * t]), hi = f32_to_bf16_rne(f[2 * t + 1]);
-            bad |= !isfinite(f[2 * t]) || !isfinite(f[2 * t + 1]);
-            const float xl = __uint_as_float((uint32_t)lo << 16), xh = __uint_as_float((uint32_t)hi << 16);
-            nf = fmaf(xl, xl, nf);
-            nf = fmaf(xh, xh, nf);
-            wv[t] = (uint32_t)lo | ((uint32_t)hi << 16);
-          }
-          if (bad) atomicExch(err, DERR_NONFINITE);
+          uint32_t wv[4] = {0u, 0u, 0u, 0u};
+          for (int t = 0; t < 16; ++t)
+            if (kc * 16 + t < d) wv[t >> 2] |= (uint32_t)src[kc * 16 + t] << (8 * (t & 3));
           out = make_uint4(wv[0], wv[1], wv[2], wv[3]);
         }
-      }
-      *(uint4*)(srow + ch * 16) = out;
-    }
-    for (int o = L >> 1; o > 0; o >>= 1) {
-      ni += __shfl_xor_sync(0xffffffffu, ni, o);
-      nf += __shfl_xor_sync(0xffffffffu, nf, o);
-    }
-    if (ch == 0) {
-      if (U8) {
-        ((int32_t*)nrm)[S.pos + local] = valid ? ni : kPadNormU8;
+        ni = (int32_t)__dp4a(out.x, out.x, (uint32_t)ni);
+        ni = (int32_t)__dp4a(out.y, out.y, (uint32_t)ni);
+        ni = (int32_t)__dp4a(out.z, out.z, (uint32_t)ni);
+        ni = (int32_t)__dp4a(out.w, out.w, (uint32_t)ni);
+      } else if (SRC == 2) {
+        // bf16 rows zero padded to ld (a multiple of 8): 16-B chunks, norm of the bf16 values
+        if (kc * 8 < ld) out = __ldg((const uint4*)((const uint16_t*)Xv + id * ld) + kc);
+        const uint32_t wv[4] = {out.x, out.y, out.z, out.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float xl = __uint_as_float(wv[t] << 16), xh = __uint_as_float(wv[t] & 0xFFFF0000u);
+          nf = fmaf(xl, xl, nf);
+          nf = fmaf(xh, xh, nf);
+        }
       } else {
-        ((float*)nrm)[S.pos + local] = nf;
-        const float t = valid ? (mips ? 0.0f : -0.5f * nf) : -kPadKey;
-        const uint16_t hi = f32_to_bf16_rne(t);
-        const float r1 = t - __uint_as_float((uint32_t)hi << 16);
-        const uint16_t mid = f32_to_bf16_rne(r1);
-        const float r2 = r1 - __uint_as_float((uint32_t)mid << 16);
-        const uint16_t lo = f32_to_bf16_rne(r2);
-        uint32_t* aug = (uint32_t*)(srow + 2 * ldm);
-        aug[0] = (uint32_t)hi | ((uint32_t)mid << 16);
-        aug[1] = (uint32_t)lo;
-        aug[2] = aug[3] = aug[4] = aug[5] = aug[6] = aug[7] = 0u;
+        const float* src = (const float*)Xv + id * ld;
+        float f[8];
+        if (vec && kc * 8 + 8 <= d) {
+          const float4 a = __ldg((const float4*)(src + kc * 8));
+          const float4 b = __ldg((const float4*)(src + kc * 8 + 4));
+          f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) f[t] = kc * 8 + t < d ? __ldg(src + kc * 8 + t) : 0.0f;
+        }
+        uint32_t wv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const uint16_t lo = f32_to_bf16_rne(f[2 * t]), hi = f32_to_bf16_rne(f[2 * t + 1]);
+          bad |= !isfinite(f[2 * t]) || !isfinite(f[2 * t + 1]);
+          const float xl = __uint_as_float((uint32_t)lo << 16), xh = __uint_as_float((uint32_t)hi << 16);
+          nf = fmaf(xl, xl, nf);
+          nf = fmaf(xh, xh, nf);
+          wv[t] = (uint32_t)lo | ((uint32_t)hi << 16);
+        }
+        out = make_uint4(wv[0], wv[1], wv[2], wv[3]);
       }
     }
+    *(uint4*)(dst + (int64_t)kc * 2048) = out;
   }
-  __syncthreads();
-  const int KC = Kb >> 4;
-  uint8_t* dst = T + (S.pos / 128 + w.rb) * (int64_t)KC * 2048;  // block-major: the block is contiguous
-  for (int p = threadIdx.x; p < 128 * KC; p += 256) {
-    const int kc = p >> 7, r = p & 127;
-    const uint4 v = *(const uint4*)(st + r * pitch + kc * 16);
-    *(uint4*)(dst + (int64_t)kc * 2048 + r * 16) = v;
+  if (bad) atomicExch(err, DERR_NONFINITE);
+  if (U8) {
+    ((int32_t*)nrm)[S.pos + local] = valid ? ni : kPadNormU8;
+  } else {
+    ((float*)nrm)[S.pos + local] = nf;
+    const float t = valid ? (mips ? 0.0f : -0.5f * nf) : -kPadKey;
+    const uint16_t hi = f32_to_bf16_rne(t);
+    const float r1 = t - __uint_as_float((uint32_t)hi << 16);
+    const uint16_t mid = f32_to_bf16_rne(r1);
+    const float r2 = r1 - __uint_as_float((uint32_t)mid << 16);
+    const uint16_t lo = f32_to_bf16_rne(r2);
+    *(uint4*)(dst + (int64_t)ncc * 2048) = make_uint4((uint32_t)hi | ((uint32_t)mid << 16), (uint32_t)lo, 0u, 0u);
+    *(uint4*)(dst + (int64_t)(ncc + 1) * 2048) = make_uint4(0u, 0u, 0u, 0u);
   }
 }
 
@@ -143,14 +118,10 @@ pipnn_status gather_tiled(const pipnn_points* X, const uint32_t* ids, const Tile
                           const int64_t* n_items, int64_t max_items, uint8_t* T, void* nrm, const Ctx& c, int Kb) {
   if (max_items <= 0) return PIPNN_OK;
   if (Kb <= 0) Kb = tiled_row_bytes(X);
-  const int smem = 128 * (Kb + 16);
   const int64_t ld = X->ld;
 #define GT_LAUNCH(SRC)                                                                                             \
-  do {                                                                                                             \
-    PIPNN_CUDA(cudaFuncSetAttribute(gather_tiled_kernel<SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));  \
-    gather_tiled_kernel<SRC><<<(unsigned)max_items, 256, smem, c.st>>>(X->data, ld, X->d, Kb, X->metric == PIPNN_MIPS, \
-                                                                        ids, segs, items, n_items, T, nrm, c.err);  \
-  } while (0)
+  gather_tiled_kernel<SRC><<<(unsigned)max_items, 128, 0, c.st>>>(X->data, ld, X->d, Kb, X->metric == PIPNN_MIPS,   \
+                                                                  ids, segs, items, n_items, T, nrm, c.err)
   if (X->dtype == PIPNN_U8) GT_LAUNCH(0);
   else if (X->dtype == kDtypeBf16) GT_LAUNCH(2);
   else GT_LAUNCH(1);
