@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
     // insertion is strict, so equal keys keep the smaller column (= smaller id).
     [&]() {
       const int ew = warp - 4;             // 0..7
-      const int wg = ew >> 2;              // warpgroup
+      const int wg = ew >> 2;              // warpgroup = pipeline
       const int q = warp & 3;              // TMEM lane quadrant of this warp (hardware: warp id % 4)
       const int tid = q * 32 + lane;       // row within the 128-row block = TMEM lane
       const KT kInf = U8 ? (KT)0x7FFFFFFF : (KT)__int_as_float(0x7F800000);
@@ -450,23 +450,26 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
               if (key < kk[KMAX - 1]) topk_insert<KT, KMAX>(kk, ii, key, (uint32_t)(c0 + jj));
             }
           } else if (!pass2) {
-            // ---- pass 1: group minima of 16 keys, inserted into the value list; 64 columns per TMEM load
-            // (one load wait per 64 columns; the tile's column count is a multiple of 32, padding columns of a
-            // 64-column load beyond Nt hold another tile's stale values and are masked to +inf)
-            for (int j0 = 0; j0 < Nt; j0 += 64) {
+            // ---- pass 1: group minima of 16 keys, inserted into the value list; uint8: 32 columns per TMEM
+            // load (with the 32 column norms in 8 int4 registers), float: 64 (one load wait per 64 columns; the
+            // tile's column count is a multiple of 32, the upper half of a 64-column load beyond Nt holds stale
+            // values and is masked to +inf)
+            constexpr int P1W = U8 ? 32 : 64;
+            for (int j0 = 0; j0 < Nt; j0 += P1W) {
               const int col0 = c0 + j0;
-              const bool two = j0 + 32 < Nt;
-              int4 nb4[16];
+              const int nw = min(P1W, Nt - j0);  // 32 or 64 (Nt is a multiple of 32)
+              int4 nb4[8];
               if (U8) {
                 const int4* p4 = reinterpret_cast<const int4*>((const int32_t*)args.nb + S.b.pos + col0);
 #pragma unroll
-                for (int u = 0; u < 16; ++u) nb4[u] = (u < 8 || two) ? __ldg(p4 + u) : make_int4(0, 0, 0, 0);
+                for (int u = 0; u < 8; ++u) nb4[u] = __ldg(p4 + u);
               }
-              uint32_t v[64];
-              ptx::tmem_ld64(taddr + j0, v);
+              uint32_t v[P1W];
+              if (P1W == 32) ptx::tmem_ld32(taddr + j0, *reinterpret_cast<uint32_t(*)[32]>(v));
+              else ptx::tmem_ld64(taddr + j0, *reinterpret_cast<uint32_t(*)[64]>(v));
               ptx::tmem_ld_wait();
 #pragma unroll
-              for (int gq = 0; gq < 4; ++gq) {
+              for (int gq = 0; gq < P1W / 16; ++gq) {
                 KT k16[16];
 #pragma unroll
                 for (int jj = 0; jj < 16; ++jj) {
@@ -490,7 +493,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
                   gm = fminf(gm, fminf(fminf(fminf(k16[8], k16[9]), fminf(k16[10], k16[11])),
                                        fminf(fminf(k16[12], k16[13]), fminf(k16[14], k16[15]))));
                 }
-                if (gq >= 2 && !two) gm = kInf;
+                if (16 * gq >= nw) gm = kInf;  // (float: the upper 32 columns of a 64-column load beyond Nt)
 #pragma unroll
                 for (int t = VK - 1; t > 0; --t) {
                   if (U8) vk[t] = max(vk[t - 1], min(vk[t], gm));
@@ -518,23 +521,20 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
             // float: the sign of a difference is exact. The mask is built with one funnel shift per element.
             const KT thr = kk[KMAX - 1] != kInf ? kk[KMAX - 1] : U;
             const KT thr_eff = U8 ? (thr == kInf ? (KT)0x40000000 : thr) : thr;
-            KT tk[32];
+            // uint8: v becomes t = key - thr in place (the staged value); float: v keeps the key bits
             uint32_t mask = 0;
             if (U8) {
 #pragma unroll
               for (int u = 0; u < 8; ++u) {
-                tk[4 * u + 0] = (nb4[u].x - thr_eff) - 2 * (int32_t)v[4 * u + 0];
-                tk[4 * u + 1] = (nb4[u].y - thr_eff) - 2 * (int32_t)v[4 * u + 1];
-                tk[4 * u + 2] = (nb4[u].z - thr_eff) - 2 * (int32_t)v[4 * u + 2];
-                tk[4 * u + 3] = (nb4[u].w - thr_eff) - 2 * (int32_t)v[4 * u + 3];
+                v[4 * u + 0] = (uint32_t)((nb4[u].x - thr_eff) - 2 * (int32_t)v[4 * u + 0]);
+                v[4 * u + 1] = (uint32_t)((nb4[u].y - thr_eff) - 2 * (int32_t)v[4 * u + 1]);
+                v[4 * u + 2] = (uint32_t)((nb4[u].z - thr_eff) - 2 * (int32_t)v[4 * u + 2]);
+                v[4 * u + 3] = (uint32_t)((nb4[u].w - thr_eff) - 2 * (int32_t)v[4 * u + 3]);
               }
-            } else {
-#pragma unroll
-              for (int jj = 0; jj < 32; ++jj) tk[jj] = __uint_as_float(v[jj]) - thr_eff;
             }
 #pragma unroll
             for (int jj = 31; jj >= 0; --jj) {
-              const uint32_t bits = U8 ? (uint32_t)tk[jj] : __float_as_uint((float)tk[jj]);
+              const uint32_t bits = U8 ? v[jj] : __float_as_uint(__uint_as_float(v[jj]) - (float)thr_eff);
               mask = __funnelshift_l(bits, mask, 1);  // (mask << 1) | sign(t_j)
             }
             if (col0 == diag_chunk) mask &= ~(1u << lane);  // self exclusion (by id: the diagonal element)
@@ -543,11 +543,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
               if (__any_sync(0xffffffffu, qlen + __popc(mask) > kQCap)) topk_drain<KT, KMAX>(kk, ii, qlen, my_qk, my_qc);
 #pragma unroll
               for (int u = 0; u < 8; ++u) {
-                uint4 w4;
-                if (U8) w4 = make_uint4((uint32_t)tk[4 * u], (uint32_t)tk[4 * u + 1], (uint32_t)tk[4 * u + 2],
-                                        (uint32_t)tk[4 * u + 3]);
-                else w4 = make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);  // float: the keys
-                *reinterpret_cast<uint4*>(stg + 4 * u) = w4;
+                *reinterpret_cast<uint4*>(stg + 4 * u) = make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
               }
               __syncwarp();
               while (mask) {
