@@ -532,11 +532,18 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
                 v[4 * u + 3] = (uint32_t)((nb4[u].w - thr_eff) - 2 * (int32_t)v[4 * u + 3]);
               }
             }
+            // four independent funnel-shift chains of 8 bits each (a single 32-long chain is latency-bound)
+            uint32_t m8[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-            for (int jj = 31; jj >= 0; --jj) {
-              const uint32_t bits = U8 ? v[jj] : __float_as_uint(__uint_as_float(v[jj]) - (float)thr_eff);
-              mask = __funnelshift_l(bits, mask, 1);  // (mask << 1) | sign(t_j)
+            for (int jj = 7; jj >= 0; --jj) {
+#pragma unroll
+              for (int qd = 0; qd < 4; ++qd) {
+                const int j = 8 * qd + jj;
+                const uint32_t bits = U8 ? v[j] : __float_as_uint(__uint_as_float(v[j]) - (float)thr_eff);
+                m8[qd] = __funnelshift_l(bits, m8[qd], 1);  // (m << 1) | sign(t_j)
+              }
             }
+            mask = m8[0] | (m8[1] << 8) | (m8[2] << 16) | (m8[3] << 24);
             if (col0 == diag_chunk) mask &= ~(1u << lane);  // self exclusion (by id: the diagonal element)
             if (__any_sync(0xffffffffu, mask != 0)) {
               // room for this chunk's passes (a drain empties the queue; a chunk can still exceed kQCap)
@@ -555,6 +562,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
                                        : (KT)reinterpret_cast<const float*>(stg)[jj];
                 my_qc[qlen * 128] = (uint16_t)(col0 + jj);
                 ++qlen;
+                if (prof) ++pw[2];
               }
               __syncwarp();
             }
@@ -565,6 +573,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
           if (lane == 0) ptx::mbar_arrive(&bar_acc_empty[buf]);
         }
         const unsigned long long t_out = prof ? clock64() : 0ull;
+        if (prof) ++pw[3];  // items (rows) of this thread
         topk_drain<KT, KMAX>(kk, ii, qlen, my_qk, my_qc);
         if (row < S.a.rows) {
           const int64_t obase = S.out_off + (int64_t)row * S.ostride;
@@ -602,6 +611,8 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
       }
       if (prof && tid == 0) {
         atomicAdd(&g_dt_prof[11], pw[9]);
+        atomicAdd(&g_dt_prof[15], pw[2]);  // pass-2 candidates appended (this thread's rows)
+        atomicAdd(&g_dt_prof[3], pw[3]);  // rows sampled
         atomicAdd(&g_dt_prof[8], pw[8]);
         atomicAdd(&g_dt_prof[9], clock64() - t_start);
         atomicAdd(&g_dt_prof[10], (unsigned long long)tcount);

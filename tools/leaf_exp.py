@@ -29,7 +29,7 @@ for dbg in (sys.argv[1:] or ["0", "1", "2", "0"]):
         buf = (ctypes.c_ulonglong * 16)()
         P._lib.pipnn_debug_dt_prof(buf)
         v = [b / 5 / 148 for b in buf]  # per launch, per SM (producer/MMA: one lane each of 2 pipelines)
-        print("  mma: tile issue (excl. ring waits) %.0f, of which MMA+commit blocks %.0f, item head %.0f" % (v[12], v[14], v[13]))
+        print("  mma: tile issue (excl. ring waits) %.0f, item head %.0f | epi: pass-2 appends per row %.2f" % (v[12], v[13], buf[15] / max(1, buf[3])))
         print("  prod: wait A %.0f, wait ring-empty %.0f, total %.0f | mma: wait A %.0f, wait acc-empty %.0f, "
               "wait ring-full %.0f, total %.0f | epi: wait acc-full %.0f, output %.0f, total %.0f, tiles %.0f (cycles/SM/launch)"
               % (v[0], v[1], v[2], v[4], v[5], v[6], v[7], v[8], v[11], v[9], v[10]))
