@@ -102,6 +102,25 @@ def dist_env():
     return ws, rank, local
 
 
+def rank_max(x: float, ws: int, device=None) -> float:
+    """Max of a per-rank scalar over all ranks (torch.distributed all_reduce MAX; the identity at ws == 1)."""
+    if ws <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(ms_local: float, n_per_rank: int, ws: int, device=None):
+    """Whole-job value of a weak-scaling step: every rank builds n_per_rank points; the job's step time is the
+    slowest rank's (max over ranks), so value = n_per_rank * ws / max_ms."""
+    ms_max = rank_max(ms_local, ws, device)
+    return ms_max, n_per_rank * ws / (ms_max / 1e3)
+
+
 def run_reference(args, cfg):
     """Reference arm: the CPU oracle, as it stands, on a bounded sample of the workload (rank 0 only)."""
     ws, rank, _ = dist_env()
@@ -236,11 +255,7 @@ def main():
         dist.barrier()
     launches = P.pipnn_launch_count() - launches0
     ms = sum(step_ms) / len(step_ms)
-    ms_t = torch.tensor([ms], device=dev)
-    if ws > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    value = cfg.n * ws / (ms_max / 1e3)
+    ms_max, value = job_throughput(ms, cfg.n, ws, dev)
 
     # ---------------- end-to-end through the public API with host buffers (pinned), copies inside
     n_rp = cfg.n + 1
@@ -261,10 +276,7 @@ def main():
         torch.cuda.synchronize()
         e2e_ms.append(e0.elapsed_time(e1))
         d2h = n_rp * 8 + o.n_edges * 4
-    e2e_t = torch.tensor([sum(e2e_ms) / len(e2e_ms)], device=dev)
-    if ws > 1:
-        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_val = cfg.n * ws / (float(e2e_t.item()) / 1e3)
+    _, e2e_val = job_throughput(sum(e2e_ms) / len(e2e_ms), cfg.n, ws, dev)
 
     if rank == 0:
         peaks, src = measured_peaks()
