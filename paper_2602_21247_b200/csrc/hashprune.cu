@@ -565,6 +565,128 @@ __global__ void __launch_bounds__(256) hp_merge_inst_kernel(int64_t n, int l_max
   }
 }
 
+// Block (256 threads) sum and exclusive scan of one int per thread; s8 = 8 ints of SMEM.
+__device__ __forceinline__ int block256_sum(int x, int* s8) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if (lane == 0) s8[w] = x;
+  __syncthreads();
+  int t = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) t += s8[i];
+  __syncthreads();
+  return t;
+}
+__device__ __forceinline__ int block256_excl(int x, int* s8) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s8[w] = inc;
+  __syncthreads();
+  int off = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) off += i < w ? s8[i] : 0;
+  __syncthreads();
+  return off + inc - x;
+}
+
+// Table merge for the deferred owners (hubs, evictions; m <= 12): one CTA per owner, a 2^m-entry SMEM table
+// indexed by the hash. Every key (reservoir + new) goes in with a 64-bit atomicMin on its bucket — the bucket
+// minimum of Alg. 3's collision rule, in any order. The occupied buckets, read back in table order, are
+// sorted by hash; when more than l_max survive, the l_max-th smallest 48-bit (dist16 | id32) value is found by
+// an MSB-first bisection with block-wide counts (values are distinct: one bucket per id) and only the entries
+// at or below it are kept (the eviction rule's end state).
+__global__ void __launch_bounds__(256) hp_merge_table_kernel(int m, int l_max, int k, const uint64_t* __restrict__ inv_start,
+                                                             const uint32_t* __restrict__ inv,
+                                                             const uint64_t* __restrict__ fwd,
+                                                             const uint64_t* __restrict__ rev,
+                                                             const uint32_t* __restrict__ rev_start,
+                                                             const uint32_t* __restrict__ rev_cnt,
+                                                             uint64_t* __restrict__ slots, uint32_t* __restrict__ count,
+                                                             const uint32_t* __restrict__ list,
+                                                             const uint32_t* __restrict__ list_n) {
+  extern __shared__ uint64_t tbl[];  // [2^m]
+  __shared__ int s8[8];
+  __shared__ uint32_t s_hist[256];
+  __shared__ uint32_t s_sel;
+  const int NB = 1 << m, tid = threadIdx.x;
+  const int per = (NB + 255) / 256;  // table entries per thread (<= 16; contiguous chunk: keeps the hash order)
+  const int64_t nl = *list_n;
+  constexpr uint64_t kLow48 = 0xFFFFFFFFFFFFull;
+  for (int64_t it = blockIdx.x; it < nl; it += gridDim.x) {
+    const int64_t u = list[it];
+    uint64_t* res = slots + u * (int64_t)l_max;
+    const int c = (int)count[u];
+    __syncthreads();  // the previous owner's table is no longer read
+    for (int t = tid; t < NB; t += 256) tbl[t] = ~0ull;
+    __syncthreads();
+    for (int t = tid; t < c; t += 256) {
+      const uint64_t key = res[t];
+      atomicMin((unsigned long long*)&tbl[key >> 48], (unsigned long long)key);
+    }
+    const uint64_t i0 = inv_start[u], i1 = inv_start[u + 1];
+    for (uint64_t q = i0; q < i1; ++q) {
+      const uint32_t i = inv[q];
+      const int ni = k + (int)rev_cnt[i];
+      const uint64_t rs = rev_start[i];
+      for (int j = tid; j < ni; j += 256) {
+        const uint64_t key = j < k ? fwd[(int64_t)i * k + j] : rev[rs + (j - k)];
+        if (key != ~0ull) atomicMin((unsigned long long*)&tbl[key >> 48], (unsigned long long)key);
+      }
+    }
+    __syncthreads();
+    uint64_t v[16];
+    int cnt = 0;
+    const int b0 = tid * per;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      v[e] = (e < per && b0 + e < NB) ? tbl[b0 + e] : ~0ull;
+      cnt += v[e] != ~0ull ? 1 : 0;
+    }
+    const int total = block256_sum(cnt, s8);
+    uint64_t thr48 = kLow48;
+    if (total > l_max) {
+      // radix select, 8-bit digits MSB first: the bucket of the need-th smallest among the values that share
+      // the prefix decided so far (6 rounds of a 256-bin SMEM histogram + scan)
+      uint32_t* hist = s_hist;
+      uint64_t prefix = 0;
+      int need = l_max;
+      for (int sh = 40; sh >= 0; sh -= 8) {
+        hist[tid] = 0u;
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const uint64_t x = v[e] & kLow48;
+          if (v[e] != ~0ull && (sh == 40 || (x >> (sh + 8)) == (prefix >> (sh + 8))))
+            atomicAdd(&hist[(x >> sh) & 0xFF], 1u);
+        }
+        __syncthreads();
+        const int hb = (int)hist[tid];
+        const int below = block256_excl(hb, s8);  // values with this prefix and a smaller digit
+        if (below < need && need <= below + hb) s_sel = (uint32_t)((tid << 16) | (uint32_t)(need - below));
+        __syncthreads();
+        const uint32_t sel = s_sel;
+        prefix |= (uint64_t)(sel >> 16) << sh;
+        need = (int)(sel & 0xFFFFu);
+      }
+      thr48 = prefix;
+    }
+    int kc = 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) kc += (v[e] != ~0ull && (v[e] & kLow48) <= thr48) ? 1 : 0;
+    int o = block256_excl(kc, s8);
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      if (v[e] != ~0ull && (v[e] & kLow48) <= thr48) res[o++] = v[e];
+    if (tid == 255) count[u] = (uint32_t)o;
+  }
+}
+
 // Generic merge for the deferred owners: the chunked SMEM algorithm of hp_merge_kernel over OwnerKeys.
 __global__ void __launch_bounds__(128) hp_merge_inst_generic_kernel(int l_max, int cap, int k,
                                                                     const uint64_t* __restrict__ inv_start,
@@ -682,13 +804,21 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
   hp_merge_inst_kernel<<<(unsigned)blocks, 256, 0, c.st>>>(n, l_max, k, g.start, inv, fwd, rev, rev_start, rev_cnt,
                                                                slots, count, defer, defer_n);
   PIPNN_LAUNCHED("hp_merge_inst_kernel", c.st);
-  const int cap = merge_cap(l_max);
-  const int gsm = 4 * 2 * cap * (int)sizeof(uint64_t);
-  PIPNN_CUDA(cudaFuncSetAttribute(hp_merge_inst_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gsm));
-  hp_merge_inst_generic_kernel<<<(unsigned)(num_sms() * 4), 128, gsm, c.st>>>(l_max, cap, k, g.start, inv, fwd, rev,
-                                                                              rev_start, rev_cnt, slots, count, defer,
-                                                                              defer_n);
-  PIPNN_LAUNCHED("hp_merge_inst_generic_kernel", c.st);
+  if (m <= 12) {
+    const int tsm = (int)((size_t)8 << m);
+    PIPNN_CUDA(cudaFuncSetAttribute(hp_merge_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm));
+    hp_merge_table_kernel<<<(unsigned)(num_sms() * 6), 256, tsm, c.st>>>(m, l_max, k, g.start, inv, fwd, rev, rev_start,
+                                                                          rev_cnt, slots, count, defer, defer_n);
+    PIPNN_LAUNCHED("hp_merge_table_kernel", c.st);
+  } else {
+    const int cap = merge_cap(l_max);
+    const int gsm = 4 * 2 * cap * (int)sizeof(uint64_t);
+    PIPNN_CUDA(cudaFuncSetAttribute(hp_merge_inst_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, gsm));
+    hp_merge_inst_generic_kernel<<<(unsigned)(num_sms() * 4), 128, gsm, c.st>>>(l_max, cap, k, g.start, inv, fwd, rev,
+                                                                                rev_start, rev_cnt, slots, count, defer,
+                                                                                defer_n);
+    PIPNN_LAUNCHED("hp_merge_inst_generic_kernel", c.st);
+  }
   static const bool dbg_timing = [] {
     const char* e = std::getenv("PIPNN_DEBUG_TIMING");
     return e && e[0] == '1';
