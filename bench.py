@@ -167,29 +167,47 @@ def cpu_baseline(cfg, n_sample):
                       f"({dt:.1f} s)"}
 
 
-def recall_eval(X, cfg, rp, ci, n_queries):
-    """recall@10 of the GPU graph: exact ground truth by a fp32 torch GEMM (exact for uint8 data), CPU beam
-    search of the oracle's evaluation harness (Alg. 1) from the mean-nearest entry point."""
+def recall_eval(Xd, cfg, row_ptr, col_idx, n_queries):
+    """recall@10 of the GPU graph over the L sweep (evaluation harness, not the method): queries from the
+    config's generator, exact ground truth by a fp32 torch GEMM (exact for uint8 data), entry point = the point
+    nearest the dataset mean (R25), search by the library's batched beam search (pipnn_search,
+    Alg. 1); plus the search's throughput (queries/s, CUDA events) at each L."""
     import torch
 
-    import oracle as O
+    import paper_2602_21247_b200 as P
 
     Q = synth.gen_queries(cfg, n_queries=n_queries)
+    Qd = torch.from_numpy(Q).to(Xd.device)
     torch.backends.cuda.matmul.allow_tf32 = False
-    Xt = torch.from_numpy(X).cuda().float()
-    Qt = torch.from_numpy(Q).cuda().float()
+    Xf = Xd.float()
+    x2 = (Xf * Xf).sum(1)
+    truth = []
+    for s0 in range(0, len(Q), 1000):
+        Qf = Qd[s0:s0 + 1000].float()
+        if cfg.metric == "mips":
+            D = -(Qf @ Xf.T)
+        else:
+            D = (Qf * Qf).sum(1, keepdim=True) + x2[None] - 2 * (Qf @ Xf.T)
+        truth.append(torch.topk(D, 10, dim=1, largest=False).indices)
+    truth = torch.cat(truth)
+    Xe = Xd.double()
     if cfg.metric == "mips":
-        D = -(Qt @ Xt.T)
+        entry = int(torch.argmax(Xe @ Xe.mean(0)).item())
     else:
-        D = (Qt * Qt).sum(1, keepdim=True) + (Xt * Xt).sum(1)[None] - 2 * (Qt @ Xt.T)
-    truth = torch.topk(D, 10, dim=1, largest=False).indices.cpu().numpy().astype(np.uint32)
-    ds = O.Dataset(X, metric=cfg.metric, mode="exact")
-    e = O.entry_point(ds)
-    out = {}
+        entry = int(torch.argmin(((Xe - Xe.mean(0)) ** 2).sum(1)).item())
+    del Xf, Xe
+    recall, qps = {}, {}
     for L in (10, 32, 64, 128):
-        res, cmps = O.beam_search(ds, rp, ci, Q, e, L, 10)
-        out[str(L)] = round(float(O.recall_at(res, truth).mean()), 4)
-    return out
+        P.pipnn_search(Xd, row_ptr, col_idx, Qd[:100], entry, L, 10, cfg.metric)  # warm-up
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ids, _, _ = P.pipnn_search(Xd, row_ptr, col_idx, Qd, entry, L, 10, cfg.metric)
+        e1.record()
+        torch.cuda.synchronize()
+        qps[str(L)] = round(len(Q) / (e0.elapsed_time(e1) / 1e3))
+        hit = (ids.long().unsqueeze(2) == truth.unsqueeze(1)).any(2).sum(1).float() / 10.0
+        recall[str(L)] = round(float(hit.mean().item()), 4)
+    return recall, qps
 
 
 def main():
@@ -202,7 +220,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=100_000)
     ap.add_argument("--cpu-sample", type=int, default=200_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--recall-queries", type=int, default=1000)
+    ap.add_argument("--recall-queries", type=int, default=10000)
     args = ap.parse_args()
     cfg = synth.CONFIGS[args.config]
     if args.impl == "reference":
@@ -319,9 +337,9 @@ def main():
         }
         if args.recall_queries > 0:
             try:
-                rp = out.row_ptr.cpu().numpy()
-                ci = out.col_idx.cpu().numpy().view(np.uint32)
-                line["recall_at_10"] = recall_eval(X, cfg, rp, ci, args.recall_queries)
+                rec, qps = recall_eval(Xd, cfg, out.row_ptr, out.col_idx, args.recall_queries)
+                line["recall_at_10"] = rec
+                line["search_qps"] = qps
                 line["recall_queries"] = args.recall_queries
             except Exception as ex:  # evaluation is reported, never gates the timing
                 line["recall_at_10"] = f"failed: {ex}"

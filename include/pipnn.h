@@ -180,6 +180,26 @@ PIPNN_API pipnn_status pipnn_final_prune(const pipnn_points* X, const pipnn_hash
 PIPNN_API pipnn_status pipnn_build(const pipnn_points* X, const pipnn_build_params* p, void* ws, size_t ws_bytes,
                          uint64_t* row_ptr, uint32_t* col_idx, int64_t* n_edges_h, pipnn_stats* stats_h, void* stream);
 
+/* Batched greedy beam search over a built graph (Alg. 1 BeamSearch), the
+ * query side of the k-NN-graph / ANN tasks. Per query: beam of the L best (D, id) seen, start
+ * at `entry`; repeatedly expand the first unvisited beam element, adding each out-neighbour that is neither
+ * visited nor in the beam; stop when the whole beam is visited; answer = the beam's first k.
+ *   queries: DEVICE, [nq, ld_q] of X's dtype (uint8 / float32), row-major; X, row_ptr, col_idx: as built by
+ *   pipnn_build (row_ptr[n+1] u64, col_idx u32, any out-degree). 1 <= k <= L <= 256, entry < n.
+ *   out_ids [nq, k] u32 (UINT32_MAX past the beam's end), out_dist [nq, k] f32 (nullable): uint8 exact
+ *   squared L2; float fp32 squared L2 or -dot (MIPS). n_cmps_dev: nullable DEVICE int64 accumulating the
+ *   number of distance evaluations. Workspace: the two-call protocol (ws == NULL -> PIPNN_EWORKSPACE with the
+ *   size in pipnn_required_workspace()); holds the device error flag. Asynchronous on `stream`; a visited set
+ *   overflow (more than 2048 expansions for one query) is reported as PIPNN_ECAPACITY by the next
+ *   synchronising call or pipnn_device_error. */
+typedef struct {
+  int32_t L, k;
+} pipnn_search_params;
+PIPNN_API pipnn_status pipnn_search(const pipnn_points* X, const uint64_t* row_ptr, const uint32_t* col_idx,
+                                    const void* queries, int64_t ld_q, int64_t nq, uint32_t entry,
+                                    const pipnn_search_params* p, uint32_t* out_ids, float* out_dist,
+                                    int64_t* n_cmps_dev, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -59,6 +59,10 @@ class PruneParams(C.Structure):
     _fields_ = [("R", C.c_int32), ("alpha_num", C.c_int32), ("alpha_den", C.c_int32), ("final_prune", C.c_int32)]
 
 
+class SearchParams(C.Structure):
+    _fields_ = [("L", C.c_int32), ("k", C.c_int32)]
+
+
 class BuildParams(C.Structure):
     _fields_ = [("part", PartitionParams), ("pick", PickParams), ("hp", HashPruneParams), ("prune", PruneParams)]
 
@@ -91,8 +95,10 @@ _lib.hashprune_insert.argtypes = [_P(HashPruneParams), C.c_int64, _vp, C.c_int32
 _lib.pipnn_final_prune.argtypes = [_P(Points), _P(HashPruneParams), _vp, _vp, _P(PruneParams), _vp, _vp, _vp,
                                    C.c_size_t, _vp]
 _lib.pipnn_build.argtypes = [_P(Points), _P(BuildParams), _vp, C.c_size_t, _vp, _vp, _P(C.c_int64), _P(Stats), _vp]
+_lib.pipnn_search.argtypes = [_P(Points), _vp, _vp, _vp, C.c_int64, C.c_int64, C.c_uint32, _P(SearchParams), _vp, _vp,
+                              _vp, _vp, C.c_size_t, _vp]
 for _f in ("pipnn_workspace_size", "pipnn_partition", "pipnn_leaf_pick", "pipnn_sketch", "pipnn_device_error",
-           "hashprune_insert", "pipnn_final_prune", "pipnn_build"):
+           "hashprune_insert", "pipnn_final_prune", "pipnn_build", "pipnn_search"):
     getattr(_lib, _f).restype = C.c_int
 
 EXPORTS = ("pipnn_last_error", "pipnn_abi_version", "pipnn_required_workspace", "pipnn_launch_count", "pipnn_workspace_size",
@@ -291,6 +297,30 @@ def pipnn_final_prune(X: torch.Tensor, slots: torch.Tensor, count: torch.Tensor,
     _check(call(_ptr(ws), ws.numel()))
     pipnn_device_error(ws, stream)
     return row_ptr, col_idx
+
+
+def pipnn_search(X: torch.Tensor, row_ptr: torch.Tensor, col_idx: torch.Tensor, Q: torch.Tensor, entry: int,
+                 L: int = 64, k: int = 10, metric="l2", stream=None, count_cmps: bool = False):
+    """Batched beam search (Alg. 1) of the queries Q [nq, d] (X's dtype, on the device) on the graph (row_ptr,
+    col_idx) from `entry` -> (ids int32 [nq, k] (uint32 ids, -1 past the beam), dist float32 [nq, k], n_cmps)."""
+    pts = points(X, metric)
+    if Q.dtype != X.dtype or Q.dim() != 2 or Q.stride(1) != 1 or not Q.is_cuda:
+        raise ValueError("Q must be a CUDA [nq, d] tensor of X's dtype with unit column stride")
+    nq = Q.shape[0]
+    sp = SearchParams(L, k)
+    ids = torch.empty((nq, k), dtype=torch.int32, device=X.device)
+    dist = torch.empty((nq, k), dtype=torch.float32, device=X.device)
+    cmps = torch.zeros(1, dtype=torch.int64, device=X.device) if count_cmps else None
+    st = _stream(stream)
+
+    def call(ws, nbytes):
+        return _lib.pipnn_search(C.byref(pts), _ptr(row_ptr), _ptr(col_idx), _ptr(Q), Q.stride(0), nq, int(entry),
+                                 C.byref(sp), _ptr(ids), _ptr(dist), _ptr(cmps), ws, nbytes, st)
+
+    ws = _workspace(call, X.device)
+    _check(call(_ptr(ws), ws.numel()))
+    pipnn_device_error(ws, stream)
+    return ids, dist, (int(cmps.item()) if cmps is not None else None)
 
 
 @dataclass

@@ -454,4 +454,25 @@ pipnn_status pipnn_build(const pipnn_points* X, const pipnn_build_params* p, voi
   return build_impl(X, p, ar, (cudaStream_t)stream, row_ptr, col_idx, n_edges_h, stats_h);
 }
 
+pipnn_status pipnn_search(const pipnn_points* X, const uint64_t* row_ptr, const uint32_t* col_idx,
+                          const void* queries, int64_t ld_q, int64_t nq, uint32_t entry, const pipnn_search_params* p,
+                          uint32_t* out_ids, float* out_dist, int64_t* n_cmps_dev, void* ws, size_t ws_bytes,
+                          void* stream) {
+  PIPNN_TRY(validate_points(X));
+  if (!p) return fail(PIPNN_EINVAL, "search params NULL");
+  if (p->k < 1 || p->L < p->k || p->L > 256) return fail(PIPNN_EINVAL, "need 1 <= k <= L <= 256");
+  if (nq < 0 || (nq > 0 && (!queries || !out_ids || !row_ptr || !col_idx))) return fail(PIPNN_EINVAL, "NULL argument");
+  if (ld_q < X->d) return fail(PIPNN_EINVAL, "ld_q < d");
+  if ((int64_t)entry >= X->n) return fail(PIPNN_EINVAL, "entry out of range");
+  if (search_smem_per_warp(X) * 4 > 227 * 1024) return fail(PIPNN_EUNSUPPORTED, "d too large for the search kernel");
+  cudaStream_t st = (cudaStream_t)stream;
+  PIPNN_TRY(check_ws(ws, ws_bytes, 256));
+  PIPNN_TRY(pending_cuda());
+  Arena ar(ws, ws_bytes);
+  int* err = err_slot(ar);
+  PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+  return search_impl(X, row_ptr, col_idx, queries, ld_q, nq, entry, p->L, p->k, out_ids, out_dist, n_cmps_dev,
+                     Ctx{st, err});
+}
+
 }  // extern "C"
