@@ -207,7 +207,26 @@ def recall_eval(Xd, cfg, row_ptr, col_idx, n_queries):
         qps[str(L)] = round(len(Q) / (e0.elapsed_time(e1) / 1e3))
         hit = (ids.long().unsqueeze(2) == truth.unsqueeze(1)).any(2).sum(1).float() / 10.0
         recall[str(L)] = round(float(hit.mean().item()), 4)
-    return recall, qps
+    # the k-NN-graph task: every base point queried on the index (itself excluded), L = 64;
+    # recall@10 on 1,000 sampled points against their exact 10 nearest other points
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    gids, _ = P.knn_graph(Xd, row_ptr, col_idx, entry, 10, 64, cfg.metric)
+    e1.record()
+    torch.cuda.synchronize()
+    knn_pps = Xd.shape[0] / (e0.elapsed_time(e1) / 1e3)
+    g = torch.Generator(device="cpu").manual_seed(5)
+    smp = torch.randperm(Xd.shape[0], generator=g)[:1000].to(Xd.device)
+    Xf = Xd.float()
+    Sf = Xf[smp]
+    if cfg.metric == "mips":
+        D = -(Sf @ Xf.T)
+    else:
+        D = (Sf * Sf).sum(1, keepdim=True) + (Xf * Xf).sum(1)[None] - 2 * (Sf @ Xf.T)
+    D[torch.arange(len(smp), device=D.device), smp] = float("inf")
+    gt = torch.topk(D, 10, dim=1, largest=False).indices
+    knn_rec = float(((gids[smp].long().unsqueeze(2) == gt.unsqueeze(1)).any(2).sum(1).float() / 10.0).mean().item())
+    return recall, qps, {"points_per_s": round(knn_pps), "L": 64, "k": 10, "recall_at_10_sample1000": round(knn_rec, 4)}
 
 
 def main():
@@ -337,9 +356,10 @@ def main():
         }
         if args.recall_queries > 0:
             try:
-                rec, qps = recall_eval(Xd, cfg, out.row_ptr, out.col_idx, args.recall_queries)
+                rec, qps, knn = recall_eval(Xd, cfg, out.row_ptr, out.col_idx, args.recall_queries)
                 line["recall_at_10"] = rec
                 line["search_qps"] = qps
+                line["knn_graph_task"] = knn
                 line["recall_queries"] = args.recall_queries
             except Exception as ex:  # evaluation is reported, never gates the timing
                 line["recall_at_10"] = f"failed: {ex}"

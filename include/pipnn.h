@@ -194,6 +194,8 @@ PIPNN_API pipnn_status pipnn_build(const pipnn_points* X, const pipnn_build_para
  *   synchronising call or pipnn_device_error. */
 typedef struct {
   int32_t L, k;
+  int32_t exclude_self;  /* 1: query i is base point i (the k-NN-graph task): id i is left out of
+                          * its own answer (it still steers the search) */
 } pipnn_search_params;
 PIPNN_API pipnn_status pipnn_search(const pipnn_points* X, const uint64_t* row_ptr, const uint32_t* col_idx,
                                     const void* queries, int64_t ld_q, int64_t nq, uint32_t entry,

@@ -60,7 +60,7 @@ class PruneParams(C.Structure):
 
 
 class SearchParams(C.Structure):
-    _fields_ = [("L", C.c_int32), ("k", C.c_int32)]
+    _fields_ = [("L", C.c_int32), ("k", C.c_int32), ("exclude_self", C.c_int32)]
 
 
 class BuildParams(C.Structure):
@@ -300,14 +300,14 @@ def pipnn_final_prune(X: torch.Tensor, slots: torch.Tensor, count: torch.Tensor,
 
 
 def pipnn_search(X: torch.Tensor, row_ptr: torch.Tensor, col_idx: torch.Tensor, Q: torch.Tensor, entry: int,
-                 L: int = 64, k: int = 10, metric="l2", stream=None, count_cmps: bool = False):
+                 L: int = 64, k: int = 10, metric="l2", stream=None, count_cmps: bool = False, exclude_self=False):
     """Batched beam search (Alg. 1) of the queries Q [nq, d] (X's dtype, on the device) on the graph (row_ptr,
     col_idx) from `entry` -> (ids int32 [nq, k] (uint32 ids, -1 past the beam), dist float32 [nq, k], n_cmps)."""
     pts = points(X, metric)
     if Q.dtype != X.dtype or Q.dim() != 2 or Q.stride(1) != 1 or not Q.is_cuda:
         raise ValueError("Q must be a CUDA [nq, d] tensor of X's dtype with unit column stride")
     nq = Q.shape[0]
-    sp = SearchParams(L, k)
+    sp = SearchParams(L, k, 1 if exclude_self else 0)
     ids = torch.empty((nq, k), dtype=torch.int32, device=X.device)
     dist = torch.empty((nq, k), dtype=torch.float32, device=X.device)
     cmps = torch.zeros(1, dtype=torch.int64, device=X.device) if count_cmps else None
@@ -321,6 +321,14 @@ def pipnn_search(X: torch.Tensor, row_ptr: torch.Tensor, col_idx: torch.Tensor, 
     _check(call(_ptr(ws), ws.numel()))
     pipnn_device_error(ws, stream)
     return ids, dist, (int(cmps.item()) if cmps is not None else None)
+
+
+def knn_graph(X: torch.Tensor, row_ptr: torch.Tensor, col_idx: torch.Tensor, entry: int, k: int = 10, L: int = 64,
+              metric="l2", stream=None):
+    """The k-NN-graph task: every base point queried on its own index, itself left out ->
+    (ids int32 [n, k], dist float32 [n, k])."""
+    ids, dist, _ = pipnn_search(X, row_ptr, col_idx, X, entry, L, k, metric, stream, exclude_self=True)
+    return ids, dist
 
 
 @dataclass

@@ -461,6 +461,7 @@ pipnn_status pipnn_search(const pipnn_points* X, const uint64_t* row_ptr, const 
   PIPNN_TRY(validate_points(X));
   if (!p) return fail(PIPNN_EINVAL, "search params NULL");
   if (p->k < 1 || p->L < p->k || p->L > 256) return fail(PIPNN_EINVAL, "need 1 <= k <= L <= 256");
+  if (p->exclude_self && (p->L < p->k + 1 || nq > X->n)) return fail(PIPNN_EINVAL, "exclude_self needs L > k, nq <= n");
   if (nq < 0 || (nq > 0 && (!queries || !out_ids || !row_ptr || !col_idx))) return fail(PIPNN_EINVAL, "NULL argument");
   if (ld_q < X->d) return fail(PIPNN_EINVAL, "ld_q < d");
   if ((int64_t)entry >= X->n) return fail(PIPNN_EINVAL, "entry out of range");
@@ -471,8 +472,8 @@ pipnn_status pipnn_search(const pipnn_points* X, const uint64_t* row_ptr, const 
   Arena ar(ws, ws_bytes);
   int* err = err_slot(ar);
   PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
-  return search_impl(X, row_ptr, col_idx, queries, ld_q, nq, entry, p->L, p->k, out_ids, out_dist, n_cmps_dev,
-                     Ctx{st, err});
+  return search_impl(X, row_ptr, col_idx, queries, ld_q, nq, entry, p->L, p->k, p->exclude_self ? 1 : 0, out_ids,
+                     out_dist, n_cmps_dev, Ctx{st, err});
 }
 
 }  // extern "C"

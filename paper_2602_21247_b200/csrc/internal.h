@@ -71,8 +71,8 @@ bool subtree_fits(const pipnn_points* X, const pipnn_partition_params* p, int64_
 // Batched beam search (search.cu, Alg. 1): one warp per query; L <= 256.
 size_t search_smem_per_warp(const pipnn_points* X);
 pipnn_status search_impl(const pipnn_points* X, const uint64_t* row_ptr, const uint32_t* col_idx, const void* Q,
-                         int64_t ldq, int64_t nq, uint32_t entry, int L, int k, uint32_t* out_ids, float* out_dist,
-                         int64_t* n_cmps_dev, const Ctx& c);
+                         int64_t ldq, int64_t nq, uint32_t entry, int L, int k, int excl, uint32_t* out_ids,
+                         float* out_dist, int64_t* n_cmps_dev, const Ctx& c);
 size_t subtree_group_bytes();
 pipnn_status subtree_launch(const pipnn_points* X, const pipnn_partition_params* p, const void* groups, int n_groups,
                             const uint32_t* mem, uint32_t* staging, int64_t stage_cap, unsigned long long* stage_cursor,

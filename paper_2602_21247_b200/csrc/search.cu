@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(32 * kSrchWarps) search_kernel(const void* __r
                                                                  const uint64_t* __restrict__ row_ptr,
                                                                  const uint32_t* __restrict__ col_idx,
                                                                  const void* __restrict__ Q, int64_t ldq, int64_t nq,
-                                                                 uint32_t entry, int L, int k,
+                                                                 uint32_t entry, int L, int k, int excl,
                                                                  uint32_t* __restrict__ out_ids,
                                                                  float* __restrict__ out_dist,
                                                                  int64_t* __restrict__ n_cmps, int* err) {
@@ -270,9 +270,20 @@ __global__ void __launch_bounds__(32 * kSrchWarps) search_kernel(const void* __r
       cur = nxt;
       nb = nt;
     }
+    // answer: the beam's first k (excluding the query's own id for the k-NN-graph task)
+    int pself = nb;
+    if (excl) {
+      for (int b0 = 0; b0 < nb; b0 += 32) {
+        const bool me = b0 + lane < nb && (uint32_t)(S.beam[cur][b0 + lane] & 0xFFFFFFFFu) == (uint32_t)qi;
+        const uint32_t bal = __ballot_sync(0xffffffffu, me);
+        if (bal && pself == nb) pself = b0 + __ffs(bal) - 1;
+      }
+    }
+    const int nav = nb - (pself < nb ? 1 : 0);
     for (int t = lane; t < k; t += 32) {
-      const bool ok = t < nb;
-      const uint64_t key = ok ? S.beam[cur][t] : ~0ull;
+      const bool ok = t < nav;
+      const int src = t + (t >= pself ? 1 : 0);
+      const uint64_t key = ok ? S.beam[cur][src] : ~0ull;
       out_ids[qi * k + t] = ok ? (uint32_t)(key & 0xFFFFFFFFu) : kEmpty;
       if (out_dist) {
         float D = __int_as_float(0x7F800000);
@@ -294,8 +305,8 @@ size_t search_smem_per_warp(const pipnn_points* X) {
 }
 
 pipnn_status search_impl(const pipnn_points* X, const uint64_t* row_ptr, const uint32_t* col_idx, const void* Q,
-                         int64_t ldq, int64_t nq, uint32_t entry, int L, int k, uint32_t* out_ids, float* out_dist,
-                         int64_t* n_cmps_dev, const Ctx& c) {
+                         int64_t ldq, int64_t nq, uint32_t entry, int L, int k, int excl, uint32_t* out_ids,
+                         float* out_dist, int64_t* n_cmps_dev, const Ctx& c) {
   if (nq == 0) return PIPNN_OK;
   const size_t smem = kSrchWarps * search_smem_per_warp(X);
   const int64_t blocks = std::min<int64_t>(ceil_div(nq, kSrchWarps), (int64_t)num_sms() * 16);
@@ -303,7 +314,7 @@ pipnn_status search_impl(const pipnn_points* X, const uint64_t* row_ptr, const u
   do {                                                                                                             \
     PIPNN_CUDA(cudaFuncSetAttribute(search_kernel<U, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
     search_kernel<U, M><<<(unsigned)blocks, 32 * kSrchWarps, smem, c.st>>>(X->data, X->ld, X->d, row_ptr, col_idx,  \
-                                                                          Q, ldq, nq, entry, L, k, out_ids,         \
+                                                                          Q, ldq, nq, entry, L, k, excl, out_ids,   \
                                                                           out_dist, n_cmps_dev, c.err);             \
   } while (0)
   if (X->dtype == PIPNN_U8) SR_LAUNCH(true, false);

@@ -78,3 +78,23 @@ def test_search_edge_cases():
     assert (ids[:, 0] == 7).all() and (ids[:, 1:] == 0xFFFFFFFF).all() and cmps == 3
     with pytest.raises(Exception):
         run(X, ref.row_ptr, ref.col_idx, Q, 0, 300, 10, "l2")  # L > 256
+
+
+def test_knn_graph_task_u8_bit_exact():
+    # the k-NN-graph task: every base point queried on the index, itself left out; against the
+    # oracle harness's beam search with k + 1 and the point itself dropped
+    cfg = synth.C2.scaled(6000)
+    X = synth.gen_points(cfg)
+    ds = O.Dataset(X)
+    ref = O.build(ds, cfg.params())
+    e = O.entry_point(ds)
+    k, L = 10, 32
+    oids, _ = O.beam_search(ds, ref.row_ptr, ref.col_idx, X, e, L, L)
+    want = np.full((len(X), k), 0xFFFFFFFF, dtype=np.uint32)
+    for i in range(len(X)):
+        row = [v for v in oids[i] if v != i and v != 0xFFFFFFFF][:k]
+        want[i, :len(row)] = row
+    ids, dist = P().knn_graph(torch.from_numpy(X).cuda(), torch.from_numpy(ref.row_ptr.astype(np.int64)).cuda(),
+                              torch.from_numpy(ref.col_idx.view(np.int32)).cuda(), e, k, L)
+    torch.cuda.synchronize()
+    assert np.array_equal(ids.cpu().numpy().view(np.uint32), want)
