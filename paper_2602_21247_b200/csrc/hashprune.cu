@@ -614,6 +614,8 @@ __global__ void __launch_bounds__(256) hp_merge_table_kernel(int m, int l_max, i
   __shared__ int s8[8];
   __shared__ uint32_t s_hist[256];
   __shared__ uint32_t s_sel;
+  __shared__ uint32_t s_inst[256], s_rs[256];
+  __shared__ int s_off[257];
   const int NB = 1 << m, tid = threadIdx.x;
   const int per = (NB + 255) / 256;  // table entries per thread (<= 16; contiguous chunk: keeps the hash order)
   const int64_t nl = *list_n;
@@ -629,17 +631,37 @@ __global__ void __launch_bounds__(256) hp_merge_table_kernel(int m, int l_max, i
       const uint64_t key = res[t];
       atomicMin((unsigned long long*)&tbl[key >> 48], (unsigned long long)key);
     }
+    // the owner's instances, 256 at a time: their (instance, reverse start, key count) staged in parallel, then
+    // the keys of all of them as one flat index space (a thread per key, segment by binary search)
     const uint64_t i0 = inv_start[u], i1 = inv_start[u + 1];
-    for (uint64_t q = i0; q < i1; ++q) {
-      const uint32_t i = inv[q];
-      const int ni = k + (int)rev_cnt[i];
-      const uint64_t rs = rev_start[i];
-      for (int j = tid; j < ni; j += 256) {
-        const uint64_t key = j < k ? fwd[(int64_t)i * k + j] : rev[rs + (j - k)];
+    for (uint64_t q0 = i0; q0 < i1; q0 += 256) {
+      const int ni = (int)(i1 - q0 < 256 ? i1 - q0 : 256);
+      int sz = 0;
+      if (tid < ni) {
+        const uint32_t i = inv[q0 + tid];
+        s_inst[tid] = i;
+        s_rs[tid] = rev_start[i];
+        sz = k + (int)rev_cnt[i];
+      }
+      const int off = block256_excl(sz, s8);  // (its barriers also publish s_inst / s_rs)
+      if (tid < ni) s_off[tid] = off;
+      if (tid == ni - 1) s_off[ni] = off + sz;
+      __syncthreads();
+      const int tot = s_off[ni];
+      for (int f = tid; f < tot; f += 256) {
+        int lo = 0, hi = ni - 1;  // the segment holding flat index f: largest t with s_off[t] <= f
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (s_off[mid] <= f) lo = mid;
+          else hi = mid - 1;
+        }
+        const int j = f - s_off[lo];
+        const uint32_t i = s_inst[lo];
+        const uint64_t key = j < k ? fwd[(int64_t)i * k + j] : rev[(uint64_t)s_rs[lo] + (j - k)];
         if (key != ~0ull) atomicMin((unsigned long long*)&tbl[key >> 48], (unsigned long long)key);
       }
+      __syncthreads();
     }
-    __syncthreads();
     uint64_t v[16];
     int cnt = 0;
     const int b0 = tid * per;

@@ -70,7 +70,11 @@ C4 = Config("C4", n=1_000_000, d=200, dtype="f32", metric="mips", n_centres=5_00
             l_max=160, n_queries=10_000)
 C5 = Config("C5", n=50_000_000, d=128, dtype="u8", metric="l2", n_centres=100_000, c_max=2048, l_max=96, R=32,
             n_queries=10_000)
-CONFIGS = {"C1": C1, "C2": C2, "C3": C3, "C4": C4, "C5": C5}
+# SURVEY §8(f) NEXT-3, the paper's overlap knobs on the C2 workload: a
+# two-level fanout [10, 3] and two replicas (bench variants, not BASELINE configs)
+C2_F103 = dataclasses.replace(C2, name="C2-f10x3", fanout=(10, 3))
+C2_R2 = dataclasses.replace(C2, name="C2-rep2", replicas=2)
+CONFIGS = {"C1": C1, "C2": C2, "C3": C3, "C4": C4, "C5": C5, "C2-f10x3": C2_F103, "C2-rep2": C2_R2}
 
 
 def _mixture_f32(rng: np.random.Generator, n: int, d: int, centres: np.ndarray, sigma: float) -> np.ndarray:
