@@ -617,24 +617,19 @@ __global__ void __launch_bounds__(256) hp_merge_table_kernel(int m, int l_max, i
   __shared__ uint32_t s_inst[256], s_rs[256];
   __shared__ int s_off[257];
   const int NB = 1 << m, tid = threadIdx.x;
-  const int per = (NB + 255) / 256;  // table entries per thread (<= 16; contiguous chunk: keeps the hash order)
   const int64_t nl = *list_n;
   constexpr uint64_t kLow48 = 0xFFFFFFFFFFFFull;
   for (int64_t it = blockIdx.x; it < nl; it += gridDim.x) {
     const int64_t u = list[it];
     uint64_t* res = slots + u * (int64_t)l_max;
     const int c = (int)count[u];
-    __syncthreads();  // the previous owner's table is no longer read
-    for (int t = tid; t < NB; t += 256) tbl[t] = ~0ull;
-    __syncthreads();
-    for (int t = tid; t < c; t += 256) {
-      const uint64_t key = res[t];
-      atomicMin((unsigned long long*)&tbl[key >> 48], (unsigned long long)key);
-    }
-    // the owner's instances, 256 at a time: their (instance, reverse start, key count) staged in parallel, then
-    // the keys of all of them as one flat index space (a thread per key, segment by binary search)
     const uint64_t i0 = inv_start[u], i1 = inv_start[u + 1];
-    for (uint64_t q0 = i0; q0 < i1; q0 += 256) {
+    // table size: 2^m slots indexed by the hash, or — for an owner whose keys all fit one staging round — the
+    // power of two >= 2 x its key count (>= 256), probed linearly from hash & (S - 1): fewer slots to clear
+    // and read back. (The build's reservoirs are read as sets; only the hash-indexed table keeps hash order.)
+    int S = NB;
+    bool staged = false;
+    auto stage = [&](uint64_t q0) -> int {  // instances q0.. (<= 256): ids, reverse starts, key offsets
       const int ni = (int)(i1 - q0 < 256 ? i1 - q0 : 256);
       int sz = 0;
       if (tid < ni) {
@@ -647,6 +642,45 @@ __global__ void __launch_bounds__(256) hp_merge_table_kernel(int m, int l_max, i
       if (tid < ni) s_off[tid] = off;
       if (tid == ni - 1) s_off[ni] = off + sz;
       __syncthreads();
+      return ni;
+    };
+    __syncthreads();  // the previous owner's table and staging arrays are no longer read
+    int ni0 = 0;
+    if (i1 - i0 <= 256) {
+      ni0 = i1 > i0 ? stage(i0) : 0;
+      staged = true;
+      const int T = c + (ni0 ? s_off[ni0] : 0);
+      while (S > 256 && S >= 4 * T) S >>= 1;
+    }
+    const bool direct = S == NB;
+    for (int t = tid; t < S; t += 256) tbl[t] = ~0ull;
+    __syncthreads();
+    auto put = [&](uint64_t key) {
+      const uint32_t h = (uint32_t)(key >> 48);
+      if (direct) {
+        atomicMin((unsigned long long*)&tbl[h], (unsigned long long)key);
+        return;
+      }
+      uint32_t sl = h & (uint32_t)(S - 1);
+      while (true) {
+        unsigned long long cur = *(volatile unsigned long long*)&tbl[sl];
+        if (cur == ~0ull) {
+          cur = atomicCAS((unsigned long long*)&tbl[sl], ~0ull, (unsigned long long)key);
+          if (cur == ~0ull) return;
+        }
+        if ((uint32_t)(cur >> 48) == h) {
+          atomicMin((unsigned long long*)&tbl[sl], (unsigned long long)key);
+          return;
+        }
+        sl = (sl + 1) & (uint32_t)(S - 1);
+      }
+    };
+    for (int t = tid; t < c; t += 256) put(res[t]);
+    // the owner's instances, 256 at a time, their keys as one flat index space (a thread per key, segment by
+    // binary search)
+    for (uint64_t q0 = i0; q0 < i1; q0 += 256) {
+      const int ni = staged ? ni0 : stage(q0);
+      staged = false;
       const int tot = s_off[ni];
       for (int f = tid; f < tot; f += 256) {
         int lo = 0, hi = ni - 1;  // the segment holding flat index f: largest t with s_off[t] <= f
@@ -658,16 +692,17 @@ __global__ void __launch_bounds__(256) hp_merge_table_kernel(int m, int l_max, i
         const int j = f - s_off[lo];
         const uint32_t i = s_inst[lo];
         const uint64_t key = j < k ? fwd[(int64_t)i * k + j] : rev[(uint64_t)s_rs[lo] + (j - k)];
-        if (key != ~0ull) atomicMin((unsigned long long*)&tbl[key >> 48], (unsigned long long)key);
+        if (key != ~0ull) put(key);
       }
       __syncthreads();
     }
     uint64_t v[16];
     int cnt = 0;
+    const int per = (S + 255) / 256;  // table entries per thread (<= 16; contiguous chunk)
     const int b0 = tid * per;
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-      v[e] = (e < per && b0 + e < NB) ? tbl[b0 + e] : ~0ull;
+      v[e] = (e < per && b0 + e < S) ? tbl[b0 + e] : ~0ull;
       cnt += v[e] != ~0ull ? 1 : 0;
     }
     const int total = block256_sum(cnt, s8);
