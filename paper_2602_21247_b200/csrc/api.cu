@@ -99,9 +99,11 @@ static pipnn_status pending_cuda() {
 }
 
 static pipnn_status read_dev_error(int* err, cudaStream_t st) {
-  int h = 0;
-  PIPNN_CUDA(cudaMemcpyAsync(&h, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  int* hp = reinterpret_cast<int*>(pinned_scratch(sizeof(int)));
+  if (!hp) return fail(PIPNN_ECUDA, "pinned host scratch");
+  PIPNN_CUDA(cudaMemcpyAsync(hp, err, sizeof(int), cudaMemcpyDeviceToHost, st));
   PIPNN_CUDA(cudaStreamSynchronize(st));
+  const int h = *hp;
   if (h == DERR_NONFINITE) return fail(PIPNN_EINVAL, "non-finite float input");
   if (h != 0) return fail(PIPNN_ECUDA, "device error flag " + std::to_string(h) + " (bounded wait timeout / capacity)");
   return PIPNN_OK;
@@ -119,6 +121,26 @@ static BuildPlan plan_of(const pipnn_points* X, const pipnn_build_params* p) {
 }
 
 // Runs the whole build through an Arena; with a measuring Arena it only sizes the workspace.
+uint8_t* pinned_scratch(size_t bytes) {
+  struct Scratch {
+    uint8_t* p = nullptr;
+    size_t cap = 0;
+    ~Scratch() {
+      if (p) cudaFreeHost(p);
+    }
+  };
+  static thread_local Scratch s;
+  if (bytes > s.cap) {
+    if (s.p) cudaFreeHost(s.p);
+    s.p = nullptr;
+    s.cap = 0;
+    const size_t cap = std::max<size_t>(bytes, (size_t)1 << 16);
+    if (cudaHostAlloc((void**)&s.p, cap, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+    s.cap = cap;
+  }
+  return s.p;
+}
+
 static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* p, Arena& ar, cudaStream_t st,
                                uint64_t* row_ptr, uint32_t* col_idx, int64_t* n_edges_h, pipnn_stats* stats_h) {
   const BuildPlan bp = plan_of(X, p);
@@ -216,8 +238,11 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
     if (s != PIPNN_OK) { cleanup(); return s; }
   } else if (n_leaves > 0) {
     std::vector<int64_t> off(n_leaves + 1);
-    PIPNN_CUDA(cudaMemcpyAsync(off.data(), leaf_off, (n_leaves + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    int64_t* hoff = reinterpret_cast<int64_t*>(pinned_scratch((n_leaves + 1) * sizeof(int64_t)));
+    if (!hoff) { cleanup(); return fail(PIPNN_ECUDA, "pinned host scratch"); }
+    PIPNN_CUDA(cudaMemcpyAsync(hoff, leaf_off, (n_leaves + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     PIPNN_CUDA(cudaStreamSynchronize(st));
+    std::copy(hoff, hoff + n_leaves + 1, off.begin());
     max_leaf_h = 1;
     for (int64_t b = 0; b < n_leaves; ++b) {
       leaf_pairs += (off[b + 1] - off[b]) * (off[b + 1] - off[b]);
@@ -264,12 +289,21 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   if (s != PIPNN_OK) { cleanup(); return s; }
   if (ar.measuring()) return PIPNN_OK;
   PIPNN_CUDA(cudaEventRecord(ev[5], st));
-  uint64_t ne = 0;
-  int64_t nstream = 0;
-  PIPNN_CUDA(cudaMemcpyAsync(&ne, row_ptr + X->n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-  PIPNN_CUDA(cudaMemcpyAsync(&nstream, n_edges_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  s = read_dev_error(err, st);
-  if (s != PIPNN_OK) { cleanup(); return s; }
+  // one pinned read-back: edge count, streamed-edge count, device error flag
+  int64_t* hb = reinterpret_cast<int64_t*>(pinned_scratch(3 * sizeof(int64_t)));
+  if (!hb) { cleanup(); return fail(PIPNN_ECUDA, "pinned host scratch"); }
+  hb[2] = 0;
+  PIPNN_CUDA(cudaMemcpyAsync(&hb[0], row_ptr + X->n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+  PIPNN_CUDA(cudaMemcpyAsync(&hb[1], n_edges_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  PIPNN_CUDA(cudaMemcpyAsync(&hb[2], err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PIPNN_CUDA(cudaStreamSynchronize(st));
+  const uint64_t ne = (uint64_t)hb[0];
+  const int64_t nstream = hb[1];
+  {
+    const int h = (int)(hb[2] & 0xFFFFFFFF);
+    if (h == DERR_NONFINITE) { cleanup(); return fail(PIPNN_EINVAL, "non-finite float input"); }
+    if (h != 0) { cleanup(); return fail(PIPNN_ECUDA, "device error flag " + std::to_string(h) + " (bounded wait timeout / capacity)"); }
+  }
   if (n_edges_h) *n_edges_h = (int64_t)ne;
   if (stats_h) {
     float t[6];
@@ -285,13 +319,7 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
     stats_h->n_instances = n_inst;
     stats_h->n_edges = nstream;
     stats_h->depth = depth;
-    int64_t mx = 0;
-    if (n_leaves > 0) {
-      std::vector<int64_t> off(n_leaves + 1);
-      cudaMemcpy(off.data(), leaf_off, (n_leaves + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost);
-      for (int64_t b = 0; b < n_leaves; ++b) mx = std::max(mx, off[b + 1] - off[b]);
-    }
-    stats_h->max_leaf = mx;
+    stats_h->max_leaf = n_leaves > 0 ? max_leaf_h : 0;  // measured from the leaf offsets read after the partition
     stats_h->leaf_pairs = leaf_pairs;
     float tt = 0.0f;
     for (auto& pr : tile_ev) {

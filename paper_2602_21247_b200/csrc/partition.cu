@@ -592,14 +592,17 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     tb = cub_bytes;
     PIPNN_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, pk, pk2, cv2, nxt, (int)Q, 0, bits_for(C), st));
     // ---- 4. host merge plan (the level's one synchronisation)
-    std::vector<uint32_t> hccnt(C), hlead(C);
-    int hredo = 0;
-    PIPNN_CUDA(cudaMemcpyAsync(hccnt.data(), ccnt, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    PIPNN_CUDA(cudaMemcpyAsync(hlead.data(), lead_sorted, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    PIPNN_CUDA(cudaMemcpyAsync(&hredo, d_redo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    // (pinned read-back: the three copies stay asynchronous, one synchronisation)
+    uint32_t* hbuf = reinterpret_cast<uint32_t*>(pinned_scratch((2 * C + 1) * sizeof(uint32_t)));
+    if (!hbuf) return fail(PIPNN_ECUDA, "pinned host scratch");
+    PIPNN_CUDA(cudaMemcpyAsync(hbuf, ccnt, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    PIPNN_CUDA(cudaMemcpyAsync(hbuf + C, lead_sorted, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    PIPNN_CUDA(cudaMemcpyAsync(hbuf + 2 * C, d_redo, sizeof(int), cudaMemcpyDeviceToHost, st));
     if (dbg_timing) t_sync0 = wall();
     PIPNN_CUDA(cudaStreamSynchronize(st));
     if (dbg_timing) t_sync1 = wall();
+    std::vector<uint32_t> hccnt(hbuf, hbuf + C), hlead(hbuf + C, hbuf + 2 * C);
+    const int hredo = (int)hbuf[2 * C];
     if (hredo) {
       if (redo_unfiltered) return fail(PIPNN_ECUDA, "partition: leader selection failed without filter");
       redo_unfiltered = true;  // exceedingly rare: every member becomes a leader candidate
@@ -703,11 +706,14 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
   g_pin_level.reset();
   PIPNN_CUDA(g_pin_level.copy(leaf_dst, h_leaf_dst.data(), n_leaves * sizeof(int64_t), st));
   {
-    unsigned long long hc[2] = {0ull, 0ull};
-    int hdepth = 0;
-    PIPNN_CUDA(cudaMemcpyAsync(hc, dev_ctr, sizeof(hc), cudaMemcpyDeviceToHost, st));
-    PIPNN_CUDA(cudaMemcpyAsync(&hdepth, dev_work + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    unsigned long long* hb = reinterpret_cast<unsigned long long*>(pinned_scratch(3 * sizeof(unsigned long long)));
+    if (!hb) return fail(PIPNN_ECUDA, "pinned host scratch");
+    hb[2] = 0;
+    PIPNN_CUDA(cudaMemcpyAsync(hb, dev_ctr, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    PIPNN_CUDA(cudaMemcpyAsync(&hb[2], dev_work + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
     PIPNN_CUDA(cudaStreamSynchronize(st));
+    const unsigned long long hc[2] = {hb[0], hb[1]};
+    const int hdepth = (int)(hb[2] & 0xFFFFFFFFull);
     const int64_t nd = (int64_t)hc[0];
     if (n_leaves + nd > cp.leaves) return fail(PIPNN_ECAPACITY, "partition: leaf capacity (device subtrees)");
     if (nd > 0) {
@@ -726,9 +732,11 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
                                                                                          staging, leaf_ids);
     PIPNN_LAUNCHED("leaf_compact_kernel", st);
   }
-  int64_t ni = 0;
-  PIPNN_CUDA(cudaMemcpyAsync(&ni, leaf_off + n_leaves, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  int64_t* hni = reinterpret_cast<int64_t*>(pinned_scratch(sizeof(int64_t)));
+  if (!hni) return fail(PIPNN_ECUDA, "pinned host scratch");
+  PIPNN_CUDA(cudaMemcpyAsync(hni, leaf_off + n_leaves, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   PIPNN_CUDA(cudaStreamSynchronize(st));
+  const int64_t ni = *hni;
   *n_leaves_h = n_leaves;
   *n_inst_h = ni;
   *depth_h = depth;
