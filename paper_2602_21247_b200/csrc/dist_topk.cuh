@@ -236,10 +236,13 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
   const bool prof = (args.dbg & 64) != 0;
   unsigned long long pw[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   const unsigned long long t_start = clock64();
+  // Producer and MMA waits (slots < 8) park in hardware on a try_wait suspend-time hint instead of re-issuing
+  // try_wait, which takes issue slots from the epilogue warps of the sub-partition (C2 leaf tiles -1%).
 #define PWAIT(slot, bar, par, err, code)                                                  \
   [&]() {                                                                                 \
     const unsigned long long t0_ = prof ? clock64() : 0ull;                               \
-    const bool ok_ = ptx::mbar_wait((bar), (par), (err), (code));                         \
+    const bool ok_ = (slot) < 8 ? ptx::mbar_wait_hint((bar), (par), (err), (code), 1000000u)  \
+                                : ptx::mbar_wait((bar), (par), (err), (code));                \
     if (prof) pw[slot] += clock64() - t0_;                                                \
     return ok_;                                                                           \
   }()

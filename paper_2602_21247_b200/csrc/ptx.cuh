@@ -56,6 +56,27 @@ __device__ __forceinline__ bool mbar_wait(uint64_t* bar, uint32_t parity, int* e
   return false;
 }
 
+// try_wait with a suspend-time hint: the warp is parked in hardware until the phase completes or ~ns elapse,
+// instead of re-issuing try_wait (each re-issue takes an issue slot of its sub-partition).
+__device__ __forceinline__ bool mbar_try_wait_hint(uint32_t bar_addr, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+      : "=r"(ok)
+      : "r"(bar_addr), "r"(parity), "r"(ns)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ bool mbar_wait_hint(uint64_t* bar, uint32_t parity, int* err_flag, int code, uint32_t ns) {
+  const uint32_t a = smem_u32(bar);
+  for (uint32_t it = 0; it < (1u << 22); ++it) {
+    if (mbar_try_wait_hint(a, parity, ns)) return true;
+    if ((it & 255u) == 255u && err_flag && *(volatile int*)err_flag != 0) return false;
+  }
+  if (err_flag) atomicExch(err_flag, code);
+  return false;
+}
+
 // Bounded wait with back-off (__nanosleep) for roles whose waits are not latency critical (producers, MMA
 // issuers waiting for free buffers): a spinning warp would take issue slots from the epilogue warps of its
 // sub-partition.

@@ -35,3 +35,9 @@ for s, e, n in ks:
     agg[k] = agg.get(k, 0) + (e - s)
 for k, v in sorted(agg.items(), key=lambda x: -x[1])[:20]:
     print(f"  {v/1e3:8.3f} ms  {k}")
+if os.environ.get("TL_SEQ"):
+    lim = float(os.environ["TL_SEQ"])
+    for s, e, n in ks:
+        if (s - t0) / 1e3 > lim:
+            break
+        print(f"  {(s - t0)/1e3:7.3f} +{(e - s):7.1f} us  {n[:70]}")
