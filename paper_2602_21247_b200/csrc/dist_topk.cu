@@ -1,4 +1,5 @@
 // dist_topk.cu — instantiations + launcher of the distance-tile / top-k kernel (dist_topk.cuh).
+#include <cstdio>
 #include <cstdlib>
 
 #include "dist_topk.cuh"
@@ -11,10 +12,18 @@ static pipnn_status launch_one(const DistTopkArgs& a0, cudaStream_t st) {
   const char* dbg_env = std::getenv("PIPNN_DEBUG_EPI");  // experiment hook (read per launch)
   a.dbg = dbg_env ? std::atoi(dbg_env) : 0;
   // threshold-pass tiles: any column subset gives a valid bound; fewer tiles trade pass-1 work for a few more
-  // pass-2 candidates (measured on C2: 3 tiles for leaves, 2 for the partition's K <= 4)
+  // pass-2 candidates (measured: 3 tiles for leaves — C2 u8, and C3/C4 float, whose leaf kernel is bound by
+  // the producer/MMA pipeline, so every pass-1 tile costs a B-tile load: C4 leaf tiles 2.70 -> 2.40 ms with 3
+  // instead of all; 2 for the partition's K <= 4)
   const char* p1_env = std::getenv(KMAX <= 4 ? "PIPNN_P1_PART" : "PIPNN_P1");
-  a.p1cap = p1_env ? std::max(1, std::atoi(p1_env)) : (KMAX <= 4 ? 2 : (U8 ? 3 : 64));
-  const DtGeom g = dt_geom(a.Kb, !U8);
+  a.p1cap = p1_env ? std::max(1, std::atoi(p1_env)) : (KMAX <= 4 ? 2 : 3);
+  const char* geo_env = std::getenv("PIPNN_GEOM");  // experiment hook: "NA,planes per chunk"
+  a.geo = 0;
+  if (geo_env) {
+    int na = 0, pc = 0;
+    if (std::sscanf(geo_env, "%d,%d", &na, &pc) == 2 && na >= 1 && na <= 2 && pc >= 2 && pc <= 14) a.geo = 16 * na + pc;
+  }
+  const DtGeom g = dt_geom(a.Kb, !U8, a.geo);
   if (g.stages < 2) return fail(PIPNN_EUNSUPPORTED, "dist_topk: row too long for the SMEM pipeline");
   auto* fn = dist_topk_kernel<U8, MIPS, KMAX>;
   PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem));

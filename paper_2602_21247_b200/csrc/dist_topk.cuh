@@ -78,6 +78,7 @@ struct DistTopkArgs {
   uint32_t* out_rowid;     // nullable: the row's id next to every output slot (same layout)
   uint32_t* out_cnt;       // nullable: out_cnt[pick id] += 1 for every valid pick (group-by histogram)
   int p1cap;               // max column tiles of the threshold pass (>= 1)
+  int geo;                 // pipeline geometry request: 0 = default (dt_geom), else 16 * NA + planes per chunk
   int dbg;                 // experiment hook (PIPNN_DEBUG_EPI): low bits 1 = epilogue skips all tile processing,
                            // 2 = skips pass 2; bit 64 = wait profile (pipnn_debug_dt_prof)
   int* err;
@@ -104,12 +105,14 @@ constexpr int kDtSmemBudget = 227 * 1024 - 1024;
 struct DtGeom {
   int KCs, KCm, KCuse, nchunks, ppc, stage_bytes, KCa, NA, stages, smem;
 };
-__host__ __device__ inline DtGeom dt_geom(int Kb, bool fold) {
+__host__ __device__ inline DtGeom dt_geom(int Kb, bool fold, int geo = 0) {
   DtGeom g;
   g.KCs = Kb / 16;
   g.KCm = fold ? g.KCs - 2 : g.KCs;
   g.KCuse = g.KCs;
-  g.nchunks = (g.KCuse + 9) / 10;  // <= 10 planes (160 B of K) per chunk: one chunk per tile up to K = 160 B
+  const int ppc_req = geo & 15, na_req = geo >> 4;
+  g.nchunks = ppc_req ? (g.KCuse + ppc_req - 1) / ppc_req
+                      : (g.KCuse + 9) / 10;  // <= 10 planes (160 B of K) per chunk: one chunk per tile up to K = 160 B
   g.ppc = ((g.KCuse + g.nchunks - 1) / g.nchunks + 1) & ~1;
   g.stage_bytes = g.ppc * 2048;
   g.KCa = g.KCm;
@@ -117,6 +120,7 @@ __host__ __device__ inline DtGeom dt_geom(int Kb, bool fold) {
   // 2 A slots per warpgroup (the next item's A block loads while the current item runs) when that still
   // leaves room for 4 B stages, else 1
   g.NA = 2 * 2 * g.KCa * 2048 + rest + 4 * g.stage_bytes <= kDtSmemBudget ? 2 : 1;
+  if (na_req) g.NA = na_req;
   const int fixed = 2 * g.NA * g.KCa * 2048 + rest;
   g.stages = (kDtSmemBudget - fixed) / g.stage_bytes;
   if (g.stages > kDtMaxStages) g.stages = kDtMaxStages;
@@ -185,7 +189,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const DtGeom GM = dt_geom(args.Kb, kFold);
+  const DtGeom GM = dt_geom(args.Kb, kFold, args.geo);
   const int KCs = GM.KCs;                // planes per 128-row block of the tiled buffers (block stride)
   const int KCm = GM.KCm;                // planes of the coordinates themselves
   const int KCu = GM.KCuse;              // planes multiplied per tile (incl. the augment step when folded)

@@ -1,6 +1,6 @@
 """Leaf-kernel experiment: time pipnn_leaf_pick on the C2 leaves for each PIPNN_DEBUG_EPI value given on the
-command line (default 0 1 2 0). Bits 0-3: 1 = epilogue skips all tile processing, 2 = skips pass 2; bit 16 / 32:
-suspend-hint waits for producer+MMA / epilogue."""
+command line (default 0 1 2 0). Bits 0-3: 1 = epilogue skips all tile processing, 2 = skips pass 2;
+bit 64: wait profile. CFG=C3|C4|... selects the config (L2 metric)."""
 import os, sys, numpy as np, torch
 sys.path.insert(0, '/root/repo')
 import synth
