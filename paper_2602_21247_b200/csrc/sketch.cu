@@ -27,14 +27,27 @@ __device__ __forceinline__ int32_t dp4a_su(uint32_t h_s8x4, uint32_t x_u8x4, int
   return r;
 }
 
+// Float paths: H as fp64 in SMEM, [dp][MP] (MP = m rounded up to even): the m weights of coordinate j are
+// read as broadcast 16-B pairs (no int8 -> fp64 conversion per multiply-add).
+__host__ __device__ __forceinline__ int sketch_mp(int m) { return (m + 1) & ~1; }
+
 template <int SRC>  // 0: uint8, 1: float32, 2: bf16 (kDtypeBf16)
 __global__ void __launch_bounds__(128) sketch_kernel(const void* __restrict__ Xv, int64_t n, int d, int64_t ld, int m,
                                                      const int8_t* __restrict__ Hg, void* __restrict__ S) {
-  extern __shared__ __align__(16) int8_t Hs[];  // [m][dp] with dp = round_up(d, 16), zero padded
+  extern __shared__ __align__(16) int8_t Hs[];  // uint8: [m][dp] int8 with dp = round_up(d, 16), zero padded
+  double* Hd = reinterpret_cast<double*>(Hs);   // float: [dp][MP] fp64, zero padded
   const int dp = (d + 15) & ~15;
-  for (int e = threadIdx.x; e < m * dp; e += blockDim.x) {
-    const int i = e / dp, j = e - i * dp;
-    Hs[e] = j < d ? Hg[i * d + j] : (int8_t)0;
+  const int MP = sketch_mp(m);
+  if (SRC == 0) {
+    for (int e = threadIdx.x; e < m * dp; e += blockDim.x) {
+      const int i = e / dp, j = e - i * dp;
+      Hs[e] = j < d ? Hg[i * d + j] : (int8_t)0;
+    }
+  } else {
+    for (int e = threadIdx.x; e < dp * MP; e += blockDim.x) {
+      const int j = e / MP, i = e - j * MP;
+      Hd[e] = (i < m && j < d) ? (double)Hg[i * d + j] : 0.0;
+    }
   }
   __syncthreads();
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -91,9 +104,14 @@ __global__ void __launch_bounds__(128) sketch_kernel(const void* __restrict__ Xv
         for (int t = 0; t < 8; ++t) {
           if (j0 + t < d) {
             const double v = (double)__uint_as_float(((w[t >> 1] >> (16 * (t & 1))) & 0xFFFFu) << 16);
+            const double2* h2 = reinterpret_cast<const double2*>(Hd + (j0 + t) * MP);
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (i < m) acc[i] += (double)Hs[i * dp + j0 + t] * v;
+            for (int i = 0; i < 16; i += 2)
+              if (i < m) {
+                const double2 h = h2[i >> 1];
+                acc[i] += h.x * v;
+                acc[i + 1] += h.y * v;  // (i + 1 == MP - 1 > m - 1: a zero weight into an unused accumulator)
+              }
           }
         }
       }
@@ -112,9 +130,14 @@ __global__ void __launch_bounds__(128) sketch_kernel(const void* __restrict__ Xv
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const double v = (double)__uint_as_float((uint32_t)f32_to_bf16_rne(f[t]) << 16);
+        const double2* h2 = reinterpret_cast<const double2*>(Hd + (j0 + t) * MP);
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (i < m) acc[i] += (double)Hs[i * dp + j0 + t] * v;
+        for (int i = 0; i < 16; i += 2)
+          if (i < m) {
+            const double2 h = h2[i >> 1];
+            acc[i] += h.x * v;
+            acc[i + 1] += h.y * v;
+          }
       }
     }
     }
@@ -179,7 +202,9 @@ pipnn_status sketch_impl(const pipnn_points* X, int m, uint64_t seed, void* sket
   const int64_t md = (int64_t)m * X->d;
   hyperplane_kernel<<<(unsigned)ceil_div(md, 256), 256, 0, c.st>>>(m, X->d, seed, H);
   PIPNN_LAUNCHED("hyperplane_kernel", c.st);
-  const int smem = (int)((int64_t)m * ((X->d + 15) & ~15));
+  const int64_t dp = (X->d + 15) & ~15;
+  const int smem = (int)(X->dtype == PIPNN_U8 ? (int64_t)m * dp : dp * sketch_mp(m) * (int64_t)sizeof(double));
+  if (smem > 227 * 1024) return fail(PIPNN_EUNSUPPORTED, "sketch: d too large for the SMEM hyperplane table");
 #define SK_LAUNCH(SRC)                                                                                             \
   do {                                                                                                             \
     if (smem > 48 * 1024)                                                                                          \
