@@ -373,11 +373,14 @@ __device__ __forceinline__ void ldsm_x4_s(uint32_t (&r)[4], uint32_t saddr) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(saddr));
 }
+// No "memory" clobber: a clobber in the staging loops makes the compiler reload every kernel parameter per
+// copy (the C4 warp tier spent a third of its instructions there). Ordering against the tile's other SMEM
+// accesses comes from cp_async_fence() before a staging loop and cp_async_wait_all() after it.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src), "r"(src_bytes)
-               : "memory");
+               "l"(src), "r"(src_bytes));
 }
+__device__ __forceinline__ void cp_async_fence() { asm volatile("" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
@@ -422,6 +425,7 @@ __device__ __forceinline__ void gp_stage(const void* __restrict__ Xv, int64_t ld
     // rows of ld bytes, or the bf16 copy's rows of ld elements (zero padded, ld a multiple of 8)
     const int64_t rb = U8 ? ld : 2 * ld;
     const int lim = U8 ? d : (int)(2 * ld);
+    cp_async_fence();
     if (act)
       for (int r = rr; r < nrp; r += rpp) {
         const bool on = r < nr && cb < lim;
@@ -699,6 +703,7 @@ __device__ __forceinline__ void gp_stage_group(const void* __restrict__ Xv, int6
   if ((U8 && fast) || (!U8 && src_bf16)) {
     const int64_t rb = U8 ? ld : 2 * ld;
     const int lim = U8 ? d : (int)(2 * ld);
+    cp_async_fence();
     if (act)
       for (int r = rr; r < nrp; r += rpp) {
         const bool on = r < nr && cb < lim;
@@ -1004,16 +1009,21 @@ __global__ void __launch_bounds__(256, 3) fp_warp_kernel(const void* __restrict_
     if (fast) {
       const uint32_t dst0 = (uint32_t)__cvta_generic_to_shared(rows + (size_t)rr * WL.pitch + ch * 16);
       const uint32_t dstep = (uint32_t)(rpp * WL.pitch);
-      const uint8_t* src0 = (const uint8_t*)Xv + ch * 16;
       const bool col_on = act_stage && ch * 16 < lim;
+      // the lane's source base: its chunk, or (chunk beyond the row) the row start with a zero-byte copy;
+      // rows >= nr read id 0 (lanes > c hold 0) with a zero-byte copy, so every address is a valid row
+      const uint8_t* src0 = (const uint8_t*)Xv + (col_on ? ch * 16 : 0);
+      uint32_t rb32;  // row stride < 2^32 B; rid * rb32 widened in one IMAD (opaque: kept in a register, not
+                      // re-derived from the kernel parameters in every iteration)
+      asm("mov.b32 %0, %1;" : "=r"(rb32) : "r"((uint32_t)rowbytes));
       uint32_t dst = dst0;
+      cp_async_fence();
       for (int r = rr; r - rr < nrp; r += rpp, dst += dstep) {
         const uint32_t rid = __shfl_sync(0xffffffffu, my_id, r & 31);
         if (act_stage && r < nrp) {
-          const bool on = col_on && r < nr;
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst),
-                       "l"(src0 + (on ? (int64_t)rid * rowbytes : 0)), "r"(on ? 16u : 0u)
-                       : "memory");
+          const uint8_t* src = src0 + (uint64_t)rid * rb32;
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+                       "r"(col_on && r < nr ? 16u : 0u));
         }
       }
     } else {
@@ -1226,8 +1236,8 @@ __host__ __device__ inline BandLayout band_layout(int d, bool u8, int CP) {
   o += (size_t)CP * 4;
   L.ids_off = o;  // [2][CP]
   o += (size_t)2 * CP * 4;
-  L.perm_off = o;
-  o += (size_t)CP * 4;
+  L.perm_off = o;  // [2][CP]
+  o += (size_t)2 * CP * 4;
   L.bytes = (o + 127) & ~(size_t)127;
   return L;
 }
@@ -1266,7 +1276,7 @@ __global__ void __launch_bounds__(2 * CP + 32, CP <= 64 ? 4 : (CP <= 128 ? 2 : 1
   DT* g0 = (DT*)(bsm + BL.g0_off);
   DT* thr = (DT*)(bsm + BL.thr_off);
   uint32_t* idsb = (uint32_t*)(bsm + BL.ids_off);
-  uint32_t* perm = (uint32_t*)(bsm + BL.perm_off);
+  uint32_t* permb = (uint32_t*)(bsm + BL.perm_off);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t n_iter = list ? (int64_t)*list_n : n;
   int p = 0;  // points handed over so far (buffer = p & 1)
@@ -1298,6 +1308,7 @@ __global__ void __launch_bounds__(2 * CP + 32, CP <= 64 ? 4 : (CP <= 128 ? 2 : 1
       uint32_t* ids = idsb + bsel * CP;
       uint32_t* M = Mb + bsel * CP * W;
       uint64_t* skey = skeyb + bsel * CP;
+      uint32_t* perm = permb + bsel * CP;
       if (p >= 2) named_sync(kBarFree + bsel, NB_T + 32);  // the scan of point p-2 released this buffer
       const uint64_t* res = slots + u * (int64_t)l_max;
       const int nr = c + 1, nrp = (nr + 15) & ~15;
@@ -1417,8 +1428,16 @@ __global__ void __launch_bounds__(2 * CP + 32, CP <= 64 ? 4 : (CP <= 128 ? 2 : 1
           }
         }
       }
+      // ---- rank of every candidate in the (D(u,.), id) order (keys are distinct: ids are), a thread per
+      // candidate (done here, in parallel, rather than in the scan warp, which bounds the tier)
+      for (int y = tid + 1; y <= c; y += NB_T) {
+        const uint64_t ky = skey[y];
+        int rank = 0;
+        for (int z = 1; z <= c; ++z) rank += skey[z] < ky ? 1 : 0;
+        perm[rank] = (uint32_t)y;
+      }
       __threadfence_block();
-      named_arrive(kBarReady + bsel, NB_T + 32);  // ids, keys and M of point p are complete
+      named_arrive(kBarReady + bsel, NB_T + 32);  // ids, keys, M and the ranks of point p are complete
       ++p;
     }
   } else {
@@ -1430,16 +1449,8 @@ __global__ void __launch_bounds__(2 * CP + 32, CP <= 64 ? 4 : (CP <= 128 ? 2 : 1
       const int bsel = p & 1;
       const uint32_t* ids = idsb + bsel * CP;
       const uint32_t* M = Mb + bsel * CP * W;
-      const uint64_t* skey = skeyb + bsel * CP;
+      const uint32_t* perm = permb + bsel * CP;
       named_sync(kBarReady + bsel, NB_T + 32);
-      // ---- rank of every candidate in the (D(u,.), id) order (keys are distinct: ids are)
-      for (int y = lane + 1; y <= c; y += 32) {
-        const uint64_t ky = skey[y];
-        int rank = 0;
-        for (int z = 1; z <= c; ++z) rank += skey[z] < ky ? 1 : 0;
-        perm[rank] = (uint32_t)y;
-      }
-      __syncwarp();
       // ---- lazy scan, 32 candidates per step
       uint32_t* out = nbr_tmp + u * (int64_t)R;
       uint32_t A[W];
@@ -1461,10 +1472,17 @@ __global__ void __launch_bounds__(2 * CP + 32, CP <= 64 ? 4 : (CP <= 128 ? 2 : 1
           if (k < lane && inb && ((Mi[ik >> 5] >> (ik & 31)) & 1u)) intra |= 1u << k;
         }
         const uint32_t cand = __ballot_sync(0xffffffffu, inb && !hitA);
-        uint32_t adm = 0u;
-        for (int k = 0; k < 32; ++k) {
-          const uint32_t ik_intra = __shfl_sync(0xffffffffu, intra, k);
-          if (((cand >> k) & 1u) && (ik_intra & adm) == 0u) adm |= 1u << k;
+        // the batch's sequential scan (admit k unless an admitted earlier candidate prunes it) as a fixpoint
+        // over ballots: a lane is admitted once all its in-batch pruners are rejected, rejected once one is
+        // admitted; the earliest undecided lane always decides, typically 2-4 rounds instead of 32 steps
+        uint32_t adm = 0u, rej = ~cand;
+        while ((adm | rej) != 0xFFFFFFFFu) {
+          const bool undecided = !(((adm | rej) >> lane) & 1u);
+          const bool hit = (intra & adm) != 0u, open = (intra & ~rej) != 0u;
+          const uint32_t a = __ballot_sync(0xffffffffu, undecided && !hit && !open);
+          const uint32_t r = __ballot_sync(0xffffffffu, undecided && hit);
+          adm |= a;
+          rej |= r;
         }
         const bool me = (adm >> lane) & 1u;
         const int pos = na + __popc(adm & ((1u << lane) - 1u));
