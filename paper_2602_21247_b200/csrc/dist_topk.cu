@@ -17,6 +17,8 @@ static pipnn_status launch_one(const DistTopkArgs& a0, cudaStream_t st) {
   // instead of all; 2 for the partition's K <= 4)
   const char* p1_env = std::getenv(KMAX <= 4 ? "PIPNN_P1_PART" : "PIPNN_P1");
   a.p1cap = p1_env ? std::max(1, std::atoi(p1_env)) : (KMAX <= 4 ? 2 : 3);
+  if (a.packed && !(KMAX == 2 && U8)) return fail(PIPNN_EUNSUPPORTED, "dist_topk: packed pass needs uint8, K <= 2");
+  if (a.packed) a.p1cap = 0;  // no threshold pass
   const char* geo_env = std::getenv("PIPNN_GEOM");  // experiment hook: "NA,planes per chunk"
   a.geo = 0;
   if (geo_env) {

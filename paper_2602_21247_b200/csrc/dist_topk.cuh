@@ -79,6 +79,8 @@ struct DistTopkArgs {
   uint32_t* out_cnt;       // nullable: out_cnt[pick id] += 1 for every valid pick (group-by histogram)
   int p1cap;               // max column tiles of the threshold pass (>= 1)
   int geo;                 // pipeline geometry request: 0 = default (dt_geom), else 16 * NA + planes per chunk
+  int packed;              // uint8, K <= 2, no self exclusion (the partition): nb holds 32 ||y||^2 + (pos mod 32)
+                           // and every tile goes through one packed pass (no threshold pass)
   int dbg;                 // experiment hook (PIPNN_DEBUG_EPI): low bits 1 = epilogue skips all tile processing,
                            // 2 = skips pass 2; bit 64 = wait profile (pipnn_debug_dt_prof)
   int* err;
@@ -417,6 +419,10 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
         int qlen = 0;
         const int diag_chunk = S.self ? (r0 + q * 32) : -1;  // column base of this warp's diagonal chunk
         const bool direct = KMAX <= 4 && dt_direct(K, ncols, S.self);
+        // packed single pass (KMAX == 2, uint8): q_j = 32 key_j + (j mod 32) = nbp_j - 64 v_j is one IMAD and
+        // orders the chunk's columns by (key, column) exactly (|32 key| < 2^30 for d <= 512); the chunk's two
+        // smallest by a min/max network on column pairs, then inserted into the row's list
+        const bool packedm = KMAX == 2 && U8 && args.packed;
         const int P1 = dt_p1(K, ncols, S.self, args.p1cap);  // tiles of pass 1 (none: direct single pass)
         for (int t2 = 0; t2 < P1 + T; ++t2, ++tcount) {
           const bool pass2 = t2 >= P1;
@@ -432,6 +438,43 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
             if (!U8) U = (KT)nextafterf((float)U, __int_as_float(0x7F800000));
           }
           if ((args.dbg & 15) == 1 || ((args.dbg & 15) == 2 && pass2)) {
+          } else if (packedm) {
+            for (int j0 = 0; j0 < Nt; j0 += 32) {
+              const int col0 = c0 + j0;
+              int4 nb4[8];
+              const int4* p4 = reinterpret_cast<const int4*>((const int32_t*)args.nb + S.b.pos + col0);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) nb4[u] = __ldg(p4 + u);
+              uint32_t v[32];
+              ptx::tmem_ld32(taddr + j0, v);
+              ptx::tmem_ld_wait();
+              int32_t qv[32];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                qv[4 * u + 0] = nb4[u].x - 64 * (int32_t)v[4 * u + 0];
+                qv[4 * u + 1] = nb4[u].y - 64 * (int32_t)v[4 * u + 1];
+                qv[4 * u + 2] = nb4[u].z - 64 * (int32_t)v[4 * u + 2];
+                qv[4 * u + 3] = nb4[u].w - 64 * (int32_t)v[4 * u + 3];
+              }
+              int32_t m1 = 0x7FFFFFFF, m2 = 0x7FFFFFFF;
+              if (K == 1) {
+#pragma unroll
+                for (int jj = 0; jj < 32; jj += 2) m1 = min(m1, min(qv[jj], qv[jj + 1]));
+              } else {
+#pragma unroll
+                for (int jj = 0; jj < 32; jj += 2) {
+                  const int32_t a = min(qv[jj], qv[jj + 1]), b = max(qv[jj], qv[jj + 1]);
+                  const int32_t t = max(m1, a);
+                  m1 = min(m1, a);
+                  m2 = min(min(t, m2), b);  // second smallest of {m1, m2} u {a, b}
+                }
+              }
+              // decode (key = q >> 5, exact: arithmetic shift) and insert; columns grow with the chunks, so
+              // the strict insertion keeps the earlier column on equal keys
+              const int32_t k1 = m1 >> 5, k2 = m2 >> 5;
+              if (k1 < kk[KMAX - 1]) topk_insert<KT, KMAX>(kk, ii, (KT)k1, (uint32_t)(col0 + (m1 & 31)));
+              if (K == 2 && k2 < kk[KMAX - 1]) topk_insert<KT, KMAX>(kk, ii, (KT)k2, (uint32_t)(col0 + (m2 & 31)));
+            }
           } else if (direct) {
             // ---- direct single pass (one chunk of <= 32 columns, K <= 4): every key through the insertion
             // network (columns ascending, strict: ties keep the smaller column)

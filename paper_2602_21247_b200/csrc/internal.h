@@ -26,7 +26,8 @@ pipnn_status validate_points(const pipnn_points* X);
 // 128-row block) work item; padding rows are zero. max_items bounds the grid.
 pipnn_status gather_tiled(const pipnn_points* X, const uint32_t* ids, const TileSeg* segs, const WorkItem* items,
                           const int64_t* n_items, int64_t max_items, uint8_t* T, void* nrm, const Ctx& c,
-                          int Kb = 0 /* 0: tiled_row_bytes(X) */);
+                          int Kb = 0 /* 0: tiled_row_bytes(X) */,
+                          int packed = 0 /* u8: norms as 32 ||y||^2 + (position mod 32), see DistTopkArgs::packed */);
 
 // Build TileSegs/items for CSR segments (off[0..ns]) with pad = round_up(rows, 128): writes segs
 // (DistSeg with a == b, self = 1, out_row = off[s], k) and the (segment, row-block) items.

@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(128) gather_tiled_kernel(const void* __restric
                                                            const TileSeg* __restrict__ segs,
                                                            const WorkItem* __restrict__ items,
                                                            const int64_t* __restrict__ n_items, uint8_t* __restrict__ T,
-                                                           void* __restrict__ nrm, int* err) {
+                                                           void* __restrict__ nrm, int* err, int packed) {
   constexpr bool U8 = SRC == 0;
   if ((int64_t)blockIdx.x >= *n_items) return;
   const WorkItem w = items[blockIdx.x];
@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(128) gather_tiled_kernel(const void* __restric
   }
   if (bad) atomicExch(err, DERR_NONFINITE);
   if (U8) {
-    ((int32_t*)nrm)[S.pos + local] = valid ? ni : kPadNormU8;
+    // packed (the partition's K <= 2 single pass, dist_topk.cuh): 32 ||y||^2 + (position mod 32)
+    ((int32_t*)nrm)[S.pos + local] = valid ? (packed ? 32 * ni + ((S.pos + local) & 31) : ni) : kPadNormU8;
   } else {
     ((float*)nrm)[S.pos + local] = nf;
     const float t = valid ? (mips ? 0.0f : -0.5f * nf) : -kPadKey;
@@ -115,13 +116,14 @@ __global__ void __launch_bounds__(128) gather_tiled_kernel(const void* __restric
 }
 
 pipnn_status gather_tiled(const pipnn_points* X, const uint32_t* ids, const TileSeg* segs, const WorkItem* items,
-                          const int64_t* n_items, int64_t max_items, uint8_t* T, void* nrm, const Ctx& c, int Kb) {
+                          const int64_t* n_items, int64_t max_items, uint8_t* T, void* nrm, const Ctx& c, int Kb,
+                          int packed) {
   if (max_items <= 0) return PIPNN_OK;
   if (Kb <= 0) Kb = tiled_row_bytes(X);
   const int64_t ld = X->ld;
 #define GT_LAUNCH(SRC)                                                                                             \
   gather_tiled_kernel<SRC><<<(unsigned)max_items, 128, 0, c.st>>>(X->data, ld, X->d, Kb, X->metric == PIPNN_MIPS,   \
-                                                                  ids, segs, items, n_items, T, nrm, c.err)
+                                                                  ids, segs, items, n_items, T, nrm, c.err, packed)
   if (X->dtype == PIPNN_U8) GT_LAUNCH(0);
   else if (X->dtype == kDtypeBf16) GT_LAUNCH(2);
   else GT_LAUNCH(1);

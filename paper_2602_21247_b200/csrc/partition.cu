@@ -567,7 +567,10 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     PIPNN_CUDA(g_pin_level.copy(n_it, nits, 2 * sizeof(int64_t), st));
     const double t_plan2 = dbg_timing ? wall() : 0.0;
     PIPNN_TRY(gather_tiled(X, mem, tsA, itA, n_it, nItA, TA, nA, c));
-    PIPNN_TRY(gather_tiled(X, lead_sorted, tsB, itB, n_it + 1, nItB, TB, nB, c));
+    // uint8 with fanout <= 2 at this level: leader norms in the packed form of the single-pass top-2
+    static const bool no_packed = std::getenv("PIPNN_NO_PACKED") != nullptr;  // experiment hook
+    const int packed = X->dtype == PIPNN_U8 && fmax_l <= 2 && !no_packed ? 1 : 0;
+    PIPNN_TRY(gather_tiled(X, lead_sorted, tsB, itB, n_it + 1, nItB, TB, nB, c, 0, packed));
     const double t_gather = dbg_timing ? wall() : 0.0;
     PIPNN_CUDA(cudaMemsetAsync(ccnt, 0, C * sizeof(uint32_t), st));
     DistTopkArgs da{};
@@ -585,6 +588,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     da.row_ids = mem;    // member ids
     da.out_rowid = cv2;
     da.out_cnt = ccnt;
+    da.packed = packed;
     da.err = c.err;
     PIPNN_TRY(launch_dist_topk(da, X->dtype == PIPNN_U8, X->metric == PIPNN_MIPS, fmax_l, st));
     const double t_dist = dbg_timing ? wall() : 0.0;
