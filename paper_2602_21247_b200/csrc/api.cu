@@ -3,6 +3,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -120,6 +121,22 @@ static BuildPlan plan_of(const pipnn_points* X, const pipnn_build_params* p) {
   return b;
 }
 
+// Timing event i of the calling thread on the current device, created on first use and reused by every later
+// build (creating and destroying the stage events per build cost tens of microseconds of host time at the
+// start of each build, with the GPU idle).
+cudaEvent_t pool_event(size_t i) {
+  static thread_local std::map<int, std::vector<cudaEvent_t>> pools;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::vector<cudaEvent_t>& pool = pools[dev];
+  while (pool.size() <= i) {
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    pool.push_back(e);
+  }
+  return pool[i];
+}
+
 // Runs the whole build through an Arena; with a measuring Arena it only sizes the workspace.
 uint8_t* pinned_scratch(size_t bytes) {
   struct Scratch {
@@ -174,19 +191,12 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   cudaEvent_t ev[7];
   if (!ar.measuring()) {
     if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small");
-    for (auto& e : ev) PIPNN_CUDA(cudaEventCreate(&e));
+    for (int i = 0; i < 7; ++i)
+      if (!(ev[i] = pool_event(i))) return fail(PIPNN_ECUDA, "timing event");
     PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
     PIPNN_CUDA(cudaEventRecord(ev[0], st));
   }
-  auto cleanup = [&]() {
-    if (!ar.measuring())
-      for (auto& e : ev) cudaEventDestroy(e);
-    for (auto& pr : tile_ev) {
-      cudaEventDestroy(pr.first);
-      cudaEventDestroy(pr.second);
-    }
-    tile_ev.clear();
-  };
+  auto cleanup = [&]() { tile_ev.clear(); };  // (pooled events: nothing to destroy)
   // (a0) bf16 copy (float data) and sketches
   if (is_float && !ar.measuring()) {
     pipnn_status s0 = to_bf16(X, Xb, ldb, c);

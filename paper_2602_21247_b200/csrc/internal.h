@@ -72,6 +72,7 @@ bool subtree_fits(const pipnn_points* X, const pipnn_partition_params* p, int64_
 // Pinned host scratch for small device -> host reads (thread-local, grows as needed; callers copy into it
 // with cudaMemcpyAsync, synchronise the stream, then read it — nothing stays pending across calls).
 uint8_t* pinned_scratch(size_t bytes);
+cudaEvent_t pool_event(size_t i);  // per-thread, per-device reusable timing event i (api.cu)
 // Batched beam search (search.cu, Alg. 1): one warp per query; L <= 256.
 size_t search_smem_per_warp(const pipnn_points* X);
 pipnn_status search_impl(const pipnn_points* X, const uint64_t* row_ptr, const uint32_t* col_idx, const void* Q,

@@ -223,8 +223,9 @@ pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, cons
   a.err = c.err;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c.tile_events) {
-    PIPNN_CUDA(cudaEventCreate(&e0));
-    PIPNN_CUDA(cudaEventCreate(&e1));
+    e0 = pool_event(7 + 2 * c.tile_events->size());
+    e1 = pool_event(8 + 2 * c.tile_events->size());
+    if (!e0 || !e1) return fail(PIPNN_ECUDA, "timing event");
     PIPNN_CUDA(cudaEventRecord(e0, c.st));
   }
   PIPNN_TRY(launch_dist_topk(a, X->dtype == PIPNN_U8, X->metric == PIPNN_MIPS, k, c.st));
