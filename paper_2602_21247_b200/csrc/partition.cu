@@ -22,6 +22,7 @@
 #include <chrono>
 #include <cstdlib>
 #include <cub/cub.cuh>
+#include <map>
 #include <vector>
 
 #include "internal.h"
@@ -220,6 +221,19 @@ struct PinnedArena {
   void reset() { used = 0; }
 };
 static thread_local PinnedArena g_pin_level, g_pin_jobs;
+
+// The level synchronisation's event (per thread and device, created once; no timing).
+static cudaEvent_t level_sync_event() {
+  static thread_local std::map<int, cudaEvent_t> evs;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  auto it = evs.find(dev);
+  if (it != evs.end()) return it->second;
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  evs[dev] = e;
+  return e;
+}
 
 // ------------------------------------------------------------------ host helpers
 static int64_t leaders_of(int64_t sz, const pipnn_partition_params* p) {
@@ -449,6 +463,23 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     return e && e[0] == '1';
   }();
   auto wall = [] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  // Device subtrees of level L run after level L + 1's kernels and read-back are enqueued: the host waits on an
+  // event behind the read-back, so the subtree kernel overlaps the host's planning of level L + 1. Stream order
+  // keeps their member buffer intact (level L + 1 writes the other buffer; level L + 2 is enqueued after it).
+  struct PendingSubtree {
+    bool on = false;
+    int ng = 0;
+    const uint32_t* mem = nullptr;
+  } pend;
+  auto launch_pending = [&]() -> pipnn_status {
+    if (!pend.on) return PIPNN_OK;
+    pend.on = false;
+    PIPNN_CUDA(cudaMemsetAsync(dev_work, 0, sizeof(int), st));
+    return subtree_launch(X, p, dev_groups, pend.ng, pend.mem, staging, 2 * cp.L, dev_ctr + 1, dev_leaf_dst,
+                          dev_leaf_size, cp.leaves, dev_ctr, dev_work, c.err, dev_work + 1, st);
+  };
+  cudaEvent_t ev_sync = level_sync_event();
+  if (!ev_sync) return fail(PIPNN_ECUDA, "partition: sync event");
   while (!open.empty()) {
     const int G = (int)open.size();
     if (G > cp.G) return fail(PIPNN_ECAPACITY, "partition: open-group capacity");
@@ -602,8 +633,10 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     PIPNN_CUDA(cudaMemcpyAsync(hbuf, ccnt, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     PIPNN_CUDA(cudaMemcpyAsync(hbuf + C, lead_sorted, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     PIPNN_CUDA(cudaMemcpyAsync(hbuf + 2 * C, d_redo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PIPNN_CUDA(cudaEventRecord(ev_sync, st));
+    PIPNN_TRY(launch_pending());  // the previous level's device subtrees (see PendingSubtree)
     if (dbg_timing) t_sync0 = wall();
-    PIPNN_CUDA(cudaStreamSynchronize(st));
+    PIPNN_CUDA(cudaEventSynchronize(ev_sync));
     if (dbg_timing) t_sync1 = wall();
     std::vector<uint32_t> hccnt(hbuf, hbuf + C), hlead(hbuf + C, hbuf + 2 * C);
     const int hredo = (int)hbuf[2 * C];
@@ -691,9 +724,9 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
         std::stable_sort(dg.begin(), dg.end(), [](const DevGroup& a, const DevGroup& b) { return a.size > b.size; });
         // the members live in `nxt`, which the level after next overwrites: stream order runs this first
         PIPNN_CUDA(g_pin_jobs.copy(dev_groups, dg.data(), dg.size() * sizeof(DevGroup), st));
-        PIPNN_CUDA(cudaMemsetAsync(dev_work, 0, sizeof(int), st));
-        PIPNN_TRY(subtree_launch(X, p, dev_groups, (int)dg.size(), nxt, staging, 2 * cp.L, dev_ctr + 1,
-                                 dev_leaf_dst, dev_leaf_size, cp.leaves, dev_ctr, dev_work, c.err, dev_work + 1, st));
+        pend.on = true;  // launched behind the next level's read-back (or after the loop)
+        pend.ng = (int)dg.size();
+        pend.mem = nxt;
         next.swap(keep);
       }
     }
@@ -706,6 +739,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     std::swap(mem, nxt);
     ++depth;
   }
+  PIPNN_TRY(launch_pending());
   // ---- leaves carved on the device follow the host's leaves
   g_pin_level.reset();
   PIPNN_CUDA(g_pin_level.copy(leaf_dst, h_leaf_dst.data(), n_leaves * sizeof(int64_t), st));
