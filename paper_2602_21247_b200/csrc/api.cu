@@ -184,6 +184,7 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
     Xbv.dtype = kDtypeBf16;
   }
   const pipnn_points* XS = is_float ? &Xbv : X;  // the rows the stages read
+  int8_t* H = ar.take<int8_t>((size_t)p->hp.m * X->d);  // sketch hyperplanes (kept: the sketch runs late)
   const size_t mark = ar.mark();
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tile_ev;
   int64_t leaf_pairs = 0;
@@ -197,20 +198,24 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
     PIPNN_CUDA(cudaEventRecord(ev[0], st));
   }
   auto cleanup = [&]() { tile_ev.clear(); };  // (pooled events: nothing to destroy)
-  // (a0) bf16 copy (float data) and sketches
+  // (a0) bf16 copy (float data); sketches below
   if (is_float && !ar.measuring()) {
     pipnn_status s0 = to_bf16(X, Xb, ldb, c);
     if (s0 != PIPNN_OK) { cleanup(); return s0; }
   }
-  pipnn_status s = sketch_impl(XS, p->hp.m, p->hp.seed, sketch, ar, c);
-  if (s != PIPNN_OK) { cleanup(); return s; }
-  ar.release(mark);
+  // the sketches are needed only by HashPrune: they are enqueued behind the partition's first read-back and
+  // run while the host plans that level (or right after the partition if it has no level); H stays reserved
+  pipnn_status s = PIPNN_OK;
   if (!ar.measuring()) cudaEventRecord(ev[1], st);
+  std::function<pipnn_status()> sketch_work = [&, H]() { return sketch_launch(XS, p->hp.m, p->hp.seed, sketch, H, c); };
+  Ctx cp_ctx = c;
+  if (!ar.measuring()) cp_ctx.side_work = &sketch_work;
   // (a1, a2) partition (Alg. 5)
   int64_t n_leaves = 0, n_inst = 0;
   int depth = 0;
   s = partition_impl(XS, &p->part, leaf_off, bp.leaf_off_cap, leaf_ids, bp.leaf_ids_cap, &n_leaves, &n_inst, &depth,
-                     ar, c);
+                     ar, cp_ctx);
+  if (s == PIPNN_OK && !ar.measuring() && sketch_work) s = sketch_work();
   if (s != PIPNN_OK) { cleanup(); return s; }
   ar.release(mark);
   if (ar.measuring()) n_inst = bp.leaf_ids_cap;  // size the later stages at their upper bounds

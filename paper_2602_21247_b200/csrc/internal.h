@@ -1,6 +1,7 @@
 // internal.h — host-side declarations shared by the libpipnn translation units (not the ABI).
 #pragma once
 #include <cstdint>
+#include <functional>
 #include <utility>
 #include <vector>
 #include <cuda_runtime.h>
@@ -14,6 +15,9 @@ struct Ctx {
   int* err;  // device error flag (DevErr)
   // optional: event pairs recorded around every distance-tile kernel of the leaf stage (stats)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>>* tile_events = nullptr;
+  // optional: independent work that the partition enqueues behind its first level's read-back, so it fills
+  // the GPU while the host plans that level (pipnn_build: the sketches); run by the caller if not taken
+  std::function<pipnn_status()>* side_work = nullptr;
 };
 
 // Bytes per row of the tiled (K-major, SWIZZLE_NONE) layout: uint8 -> round_up(d, 32);
@@ -44,6 +48,8 @@ pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, cons
 // fp32 -> bf16 copy of float points (kDtypeBf16 rows of ldb = round_up(d, 8) elements).
 pipnn_status to_bf16(const pipnn_points* X, uint16_t* Xb, int ldb, const Ctx& c);
 pipnn_status sketch_impl(const pipnn_points* X, int m, uint64_t seed, void* sketch, Arena& ar, const Ctx& c);
+// The same with the hyperplane buffer H (m x d int8) given: hyperplanes + sketches, enqueued on c.st.
+pipnn_status sketch_launch(const pipnn_points* X, int m, uint64_t seed, void* sketch, int8_t* H, const Ctx& c);
 
 pipnn_status hashprune_impl(int m, int l_max, int64_t n, const void* sketch, bool sk_int, uint64_t* slots,
                             uint32_t* count, const uint32_t* owner, const uint32_t* cand, const float* dist,

@@ -19,6 +19,7 @@
 //      (b) the next level's subproblems (children larger than C_max, key mix(K_g, l + 1)).
 // At the end, leaf sizes -> exclusive scan -> leaf_off, and the staged leaves are compacted into leaf_ids.
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdlib>
 #include <cub/cub.cuh>
@@ -325,6 +326,31 @@ static int bits_for(int64_t v) {
   return b;
 }
 
+// CUB temporary bytes of every sort/scan of the partition at these capacities. The size queries cost tens of
+// microseconds of host time at the start of each build (GPU idle), so they are cached per thread.
+static size_t partition_cub_bytes(const PartCaps& cp) {
+  static thread_local std::map<std::array<int64_t, 4>, size_t> cache;
+  const std::array<int64_t, 4> key{cp.L, cp.G, cp.C, cp.leaves};
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+  cub::DeviceSegmentedSort::SortPairs(nullptr, t1, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                      (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)std::min<int64_t>(cp.L, INT32_MAX),
+                                      (int)cp.G, (const int64_t*)nullptr, (const int64_t*)nullptr);
+  cub::DeviceSegmentedSort::SortKeys(nullptr, t2, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)cp.C, (int)cp.G,
+                                     (const int64_t*)nullptr, (const int64_t*)nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, t3, (const uint32_t*)nullptr, (uint32_t*)nullptr, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (int)std::min<int64_t>(cp.L, INT32_MAX));
+  cub::DeviceScan::ExclusiveSum(nullptr, t4, (const int64_t*)nullptr, (int64_t*)nullptr, (int)cp.leaves);
+  size_t t5 = 0, t6 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t5, (const uint64_t*)nullptr, (uint64_t*)nullptr, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (int)std::min<int64_t>(cp.L, INT32_MAX), 0, 64);
+  cub::DeviceRadixSort::SortKeys(nullptr, t6, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)cp.C, 0, 32);
+  const size_t bytes = std::max(std::max(std::max(t1, t2), std::max(t3, t4)), std::max(t5, t6));
+  cache[key] = bytes;
+  return bytes;
+}
+
 pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params* p, int64_t* leaf_off,
                             int64_t leaf_off_cap, uint32_t* leaf_ids, int64_t leaf_ids_cap, int64_t* n_leaves_h,
                             int64_t* n_inst_h, int* depth_h, Arena& ar, const Ctx& c) {
@@ -371,20 +397,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
   uint32_t* pk2 = ar.take<uint32_t>(cp.L);
   LeafJob* d_jobs = ar.take<LeafJob>(cp.J);
   LeafPart* d_parts = ar.take<LeafPart>(cp.J);
-  size_t t1 = 0, t2 = 0, t3 = 0, t4 = 0;
-  cub::DeviceSegmentedSort::SortPairs(nullptr, t1, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                      (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)std::min<int64_t>(cp.L, INT32_MAX),
-                                      (int)cp.G, (const int64_t*)nullptr, (const int64_t*)nullptr);
-  cub::DeviceSegmentedSort::SortKeys(nullptr, t2, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)cp.C, (int)cp.G,
-                                     (const int64_t*)nullptr, (const int64_t*)nullptr);
-  cub::DeviceRadixSort::SortPairs(nullptr, t3, (const uint32_t*)nullptr, (uint32_t*)nullptr, (const uint32_t*)nullptr,
-                                  (uint32_t*)nullptr, (int)std::min<int64_t>(cp.L, INT32_MAX));
-  cub::DeviceScan::ExclusiveSum(nullptr, t4, (const int64_t*)nullptr, (int64_t*)nullptr, (int)cp.leaves);
-  size_t t5 = 0, t6 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, t5, (const uint64_t*)nullptr, (uint64_t*)nullptr, (const uint32_t*)nullptr,
-                                  (uint32_t*)nullptr, (int)std::min<int64_t>(cp.L, INT32_MAX), 0, 64);
-  cub::DeviceRadixSort::SortKeys(nullptr, t6, (const uint32_t*)nullptr, (uint32_t*)nullptr, (int)cp.C, 0, 32);
-  const size_t cub_bytes = std::max(std::max(std::max(t1, t2), std::max(t3, t4)), std::max(t5, t6));
+  const size_t cub_bytes = partition_cub_bytes(cp);
   void* cub_tmp = ar.take<uint8_t>(cub_bytes);
   if (ar.measuring()) return PIPNN_OK;
   if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (partition)");
@@ -635,6 +648,11 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     PIPNN_CUDA(cudaMemcpyAsync(hbuf + 2 * C, d_redo, sizeof(int), cudaMemcpyDeviceToHost, st));
     PIPNN_CUDA(cudaEventRecord(ev_sync, st));
     PIPNN_TRY(launch_pending());  // the previous level's device subtrees (see PendingSubtree)
+    if (c.side_work && *c.side_work) {  // the caller's independent work (pipnn_build: sketches), once
+      std::function<pipnn_status()> fn;
+      fn.swap(*c.side_work);
+      PIPNN_TRY(fn());
+    }
     if (dbg_timing) t_sync0 = wall();
     PIPNN_CUDA(cudaEventSynchronize(ev_sync));
     if (dbg_timing) t_sync1 = wall();

@@ -199,6 +199,10 @@ pipnn_status sketch_impl(const pipnn_points* X, int m, uint64_t seed, void* sket
   int8_t* H = ar.take<int8_t>((size_t)m * X->d);
   if (ar.measuring()) return PIPNN_OK;
   if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (sketch)");
+  return sketch_launch(X, m, seed, sketch, H, c);
+}
+
+pipnn_status sketch_launch(const pipnn_points* X, int m, uint64_t seed, void* sketch, int8_t* H, const Ctx& c) {
   const int64_t md = (int64_t)m * X->d;
   hyperplane_kernel<<<(unsigned)ceil_div(md, 256), 256, 0, c.st>>>(m, X->d, seed, H);
   PIPNN_LAUNCHED("hyperplane_kernel", c.st);
