@@ -146,6 +146,23 @@ def test_partition_duplicates_guard():
     assert canon(goff.cpu().numpy(), u32(gids)) == canon(off, ids)
 
 
+@pytest.mark.parametrize("vals,d,n,fanout", [(3, 32, 20000, (2,)), (3, 32, 20000, (1,)), (3, 32, 20000, (3,)),
+                                             (2, 512, 6000, (2,))])
+def test_partition_u8_ties_and_extreme_rows(vals, d, n, fanout):
+    """Coarse values (many equal point-leader distances: the (D, leader id) tie order) and the widest rows
+    (d = 512, coordinates 0 or 255: the largest keys of the packed fanout <= 2 pass, dist_topk.cuh)."""
+    rng = np.random.default_rng(7 + d + len(fanout) + fanout[0])
+    X = (rng.integers(0, vals, size=(n, d)) * (255 if vals == 2 else 1)).astype(np.uint8)
+    c_max, c_min = 256, 40
+    p = synth.C2.params()
+    p.update(c_max=c_max, p_den=c_max, c_min=c_min, fanout=fanout, replicas=1)
+    off, ids, _ = O.partition(O.Dataset(X), p)
+    pp = P().partition_params(c_max=c_max, c_min=c_min, p_samp=(2, c_max), fanout=fanout, replicas=1,
+                              seed=p["seed"])
+    goff, gids = P().pipnn_partition(cuda(X), pp)
+    assert canon(goff.cpu().numpy(), u32(gids)) == canon(off, ids)
+
+
 @pytest.mark.parametrize("name", ["C1", "C3", "C4"])
 def test_partition_float_invariants_and_overlap(name):
     cfg = synth.CONFIGS[name]
