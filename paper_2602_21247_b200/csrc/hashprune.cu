@@ -220,6 +220,13 @@ pipnn_status hashprune_impl(int m, int l_max, int64_t n, const void* sketch, boo
 // (the leaf emits as many reverse as forward edges), with rev_start[j] / rev_cnt[j]. The residual hashes
 // (Eq. 1 via sketches) of both directions come from the leaf members' sketches staged in SMEM.
 template <typename ST>
+__device__ __forceinline__ ST bitcast_st(int x);
+template <>
+__device__ __forceinline__ int32_t bitcast_st<int32_t>(int x) { return x; }
+template <>
+__device__ __forceinline__ float bitcast_st<float>(int x) { return __int_as_float(x); }
+
+template <typename ST>
 __global__ void __launch_bounds__(256) hp_emit_kernel(const int64_t* __restrict__ leaf_off, const uint32_t* __restrict__ leaf_ids,
                                                       int k, const uint16_t* __restrict__ cols,
                                                       const float* __restrict__ dist, const ST* __restrict__ S, int m,
@@ -244,13 +251,29 @@ __global__ void __launch_bounds__(256) hp_emit_kernel(const int64_t* __restrict_
     rc[j] = 0;
     if (stage_sk) {
       const ST* src = S + (int64_t)id * m;
-      ST v[16];
+      if ((m & 3) == 0) {  // rows of m 4-byte values are 16-B aligned: m / 4 vector loads
+        int4 w[4];
 #pragma unroll
-      for (int t = 0; t < 16; ++t)
-        if (t < m) v[t] = src[t];  // independent loads, all in flight
+        for (int t = 0; t < 4; ++t)
+          if (4 * t < m) w[t] = __ldg(reinterpret_cast<const int4*>(src) + t);
 #pragma unroll
-      for (int t = 0; t < 16; ++t)
-        if (t < m) sk[j * ms + t] = v[t];
+        for (int t = 0; t < 4; ++t)
+          if (4 * t < m) {
+            ST* d = sk + j * ms + 4 * t;
+            d[0] = bitcast_st<ST>(w[t].x);
+            d[1] = bitcast_st<ST>(w[t].y);
+            d[2] = bitcast_st<ST>(w[t].z);
+            d[3] = bitcast_st<ST>(w[t].w);
+          }
+      } else {
+        ST v[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          if (t < m) v[t] = src[t];  // independent loads, all in flight
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          if (t < m) sk[j * ms + t] = v[t];
+      }
     }
   }
   __syncthreads();
