@@ -10,9 +10,10 @@
 //   <= 31 candidates : one warp per point — fp_gram_kernel (uint8: Gram in SMEM, fixpoint over ballots) or
 //                      fp_warp_kernel (float: Gram in registers, masks from the MMA fragments, warp bitonic
 //                      sort, sequential scan over shuffles);
-//   <= 63            : fp_coop_kernel (uint8: a CTA of 2 warps, Gram in SMEM) or fp_band_kernel<64> (float);
-//   <= 127, <= 191   : fp_band_kernel (a warp per 16-row Gram band, masks from the fragments, a scan warp
-//                      that ranks and scans while the band warps start the next point);
+//   <= 63, <= 127,   : fp_band_kernel (a warp per 16-row Gram band, masks from the fragments and the
+//   <= 191             candidates' ranks in the band warps, a scan warp that resolves 32-candidate batches
+//                      as ballot fixpoints while the band warps start the next point); PIPNN_FP_COOP=1 selects
+//                      the older fp_coop_kernel (a CTA of W warps, Gram in SMEM) for the 63 and 127 tiers;
 //   larger           : the generic final_prune_kernel.
 // final_prune = 0 (keep the R nearest reservoir entries) uses the generic kernel.
 // Then row_ptr = exclusive scan of the degrees and a coalesced copy into col_idx.
@@ -1639,7 +1640,7 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
 #define GP_ALL(U, M)                                                                                               \
   do {                                                                                                             \
     if (gram32 || (U)) GP_TIER(U, M, 32, 0); else GP_WARP(U, M);                                                   \
-    if (l_max > 31) { if (band && !(U)) GP_BAND(U, M, 64, 1); else GP_COOP(U, M, 64, 1); }                         \
+    if (l_max > 31) { if (band) GP_BAND(U, M, 64, 1); else GP_COOP(U, M, 64, 1); }                                 \
     if (l_max > 63) { if (band) GP_BAND(U, M, 128, 2); else GP_COOP(U, M, 128, 2); }                               \
     if (l_max > 127 && band && band_layout(X->d, U, 192).bytes <= 200 * 1024) GP_BAND(U, M, 192, 3);             \
     if (l_max > (band && band_layout(X->d, U, 192).bytes <= 200 * 1024 ? 191 : 127)) {                            \
