@@ -213,8 +213,17 @@ __global__ void __launch_bounds__(kStThreads, 2) subtree_kernel(const SubtreeArg
         for (int j0 = 0; j0 < l; j0 += 8) {
           uint32_t au[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
           float af[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-          for (int c = 0; c < nchunk; ++c) {
-            const uint4 x = __ldg(xr + c);
+          // the member row in batches of 4 chunks, the batch's loads issued together (latency-bound otherwise)
+          for (int c0 = 0; c0 < nchunk; c0 += 4) {
+          uint4 xs[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (c0 + t < nchunk) xs[t] = __ldg(xr + c0 + t);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            if (c0 + t >= nchunk) break;
+            const int c = c0 + t;
+            const uint4 x = xs[t];
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
               if (j0 + jj < l) {
@@ -245,6 +254,7 @@ __global__ void __launch_bounds__(kStThreads, 2) subtree_kernel(const SubtreeArg
                 }
               }
             }
+          }
           }
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
