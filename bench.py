@@ -318,8 +318,8 @@ def main():
     # ---------------- end-to-end, pipelined as a build service runs it: every step still copies its input
     # host->device and reads its CSR back, but on a copy stream, so the copy of step i+1's input and the read-back
     # of step i overlap build i (two device input buffers and two builders' outputs; skipped when memory is short).
-    # The overlap is partial: the build's own small plan uploads and read-backs queue behind the big copies on
-    # the copy engines (4 MB pieces did not help: all pieces are queued before them; 512 KB pieces cost host time).
+    # (The library moves its own small uploads/read-backs with kernels, so they do not queue behind these copies
+    # on the copy engines; splitting these copies into pieces did not help.)
     e2e_val, e2e_mode = e2e_serial, "serial: H2D, build, D2H per step on one stream"
     free_b, _ = torch.cuda.mem_get_info(dev)
     need = builder.ws_bytes + Xd.nbytes + builder.row_ptr.nbytes + builder.col_idx.nbytes

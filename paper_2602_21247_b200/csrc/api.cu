@@ -102,7 +102,7 @@ static pipnn_status pending_cuda() {
 static pipnn_status read_dev_error(int* err, cudaStream_t st) {
   int* hp = reinterpret_cast<int*>(pinned_scratch(sizeof(int)));
   if (!hp) return fail(PIPNN_ECUDA, "pinned host scratch");
-  PIPNN_CUDA(cudaMemcpyAsync(hp, err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PIPNN_CUDA(kcopy(hp, err, sizeof(int), st));
   PIPNN_CUDA(cudaStreamSynchronize(st));
   const int h = *hp;
   if (h == DERR_NONFINITE) return fail(PIPNN_EINVAL, "non-finite float input");
@@ -137,6 +137,52 @@ cudaEvent_t pool_event(size_t i) {
   return pool[i];
 }
 
+// Stream-ordered copy by a kernel between device memory and mapped pinned host memory (UVA pointers). The
+// build's small plan uploads and level read-backs then do not queue on the copy engines behind large transfers
+// of other streams (a service copying the next input while this build runs: bench.py's pipelined e2e).
+__global__ void kcopy_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, size_t bytes) {
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+  size_t done = 0;
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    const size_t n16 = bytes >> 4;
+    for (size_t i = tid; i < n16; i += nt) reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    done = n16 << 4;
+  }
+  for (size_t i = done + tid; i < bytes; i += nt) dst[i] = src[i];
+}
+cudaError_t kcopy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return cudaSuccess;
+  static const bool engine = std::getenv("PIPNN_COPY_ENGINE") != nullptr;  // experiment hook: cudaMemcpyAsync
+  if (engine) return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st);
+  const unsigned grid = (unsigned)std::min<size_t>(64, (bytes + 4095) / 4096);
+  kcopy_kernel<<<grid, 256, 0, st>>>(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), bytes);
+  count_launch();
+  return cudaGetLastError();
+}
+
+// Stream-ordered byte fill by a kernel (cudaMemsetAsync's signature), for the same reason as kcopy.
+__global__ void kmemset_kernel(uint8_t* __restrict__ dst, uint8_t v, size_t bytes) {
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+  size_t done = 0;
+  if ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    const uint32_t w = 0x01010101u * v;
+    const uint4 q = make_uint4(w, w, w, w);
+    const size_t n16 = bytes >> 4;
+    for (size_t i = tid; i < n16; i += nt) reinterpret_cast<uint4*>(dst)[i] = q;
+    done = n16 << 4;
+  }
+  for (size_t i = done + tid; i < bytes; i += nt) dst[i] = v;
+}
+cudaError_t kmemset(void* dst, int value, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return cudaSuccess;
+  static const bool engine = std::getenv("PIPNN_COPY_ENGINE") != nullptr;  // experiment hook: cudaMemsetAsync
+  if (engine) return cudaMemsetAsync(dst, value, bytes, st);
+  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((size_t)num_sms() * 8, (bytes + 4095) / 4096));
+  kmemset_kernel<<<grid, 256, 0, st>>>(static_cast<uint8_t*>(dst), (uint8_t)value, bytes);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // Runs the whole build through an Arena; with a measuring Arena it only sizes the workspace.
 uint8_t* pinned_scratch(size_t bytes) {
   struct Scratch {
@@ -152,7 +198,7 @@ uint8_t* pinned_scratch(size_t bytes) {
     s.p = nullptr;
     s.cap = 0;
     const size_t cap = std::max<size_t>(bytes, (size_t)1 << 16);
-    if (cudaHostAlloc((void**)&s.p, cap, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+    if (cudaHostAlloc((void**)&s.p, cap, cudaHostAllocMapped) != cudaSuccess) return nullptr;  // kcopy'd
     s.cap = cap;
   }
   return s.p;
@@ -194,7 +240,7 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
     if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small");
     for (int i = 0; i < 7; ++i)
       if (!(ev[i] = pool_event(i))) return fail(PIPNN_ECUDA, "timing event");
-    PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+    PIPNN_CUDA(kmemset(err, 0, 256, st));
     PIPNN_CUDA(cudaEventRecord(ev[0], st));
   }
   auto cleanup = [&]() { tile_ev.clear(); };  // (pooled events: nothing to destroy)
@@ -255,7 +301,7 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
     std::vector<int64_t> off(n_leaves + 1);
     int64_t* hoff = reinterpret_cast<int64_t*>(pinned_scratch((n_leaves + 1) * sizeof(int64_t)));
     if (!hoff) { cleanup(); return fail(PIPNN_ECUDA, "pinned host scratch"); }
-    PIPNN_CUDA(cudaMemcpyAsync(hoff, leaf_off, (n_leaves + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    PIPNN_CUDA(kcopy(hoff, leaf_off, (n_leaves + 1) * sizeof(int64_t), st));
     PIPNN_CUDA(cudaStreamSynchronize(st));
     std::copy(hoff, hoff + n_leaves + 1, off.begin());
     max_leaf_h = 1;
@@ -284,7 +330,7 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   // (a5, a6) bidirected edges -> HashPrune reservoirs (Alg. 3)
   // Reservoirs start empty (count = 0). The build never reads a slot at or beyond count[u] (merge and final
   // prune), so the n*l_max arena is not initialised here (it is internal to pipnn_build).
-  if (!ar.measuring()) PIPNN_CUDA(cudaMemsetAsync(count, 0, (size_t)X->n * sizeof(uint32_t), st));
+  if (!ar.measuring()) PIPNN_CUDA(kmemset(count, 0, (size_t)X->n * sizeof(uint32_t), st));
   s = hashprune_from_leaves(p->hp.m, p->hp.l_max, X->n, sketch, sk_int, slots, count, leaf_off, n_leaves, leaf_ids,
                             n_inst, k, cols, dist, max_leaf_h, n_edges_dev, ar, c);
   if (s != PIPNN_OK) { cleanup(); return s; }
@@ -308,9 +354,9 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   int64_t* hb = reinterpret_cast<int64_t*>(pinned_scratch(3 * sizeof(int64_t)));
   if (!hb) { cleanup(); return fail(PIPNN_ECUDA, "pinned host scratch"); }
   hb[2] = 0;
-  PIPNN_CUDA(cudaMemcpyAsync(&hb[0], row_ptr + X->n, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
-  PIPNN_CUDA(cudaMemcpyAsync(&hb[1], n_edges_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  PIPNN_CUDA(cudaMemcpyAsync(&hb[2], err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  PIPNN_CUDA(kcopy(&hb[0], row_ptr + X->n, sizeof(uint64_t), st));
+  PIPNN_CUDA(kcopy(&hb[1], n_edges_dev, sizeof(int64_t), st));
+  PIPNN_CUDA(kcopy(&hb[2], err, sizeof(int), st));
   PIPNN_CUDA(cudaStreamSynchronize(st));
   const uint64_t ne = (uint64_t)hb[0];
   const int64_t nstream = hb[1];
@@ -401,7 +447,7 @@ pipnn_status pipnn_partition(const pipnn_points* X, const pipnn_partition_params
   PIPNN_TRY(pending_cuda());
   Arena ar(ws, ws_bytes);
   int* err = err_slot(ar);
-  PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+  PIPNN_CUDA(kmemset(err, 0, 256, st));
   int depth = 0;
   PIPNN_TRY(partition_impl(X, p, leaf_off, leaf_off_cap, leaf_ids, leaf_ids_cap, n_leaves_h, n_instances_h, &depth, ar,
                            Ctx{st, err}));
@@ -423,7 +469,7 @@ pipnn_status pipnn_leaf_pick(const pipnn_points* X, const int64_t* leaf_off, con
   PIPNN_TRY(pending_cuda());
   Arena ar(ws, ws_bytes);
   int* err = err_slot(ar);
-  PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+  PIPNN_CUDA(kmemset(err, 0, 256, st));
   return leaf_pick_impl(X, leaf_off, leaf_ids, n_leaves, n_instances, p->k, nbr, dist, ar, Ctx{st, err});
 }
 
@@ -440,7 +486,7 @@ pipnn_status pipnn_sketch(const pipnn_points* X, const pipnn_hashprune_params* p
   PIPNN_TRY(pending_cuda());
   Arena ar(ws, ws_bytes);
   int* err = err_slot(ar);
-  PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+  PIPNN_CUDA(kmemset(err, 0, 256, st));
   return sketch_impl(X, p->m, p->seed, sketch, ar, Ctx{st, err});
 }
 
@@ -462,7 +508,7 @@ pipnn_status hashprune_insert(const pipnn_hashprune_params* p, int64_t n, const 
   PIPNN_TRY(pending_cuda());
   Arena ar(ws, ws_bytes);
   int* err = err_slot(ar);
-  PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+  PIPNN_CUDA(kmemset(err, 0, 256, st));
   return hashprune_impl(p->m, p->l_max, n, sketch, sk_dtype == PIPNN_U8, slots, count, owner, cand, dist, n_edges, ar,
                         Ctx{st, err});
 }
@@ -482,7 +528,7 @@ pipnn_status pipnn_final_prune(const pipnn_points* X, const pipnn_hashprune_para
   PIPNN_TRY(pending_cuda());
   Arena ar(ws, ws_bytes);
   int* err = err_slot(ar);
-  PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+  PIPNN_CUDA(kmemset(err, 0, 256, st));
   return final_prune_impl(X, hp->l_max, slots, count, p, row_ptr, col_idx, ar, Ctx{st, err});
 }
 
@@ -514,7 +560,7 @@ pipnn_status pipnn_search(const pipnn_points* X, const uint64_t* row_ptr, const 
   PIPNN_TRY(pending_cuda());
   Arena ar(ws, ws_bytes);
   int* err = err_slot(ar);
-  PIPNN_CUDA(cudaMemsetAsync(err, 0, 256, st));
+  PIPNN_CUDA(kmemset(err, 0, 256, st));
   return search_impl(X, row_ptr, col_idx, queries, ld_q, nq, entry, p->L, p->k, p->exclude_self ? 1 : 0, out_ids,
                      out_dist, n_cmps_dev, Ctx{st, err});
 }

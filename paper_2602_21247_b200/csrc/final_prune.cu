@@ -1533,7 +1533,7 @@ pipnn_status leaf_order(const uint32_t* leaf_ids, int64_t n_inst, int64_t n, uin
   void* tmp = ar.take<uint8_t>(tb);
   if (ar.measuring()) return PIPNN_OK;
   if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (leaf_order)");
-  PIPNN_CUDA(cudaMemsetAsync(first, 0xFF, (size_t)n * sizeof(uint32_t), c.st));
+  PIPNN_CUDA(kmemset(first, 0xFF, (size_t)n * sizeof(uint32_t), c.st));
   const int64_t g = std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_inst, 256), num_sms() * 32));
   first_instance_kernel<<<(unsigned)g, 256, 0, c.st>>>(leaf_ids, n_inst, first);
   PIPNN_LAUNCHED("first_instance_kernel", c.st);
@@ -1561,8 +1561,8 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
   if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (final_prune)");
   if (R > 256) return fail(PIPNN_EUNSUPPORTED, "R > 256");
   const bool u8 = X->dtype == PIPNN_U8, mips = X->metric == PIPNN_MIPS;
-  PIPNN_CUDA(cudaMemsetAsync(deg + n, 0, sizeof(uint32_t), c.st));
-  PIPNN_CUDA(cudaMemsetAsync(defer_n, 0, 5 * sizeof(uint32_t), c.st));
+  PIPNN_CUDA(kmemset(deg + n, 0, sizeof(uint32_t), c.st));
+  PIPNN_CUDA(kmemset(defer_n, 0, 5 * sizeof(uint32_t), c.st));
   const size_t pair_bytes = (size_t)kFpStage * (kFpStage - 1) * 2;  // u16 (i, j) pairs of the generic kernel
   int cap1 = l_max;
   FpLayout L1 = fp_layout(X->d, u8, l_max, cap1);

@@ -196,8 +196,8 @@ pipnn_status hashprune_impl(int m, int l_max, int64_t n, const void* sketch, boo
   if (ar.measuring()) return PIPNN_OK;
   if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (hashprune)");
   if (n_edges == 0) return PIPNN_OK;
-  PIPNN_CUDA(cudaMemsetAsync(g.cnt, 0, (n + 1) * sizeof(uint32_t), c.st));
-  PIPNN_CUDA(cudaMemsetAsync(g.cursor, 0, n * sizeof(uint32_t), c.st));
+  PIPNN_CUDA(kmemset(g.cnt, 0, (n + 1) * sizeof(uint32_t), c.st));
+  PIPNN_CUDA(kmemset(g.cursor, 0, n * sizeof(uint32_t), c.st));
   hp_hist_kernel<<<(unsigned)grid_for(n_edges), 256, 0, c.st>>>(owner, n_edges, g.cnt);
   PIPNN_LAUNCHED("hp_hist_kernel", c.st);
   PIPNN_CUDA(cub::DeviceScan::ExclusiveSum(g.tmp, g.tmp_bytes, g.cnt, g.start, (int)(n + 1), c.st));
@@ -851,7 +851,7 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
   if (ar.measuring()) return PIPNN_OK;
   if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (hashprune)");
   if (P >= ((int64_t)1 << 32)) return fail(PIPNN_EUNSUPPORTED, "hashprune: more than 2^32 picks in one wave");
-  PIPNN_CUDA(cudaMemsetAsync(n_edges_dev, 0, sizeof(int64_t), c.st));
+  PIPNN_CUDA(kmemset(n_edges_dev, 0, sizeof(int64_t), c.st));
   if (n_inst == 0 || n_leaves == 0) return PIPNN_OK;
   // (1) leaf-local emission of both edge directions
   max_leaf = std::max(1, std::min(max_leaf, 4096));
@@ -871,15 +871,15 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
   }
   PIPNN_LAUNCHED("hp_emit_kernel", c.st);
   // (2) point -> instances
-  PIPNN_CUDA(cudaMemsetAsync(g.cnt, 0, (n + 1) * sizeof(uint32_t), c.st));
-  PIPNN_CUDA(cudaMemsetAsync(g.cursor, 0, n * sizeof(uint32_t), c.st));
+  PIPNN_CUDA(kmemset(g.cnt, 0, (n + 1) * sizeof(uint32_t), c.st));
+  PIPNN_CUDA(kmemset(g.cursor, 0, n * sizeof(uint32_t), c.st));
   hp_inv_hist_kernel<<<(unsigned)grid_for(n_inst), 256, 0, c.st>>>(leaf_ids, n_inst, g.cnt);
   PIPNN_LAUNCHED("hp_inv_hist_kernel", c.st);
   PIPNN_CUDA(cub::DeviceScan::ExclusiveSum(g.tmp, g.tmp_bytes, g.cnt, g.start, (int)(n + 1), c.st));
   hp_inv_fill_kernel<<<(unsigned)grid_for(n_inst), 256, 0, c.st>>>(leaf_ids, n_inst, g.start, g.cursor, inv);
   PIPNN_LAUNCHED("hp_inv_fill_kernel", c.st);
   // (3) merge per owner (register path), deferred owners through the generic chunked path
-  PIPNN_CUDA(cudaMemsetAsync(defer_n, 0, sizeof(uint32_t), c.st));
+  PIPNN_CUDA(kmemset(defer_n, 0, sizeof(uint32_t), c.st));
   const int64_t blocks = std::min<int64_t>(ceil_div(n, 8), (int64_t)num_sms() * 32);
   hp_merge_inst_kernel<<<(unsigned)blocks, 256, 0, c.st>>>(n, l_max, k, g.start, inv, fwd, rev, rev_start, rev_cnt,
                                                                slots, count, defer, defer_n);

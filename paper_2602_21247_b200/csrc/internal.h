@@ -77,7 +77,10 @@ pipnn_status leaf_order(const uint32_t* leaf_ids, int64_t n_inst, int64_t n, uin
 bool subtree_fits(const pipnn_points* X, const pipnn_partition_params* p, int64_t size, int depth);
 // Pinned host scratch for small device -> host reads (thread-local, grows as needed; callers copy into it
 // with cudaMemcpyAsync, synchronise the stream, then read it — nothing stays pending across calls).
-uint8_t* pinned_scratch(size_t bytes);
+uint8_t* pinned_scratch(size_t bytes);  // mapped pinned host memory, reused per thread (api.cu)
+// Stream-ordered copy by a kernel (device <-> mapped pinned host or device), not by a copy engine (api.cu).
+cudaError_t kcopy(void* dst, const void* src, size_t bytes, cudaStream_t st);
+cudaError_t kmemset(void* dst, int value, size_t bytes, cudaStream_t st);  // likewise for cudaMemsetAsync
 cudaEvent_t pool_event(size_t i);  // per-thread, per-device reusable timing event i (api.cu)
 // Batched beam search (search.cu, Alg. 1): one warp per query; L <= 256.
 size_t search_smem_per_warp(const pipnn_points* X);

@@ -172,7 +172,7 @@ pipnn_status csr_dist_segs(const int64_t* off, int64_t ns, int k, int self, Dist
   if (ar.measuring()) return PIPNN_OK;
   if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (csr_dist_segs)");
   if (ns == 0) {
-    PIPNN_CUDA(cudaMemsetAsync(n_items, 0, sizeof(int64_t), c.st));
+    PIPNN_CUDA(kmemset(n_items, 0, sizeof(int64_t), c.st));
     return PIPNN_OK;
   }
   const int tb = 256;
@@ -182,6 +182,12 @@ pipnn_status csr_dist_segs(const int64_t* off, int64_t ns, int k, int self, Dist
   csr_fill_kernel<<<(unsigned)ceil_div(ns, tb), tb, 0, c.st>>>(off, ns, blocks, bpos, k, self, segs, items, n_items);
   PIPNN_LAUNCHED("csr_fill_kernel", c.st);
   return PIPNN_OK;
+}
+
+// The gather's compact view of the leaf segments (a kernel rather than a strided copy-engine copy).
+__global__ void tileseg_view_kernel(const DistSeg* __restrict__ segs, int64_t n, TileSeg* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = segs[i].a;
 }
 
 // ------------------------------------------------------------------ leaf pick
@@ -204,8 +210,8 @@ pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, cons
   if (ar.measuring()) return PIPNN_OK;
   if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (leaf_pick)");
   if (n_leaves == 0 || n_inst == 0) return PIPNN_OK;
-  PIPNN_CUDA(cudaMemcpy2DAsync(tsegs, sizeof(TileSeg), segs, sizeof(DistSeg), sizeof(TileSeg), (size_t)n_leaves,
-                               cudaMemcpyDeviceToDevice, c.st));
+  tileseg_view_kernel<<<(unsigned)ceil_div(n_leaves, 256), 256, 0, c.st>>>(segs, n_leaves, tsegs);
+  PIPNN_LAUNCHED("tileseg_view_kernel", c.st);
   PIPNN_TRY(gather_tiled(X, leaf_ids, tsegs, items, n_items, max_items, T, nrm, c, Kb));
   DistTopkArgs a{};
   a.Ta = T;

@@ -207,7 +207,7 @@ struct PinnedArena {
       base = nullptr;
       cap = std::max<size_t>(2 * cap, std::max<size_t>(need, (size_t)1 << 20));
       used = 0;
-      e = cudaHostAlloc((void**)&base, cap, cudaHostAllocDefault);
+      e = cudaHostAlloc((void**)&base, cap, cudaHostAllocMapped);  // read by kcopy's kernel
       if (e != cudaSuccess) {
         base = nullptr;
         cap = 0;
@@ -217,7 +217,7 @@ struct PinnedArena {
     uint8_t* p = base + used;
     used = (used + bytes + 255) & ~(size_t)255;
     std::memcpy(p, src, bytes);
-    return cudaMemcpyAsync(dst, p, bytes, cudaMemcpyHostToDevice, st);
+    return kcopy(dst, p, bytes, st);
   }
   void reset() { used = 0; }
 };
@@ -487,7 +487,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
   auto launch_pending = [&]() -> pipnn_status {
     if (!pend.on) return PIPNN_OK;
     pend.on = false;
-    PIPNN_CUDA(cudaMemsetAsync(dev_work, 0, sizeof(int), st));
+    PIPNN_CUDA(kmemset(dev_work, 0, sizeof(int), st));
     return subtree_launch(X, p, dev_groups, pend.ng, pend.mem, staging, 2 * cp.L, dev_ctr + 1, dev_leaf_dst,
                           dev_leaf_size, cp.leaves, dev_ctr, dev_work, c.err, dev_work + 1, st);
   };
@@ -548,9 +548,9 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     PIPNN_CUDA(g_pin_level.copy(d_cbase, cb.data(), G * sizeof(int64_t), st));
     PIPNN_CUDA(g_pin_level.copy(d_cand_seg, cand_seg.data(), (G + 1) * sizeof(int64_t), st));
     PIPNN_CUDA(g_pin_level.copy(d_lead_seg, lead_seg.data(), (G + 1) * sizeof(int64_t), st));
-    PIPNN_CUDA(cudaMemsetAsync(d_cnt, 0, G * sizeof(uint32_t), st));
-    PIPNN_CUDA(cudaMemsetAsync(d_redo, 0, sizeof(int), st));
-    PIPNN_CUDA(cudaMemsetAsync(ck, 0xFF, NC * sizeof(uint64_t), st));
+    PIPNN_CUDA(kmemset(d_cnt, 0, G * sizeof(uint32_t), st));
+    PIPNN_CUDA(kmemset(d_redo, 0, sizeof(int), st));
+    PIPNN_CUDA(kmemset(ck, 0xFF, NC * sizeof(uint64_t), st));
     prio_kernel<<<(unsigned)std::min<int64_t>(ceil_div(M, 256), num_sms() * 64), 256, 0, st>>>(
         d_groups, d_cbase, G, M, mem, d_cnt, ck, cv, d_redo);
     PIPNN_LAUNCHED("prio_kernel", st);
@@ -616,7 +616,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     const int packed = X->dtype == PIPNN_U8 && fmax_l <= 2 && !no_packed ? 1 : 0;
     PIPNN_TRY(gather_tiled(X, lead_sorted, tsB, itB, n_it + 1, nItB, TB, nB, c, 0, packed));
     const double t_gather = dbg_timing ? wall() : 0.0;
-    PIPNN_CUDA(cudaMemsetAsync(ccnt, 0, C * sizeof(uint32_t), st));
+    PIPNN_CUDA(kmemset(ccnt, 0, C * sizeof(uint32_t), st));
     DistTopkArgs da{};
     da.Ta = TA;
     da.Tb = TB;
@@ -643,9 +643,9 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     // (pinned read-back: the three copies stay asynchronous, one synchronisation)
     uint32_t* hbuf = reinterpret_cast<uint32_t*>(pinned_scratch((2 * C + 1) * sizeof(uint32_t)));
     if (!hbuf) return fail(PIPNN_ECUDA, "pinned host scratch");
-    PIPNN_CUDA(cudaMemcpyAsync(hbuf, ccnt, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    PIPNN_CUDA(cudaMemcpyAsync(hbuf + C, lead_sorted, C * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-    PIPNN_CUDA(cudaMemcpyAsync(hbuf + 2 * C, d_redo, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PIPNN_CUDA(kcopy(hbuf, ccnt, C * sizeof(uint32_t), st));
+    PIPNN_CUDA(kcopy(hbuf + C, lead_sorted, C * sizeof(uint32_t), st));
+    PIPNN_CUDA(kcopy(hbuf + 2 * C, d_redo, sizeof(int), st));
     PIPNN_CUDA(cudaEventRecord(ev_sync, st));
     PIPNN_TRY(launch_pending());  // the previous level's device subtrees (see PendingSubtree)
     if (c.side_work && *c.side_work) {  // the caller's independent work (pipnn_build: sketches), once
@@ -765,22 +765,22 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     unsigned long long* hb = reinterpret_cast<unsigned long long*>(pinned_scratch(3 * sizeof(unsigned long long)));
     if (!hb) return fail(PIPNN_ECUDA, "pinned host scratch");
     hb[2] = 0;
-    PIPNN_CUDA(cudaMemcpyAsync(hb, dev_ctr, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-    PIPNN_CUDA(cudaMemcpyAsync(&hb[2], dev_work + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    PIPNN_CUDA(kcopy(hb, dev_ctr, 2 * sizeof(unsigned long long), st));
+    PIPNN_CUDA(kcopy(&hb[2], dev_work + 1, sizeof(int), st));
     PIPNN_CUDA(cudaStreamSynchronize(st));
     const unsigned long long hc[2] = {hb[0], hb[1]};
     const int hdepth = (int)(hb[2] & 0xFFFFFFFFull);
     const int64_t nd = (int64_t)hc[0];
     if (n_leaves + nd > cp.leaves) return fail(PIPNN_ECAPACITY, "partition: leaf capacity (device subtrees)");
     if (nd > 0) {
-      PIPNN_CUDA(cudaMemcpyAsync(leaf_size + n_leaves, dev_leaf_size, nd * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-      PIPNN_CUDA(cudaMemcpyAsync(leaf_dst + n_leaves, dev_leaf_dst, nd * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+      PIPNN_CUDA(kcopy(leaf_size + n_leaves, dev_leaf_size, nd * sizeof(int64_t), st));
+      PIPNN_CUDA(kcopy(leaf_dst + n_leaves, dev_leaf_dst, nd * sizeof(int64_t), st));
       n_leaves += nd;
     }
     depth = std::max(depth, hdepth);
   }
   // ---- leaf_off = exclusive scan of the leaf sizes; compact the staged leaves into leaf_ids
-  PIPNN_CUDA(cudaMemsetAsync(leaf_size + n_leaves, 0, sizeof(int64_t), st));
+  PIPNN_CUDA(kmemset(leaf_size + n_leaves, 0, sizeof(int64_t), st));
   size_t tb = cub_bytes;
   PIPNN_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp, tb, leaf_size, leaf_off, (int)(n_leaves + 1), st));
   if (n_leaves > 0) {
@@ -790,7 +790,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
   }
   int64_t* hni = reinterpret_cast<int64_t*>(pinned_scratch(sizeof(int64_t)));
   if (!hni) return fail(PIPNN_ECUDA, "pinned host scratch");
-  PIPNN_CUDA(cudaMemcpyAsync(hni, leaf_off + n_leaves, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  PIPNN_CUDA(kcopy(hni, leaf_off + n_leaves, sizeof(int64_t), st));
   PIPNN_CUDA(cudaStreamSynchronize(st));
   const int64_t ni = *hni;
   *n_leaves_h = n_leaves;
