@@ -1503,12 +1503,44 @@ __global__ void __launch_bounds__(2 * CP + 32, CP <= 64 ? 4 : (CP <= 128 ? 2 : 1
 
 __global__ void csr_copy_kernel(int64_t n, int R, const uint32_t* __restrict__ nbr_tmp, const uint32_t* __restrict__ deg,
                                 const uint64_t* __restrict__ row_ptr, uint32_t* __restrict__ col_idx) {
+  // a warp per 32 consecutive points: their degrees and offsets in one coalesced load each, then the rows in
+  // groups of 4 points with all loads of a group in flight before its stores (latency-bound otherwise)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; u < n;
-       u += (int64_t)gridDim.x * (blockDim.x >> 5)) {
-    const uint32_t dg = deg[u];
-    const uint64_t o = row_ptr[u];
-    for (uint32_t t = lane; t < dg; t += 32) col_idx[o + t] = nbr_tmp[u * (int64_t)R + t];
+  const int64_t nchunk = (n + 31) >> 5;
+  for (int64_t ch = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; ch < nchunk;
+       ch += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int64_t u0 = ch << 5;
+    const int64_t ul = u0 + lane;
+    const uint32_t dgl = ul < n ? deg[ul] : 0u;
+    const uint64_t ol = ul < n ? row_ptr[ul] : 0ull;
+    for (int j0 = 0; j0 < 32; j0 += 4) {
+      uint32_t v[4][2];
+      uint32_t dgs[4];
+      uint64_t os[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        dgs[q] = __shfl_sync(0xffffffffu, dgl, j0 + q);
+        os[q] = __shfl_sync(0xffffffffu, ol, j0 + q);
+        const uint32_t* src = nbr_tmp + (u0 + j0 + q) * (int64_t)R;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t t = lane + 32 * h;
+          v[q][h] = t < dgs[q] ? src[t] : 0u;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t t = lane + 32 * h;
+          if (t < dgs[q]) col_idx[os[q] + t] = v[q][h];
+        }
+      }
+      // rows longer than 64 entries (R > 64)
+      for (int q = 0; q < 4; ++q)
+        for (uint32_t t = 64 + lane; t < dgs[q]; t += 32)
+          col_idx[os[q] + t] = nbr_tmp[(u0 + j0 + q) * (int64_t)R + t];
+    }
   }
 }
 
@@ -1693,7 +1725,7 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
 #undef FP_LAUNCH
   }
   PIPNN_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, deg, row_ptr, (int)(n + 1), c.st));
-  csr_copy_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 8), num_sms() * 32), 256, 0, c.st>>>(n, R, nbr_tmp, deg,
+  csr_copy_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), num_sms() * 16), 256, 0, c.st>>>(n, R, nbr_tmp, deg,
                                                                                                  row_ptr, col_idx);
   PIPNN_LAUNCHED("csr_copy_kernel", c.st);
   return PIPNN_OK;
