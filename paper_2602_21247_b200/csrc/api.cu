@@ -160,6 +160,38 @@ cudaError_t kcopy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// Several copies in one launch: blockIdx.y selects the descriptor, the x blocks split it.
+__global__ void kcopy_batch_kernel(const KCopyDesc* __restrict__ descs) {
+  const KCopyDesc d = descs[blockIdx.y];
+  uint8_t* dst = static_cast<uint8_t*>(d.dst);
+  const uint8_t* src = static_cast<const uint8_t*>(d.src);
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;
+  size_t done = 0;
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    const size_t n16 = d.bytes >> 4;
+    for (size_t i = tid; i < n16; i += nt) reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    done = n16 << 4;
+  }
+  for (size_t i = done + tid; i < d.bytes; i += nt) dst[i] = src[i];
+}
+cudaError_t kcopy_batch(const KCopyDesc* descs, int n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  static const bool engine = std::getenv("PIPNN_COPY_ENGINE") != nullptr;  // experiment hook
+  if (engine) {
+    for (int i = 0; i < n; ++i) {
+      cudaError_t e = cudaMemcpyAsync(descs[i].dst, descs[i].src, descs[i].bytes, cudaMemcpyDefault, st);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  unsigned long long mx = 0;
+  for (int i = 0; i < n; ++i) mx = std::max(mx, descs[i].bytes);
+  const unsigned gx = (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>(32, (mx + 4095) / 4096));
+  kcopy_batch_kernel<<<dim3(gx, (unsigned)n), 256, 0, st>>>(descs);
+  count_launch();
+  return cudaGetLastError();
+}
+
 // Stream-ordered byte fill by a kernel (cudaMemsetAsync's signature), for the same reason as kcopy.
 __global__ void kmemset_kernel(uint8_t* __restrict__ dst, uint8_t v, size_t bytes) {
   const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nt = (size_t)gridDim.x * blockDim.x;

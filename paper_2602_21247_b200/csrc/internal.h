@@ -81,6 +81,13 @@ uint8_t* pinned_scratch(size_t bytes);  // mapped pinned host memory, reused per
 // Stream-ordered copy by a kernel (device <-> mapped pinned host or device), not by a copy engine (api.cu).
 cudaError_t kcopy(void* dst, const void* src, size_t bytes, cudaStream_t st);
 cudaError_t kmemset(void* dst, int value, size_t bytes, cudaStream_t st);  // likewise for cudaMemsetAsync
+struct KCopyDesc {
+  void* dst;
+  const void* src;
+  unsigned long long bytes;
+};
+// n copies in one kernel; descs in mapped pinned (or device) memory, valid until the kernel has run (api.cu)
+cudaError_t kcopy_batch(const KCopyDesc* descs, int n, cudaStream_t st);
 cudaEvent_t pool_event(size_t i);  // per-thread, per-device reusable timing event i (api.cu)
 // Batched beam search (search.cu, Alg. 1): one warp per query; L <= 256.
 size_t search_smem_per_warp(const pipnn_points* X);

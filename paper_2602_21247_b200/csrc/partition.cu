@@ -197,29 +197,61 @@ struct PinnedArena {
   ~PinnedArena() {
     if (base) cudaFreeHost(base);
   }
-  cudaError_t copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
-    if (bytes == 0) return cudaSuccess;
-    const size_t need = (used + bytes + 255) & ~(size_t)255;
-    if (need > cap) {
-      cudaError_t e = cudaStreamSynchronize(st);  // every pending copy from this arena has completed
-      if (e != cudaSuccess) return e;
-      if (base) cudaFreeHost(base);
+  std::vector<KCopyDesc> pend;  // staged copies not yet launched (flush: one kernel for all of them)
+  cudaError_t grow(size_t need, cudaStream_t st) {
+    cudaError_t e = flush(st);  // the pending copies read the old block: launch them first
+    if (e != cudaSuccess) return e;
+    e = cudaStreamSynchronize(st);  // every pending copy from this arena has completed
+    if (e != cudaSuccess) return e;
+    if (base) cudaFreeHost(base);
+    base = nullptr;
+    cap = std::max<size_t>(2 * cap, std::max<size_t>(need, (size_t)1 << 20));
+    used = 0;
+    e = cudaHostAlloc((void**)&base, cap, cudaHostAllocMapped);  // read by the copy kernel
+    if (e != cudaSuccess) {
       base = nullptr;
-      cap = std::max<size_t>(2 * cap, std::max<size_t>(need, (size_t)1 << 20));
-      used = 0;
-      e = cudaHostAlloc((void**)&base, cap, cudaHostAllocMapped);  // read by kcopy's kernel
-      if (e != cudaSuccess) {
-        base = nullptr;
-        cap = 0;
-        return e;
-      }
+      cap = 0;
     }
+    return e;
+  }
+  uint8_t* stage(const void* src, size_t bytes, cudaStream_t st, cudaError_t& e) {
+    e = cudaSuccess;
+    const size_t need = (used + bytes + 255) & ~(size_t)255;
+    if (need > cap && (e = grow(need, st)) != cudaSuccess) return nullptr;
     uint8_t* p = base + used;
     used = (used + bytes + 255) & ~(size_t)255;
-    std::memcpy(p, src, bytes);
-    return kcopy(dst, p, bytes, st);
+    if (src) std::memcpy(p, src, bytes);
+    return p;
   }
-  void reset() { used = 0; }
+  // Stage src and queue its copy to dst; it runs at the next flush (call flush before the first kernel
+  // that reads dst).
+  cudaError_t copy(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return cudaSuccess;
+    cudaError_t e;
+    uint8_t* p = stage(src, bytes, st, e);
+    if (!p) return e;
+    pend.push_back(KCopyDesc{dst, p, (unsigned long long)bytes});
+    return cudaSuccess;
+  }
+  cudaError_t flush(cudaStream_t st) {
+    if (pend.empty()) return cudaSuccess;
+    const size_t nb = pend.size() * sizeof(KCopyDesc);
+    std::vector<KCopyDesc> d;
+    d.swap(pend);
+    const size_t need = (used + nb + 255) & ~(size_t)255;
+    if (need > cap) {  // no room for the descriptors: launch the copies one by one (rare)
+      for (const KCopyDesc& x : d) {
+        cudaError_t e = kcopy(x.dst, x.src, x.bytes, st);
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    }
+    uint8_t* p = base + used;
+    used = need;
+    std::memcpy(p, d.data(), nb);
+    return kcopy_batch(reinterpret_cast<const KCopyDesc*>(p), (int)d.size(), st);
+  }
+  void reset() { used = 0; pend.clear(); }
 };
 static thread_local PinnedArena g_pin_level, g_pin_jobs;
 
@@ -444,6 +476,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     g_pin_jobs.reset();  // its previous copies completed at the last synchronisation
     PIPNN_CUDA(g_pin_jobs.copy(d_jobs, jobs.data(), jobs.size() * sizeof(LeafJob), st));
     PIPNN_CUDA(g_pin_jobs.copy(d_parts, parts.data(), parts.size() * sizeof(LeafPart), st));
+    PIPNN_CUDA(g_pin_jobs.flush(st));
     leaf_job_kernel<<<(unsigned)jobs.size(), 256, 0, st>>>(d_jobs, (int)jobs.size(), d_parts, src, staging, leaf_size);
     PIPNN_LAUNCHED("leaf_job_kernel", st);
     // (host->device copies from pageable memory have consumed jobs/parts when they return)
@@ -548,6 +581,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     PIPNN_CUDA(g_pin_level.copy(d_cbase, cb.data(), G * sizeof(int64_t), st));
     PIPNN_CUDA(g_pin_level.copy(d_cand_seg, cand_seg.data(), (G + 1) * sizeof(int64_t), st));
     PIPNN_CUDA(g_pin_level.copy(d_lead_seg, lead_seg.data(), (G + 1) * sizeof(int64_t), st));
+    PIPNN_CUDA(g_pin_level.flush(st));
     PIPNN_CUDA(kmemset(d_cnt, 0, G * sizeof(uint32_t), st));
     PIPNN_CUDA(kmemset(d_redo, 0, sizeof(int), st));
     PIPNN_CUDA(kmemset(ck, 0xFF, NC * sizeof(uint64_t), st));
@@ -609,6 +643,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     PIPNN_CUDA(g_pin_level.copy(itA, hItA.data(), nItA * sizeof(WorkItem), st));
     PIPNN_CUDA(g_pin_level.copy(itB, hItB.data(), nItB * sizeof(WorkItem), st));
     PIPNN_CUDA(g_pin_level.copy(n_it, nits, 2 * sizeof(int64_t), st));
+    PIPNN_CUDA(g_pin_level.flush(st));
     const double t_plan2 = dbg_timing ? wall() : 0.0;
     PIPNN_TRY(gather_tiled(X, mem, tsA, itA, n_it, nItA, TA, nA, c));
     // uint8 with fanout <= 2 at this level: leader norms in the packed form of the single-pass top-2
@@ -742,6 +777,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
         std::stable_sort(dg.begin(), dg.end(), [](const DevGroup& a, const DevGroup& b) { return a.size > b.size; });
         // the members live in `nxt`, which the level after next overwrites: stream order runs this first
         PIPNN_CUDA(g_pin_jobs.copy(dev_groups, dg.data(), dg.size() * sizeof(DevGroup), st));
+        PIPNN_CUDA(g_pin_jobs.flush(st));
         pend.on = true;  // launched behind the next level's read-back (or after the loop)
         pend.ng = (int)dg.size();
         pend.mem = nxt;
@@ -761,6 +797,7 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
   // ---- leaves carved on the device follow the host's leaves
   g_pin_level.reset();
   PIPNN_CUDA(g_pin_level.copy(leaf_dst, h_leaf_dst.data(), n_leaves * sizeof(int64_t), st));
+  PIPNN_CUDA(g_pin_level.flush(st));
   {
     unsigned long long* hb = reinterpret_cast<unsigned long long*>(pinned_scratch(3 * sizeof(unsigned long long)));
     if (!hb) return fail(PIPNN_ECUDA, "pinned host scratch");
