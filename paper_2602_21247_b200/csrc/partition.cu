@@ -676,11 +676,17 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
     PIPNN_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, pk, pk2, cv2, nxt, (int)Q, 0, bits_for(C), st));
     // ---- 4. host merge plan (the level's one synchronisation)
     // (pinned read-back: the three copies stay asynchronous, one synchronisation)
-    uint32_t* hbuf = reinterpret_cast<uint32_t*>(pinned_scratch((2 * C + 1) * sizeof(uint32_t)));
-    if (!hbuf) return fail(PIPNN_ECUDA, "pinned host scratch");
-    PIPNN_CUDA(kcopy(hbuf, ccnt, C * sizeof(uint32_t), st));
-    PIPNN_CUDA(kcopy(hbuf + C, lead_sorted, C * sizeof(uint32_t), st));
-    PIPNN_CUDA(kcopy(hbuf + 2 * C, d_redo, sizeof(int), st));
+    // one batched read-back (child counts, sorted leaders, redo flag) into pinned scratch; its descriptors
+    // sit behind the data in the same mapped buffer
+    const size_t hb_data = ((2 * C + 1) * sizeof(uint32_t) + 15) & ~(size_t)15;
+    uint8_t* hraw = pinned_scratch(hb_data + 3 * sizeof(KCopyDesc));
+    if (!hraw) return fail(PIPNN_ECUDA, "pinned host scratch");
+    uint32_t* hbuf = reinterpret_cast<uint32_t*>(hraw);
+    KCopyDesc* hd = reinterpret_cast<KCopyDesc*>(hraw + hb_data);
+    hd[0] = KCopyDesc{hbuf, ccnt, (unsigned long long)(C * sizeof(uint32_t))};
+    hd[1] = KCopyDesc{hbuf + C, lead_sorted, (unsigned long long)(C * sizeof(uint32_t))};
+    hd[2] = KCopyDesc{hbuf + 2 * C, d_redo, (unsigned long long)sizeof(int)};
+    PIPNN_CUDA(kcopy_batch(hd, 3, st));
     PIPNN_CUDA(cudaEventRecord(ev_sync, st));
     PIPNN_TRY(launch_pending());  // the previous level's device subtrees (see PendingSubtree)
     if (c.side_work && *c.side_work) {  // the caller's independent work (pipnn_build: sketches), once
