@@ -288,6 +288,8 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   std::function<pipnn_status()> sketch_work = [&, H]() { return sketch_launch(XS, p->hp.m, p->hp.seed, sketch, H, c); };
   Ctx cp_ctx = c;
   if (!ar.measuring()) cp_ctx.side_work = &sketch_work;
+  static const bool dbg_check = std::getenv("PIPNN_DEBUG_CHECK") != nullptr;
+  cp_ctx.defer_inst_count = !ar.measuring() && !dbg_check;  // read below with the leaf offsets
   // (a1, a2) partition (Alg. 5)
   int64_t n_leaves = 0, n_inst = 0;
   int depth = 0;
@@ -297,6 +299,7 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   if (s != PIPNN_OK) { cleanup(); return s; }
   ar.release(mark);
   if (ar.measuring()) n_inst = bp.leaf_ids_cap;  // size the later stages at their upper bounds
+  else if (n_leaves == 0) n_inst = 0;
   if (!ar.measuring() && std::getenv("PIPNN_DEBUG_CHECK")) {
     // debug: host-side check of the partition output (sorted unique ids < n, sizes <= C_max, coverage)
     std::vector<int64_t> ho(n_leaves + 1);
@@ -336,6 +339,7 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
     PIPNN_CUDA(kcopy(hoff, leaf_off, (n_leaves + 1) * sizeof(int64_t), st));
     PIPNN_CUDA(cudaStreamSynchronize(st));
     std::copy(hoff, hoff + n_leaves + 1, off.begin());
+    n_inst = off[n_leaves];  // (the partition left it unread: cp_ctx.defer_inst_count)
     max_leaf_h = 1;
     for (int64_t b = 0; b < n_leaves; ++b) {
       leaf_pairs += (off[b + 1] - off[b]) * (off[b + 1] - off[b]);

@@ -18,6 +18,8 @@ struct Ctx {
   // optional: independent work that the partition enqueues behind its first level's read-back, so it fills
   // the GPU while the host plans that level (pipnn_build: the sketches); run by the caller if not taken
   std::function<pipnn_status()>* side_work = nullptr;
+  // partition_impl: leave the instance count unread (*n_inst_h = -1); the caller reads leaf_off itself
+  bool defer_inst_count = false;
 };
 
 // Bytes per row of the tiled (K-major, SWIZZLE_NONE) layout: uint8 -> round_up(d, 32);

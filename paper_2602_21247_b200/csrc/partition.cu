@@ -831,13 +831,17 @@ pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params*
                                                                                          staging, leaf_ids);
     PIPNN_LAUNCHED("leaf_compact_kernel", st);
   }
+  *n_leaves_h = n_leaves;
+  *depth_h = depth;
+  if (c.defer_inst_count) {  // pipnn_build reads leaf_off (and with it the count) right after
+    *n_inst_h = -1;
+    return PIPNN_OK;
+  }
   int64_t* hni = reinterpret_cast<int64_t*>(pinned_scratch(sizeof(int64_t)));
   if (!hni) return fail(PIPNN_ECUDA, "pinned host scratch");
   PIPNN_CUDA(kcopy(hni, leaf_off + n_leaves, sizeof(int64_t), st));
   PIPNN_CUDA(cudaStreamSynchronize(st));
-  const int64_t ni = *hni;
-  *n_leaves_h = n_leaves;
-  *n_inst_h = ni;
+  *n_inst_h = *hni;
   *depth_h = depth;
   return PIPNN_OK;
 }
