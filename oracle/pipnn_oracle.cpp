@@ -163,6 +163,16 @@ struct Data {
     }
     return s;
   }
+  // The dissimilarity RobustPrune's alpha test is applied to (reading R22, changed): the dataset's own
+  // measure for L2; for MIPS the angular dissimilarity 1 - <a,b>/(||a|| ||b||) (cosine 0 when a norm is 0).
+  // alpha >= 1 relaxes the prune only on non-negative values; on the signed -<a,b> the
+  // same product tightens it and the final prune leaves out-degree ~1 (R22).
+  double dprune(int64_t a, int64_t b) const {
+    if (!mips) return dist(a, b);
+    const double ab = -dist(a, b), aa = -dist(a, a), bb = -dist(b, b);
+    if (aa <= 0.0 || bb <= 0.0) return 1.0;
+    return 1.0 - ab / (std::sqrt(aa) * std::sqrt(bb));
+  }
   // ||q,b|| for an external query vector q given in fp64
   double dist_q(const double* q, int64_t b) const {
     double s = 0;
@@ -506,7 +516,9 @@ bool run_hashprune(int64_t n, const std::vector<double>& S, int m, int lmax, con
 }
 
 // ------------------------------------------------------------------ Alg. 2 RobustPrune (eager + lazy)
-// alpha = an/ad; the test "alpha*||y,z|| < ||x,z||" is written an*D(y,z) < ad*D(x,z).
+// alpha = an/ad; the test "alpha*||y,z|| < ||x,z||" is written an*D'(y,z) < ad*D'(x,z), D' = the
+// prune dissimilarity (Data::dprune: D itself for L2, the angular one for MIPS); candidates are taken in the
+// (D(x,.), id) order of the dataset's measure either way.
 std::vector<uint32_t> robust_prune_eager(const Data& X, uint32_t x, std::vector<std::pair<double, uint32_t>> N,
                                          int R, int an, int ad) {
   std::vector<uint32_t> E;
@@ -519,21 +531,21 @@ std::vector<uint32_t> robust_prune_eager(const Data& X, uint32_t x, std::vector<
     N.erase(N.begin() + bi);
     std::vector<std::pair<double, uint32_t>> keep;
     for (auto& z : N)
-      if (!((double)an * X.dist(y.second, z.second) < (double)ad * z.first)) keep.push_back(z);
+      if (!((double)an * X.dprune(y.second, z.second) < (double)ad * X.dprune(x, z.second))) keep.push_back(z);
     N.swap(keep);
   }
-  (void)x;
   return E;
 }
-std::vector<uint32_t> robust_prune_lazy(const Data& X, std::vector<std::pair<double, uint32_t>> N, int R, int an,
-                                        int ad) {
+std::vector<uint32_t> robust_prune_lazy(const Data& X, uint32_t x, std::vector<std::pair<double, uint32_t>> N, int R,
+                                        int an, int ad) {
   std::sort(N.begin(), N.end());
   std::vector<uint32_t> E;
   for (auto& c : N) {
     if ((int)E.size() >= R) break;
     bool pruned = false;
+    const double dxc = X.dprune(x, c.second);
     for (uint32_t y : E)
-      if ((double)an * X.dist(y, c.second) < (double)ad * c.first) {
+      if ((double)an * X.dprune(y, c.second) < (double)ad * dxc) {
         pruned = true;
         break;
       }
@@ -560,7 +572,7 @@ bool run_final_prune(const Data& X, const uint64_t* slots, const uint32_t* count
       uint32_t v = (uint32_t)(slots[(size_t)u * lmax + t] & 0xFFFFFFFFu);
       N.push_back({X.dist(u, v), v});  // recompute at path precision
     }
-    std::vector<uint32_t> lazy = robust_prune_lazy(X, N, R, an, ad);
+    std::vector<uint32_t> lazy = robust_prune_lazy(X, (uint32_t)u, N, R, an, ad);
     std::vector<uint32_t> eager = robust_prune_eager(X, (uint32_t)u, N, R, an, ad);
     if (lazy != eager) bad++;
     adj[u] = lazy;
@@ -734,7 +746,7 @@ int32_t or_robust_prune(const or_points* p, uint32_t x, const uint32_t* cands, i
   Data X(p);
   std::vector<std::pair<double, uint32_t>> N;
   for (int i = 0; i < nc; ++i) N.push_back({X.dist(x, cands[i]), cands[i]});
-  std::vector<uint32_t> E = lazy ? robust_prune_lazy(X, N, R, an, ad) : robust_prune_eager(X, x, N, R, an, ad);
+  std::vector<uint32_t> E = lazy ? robust_prune_lazy(X, x, N, R, an, ad) : robust_prune_eager(X, x, N, R, an, ad);
   std::copy(E.begin(), E.end(), out);
   return (int32_t)E.size();
 }

@@ -401,6 +401,78 @@ def test_robust_prune_eager_equals_lazy_and_diversity():
                 assert 6 * ((Xd[y] - Xd[z]) ** 2).sum() >= 5 * ((Xd[0] - Xd[z]) ** 2).sum()
 
 
+def _slot(hash16, bf16_bits, vid):
+    # reservoir slot layout of SURVEY §8(b): hash(16) | okey(bf16 dist)(16) | id(32); for a positive bf16 value
+    # okey(b) = b ^ 0x8000 (the sign bit set), written out by hand here
+    return (hash16 << 48) | ((bf16_bits ^ 0x8000) << 32) | vid
+
+
+def test_final_prune_zero_keeps_first_R_by_key():
+    # final_prune = 0 keeps the first R reservoir entries by (stored bf16 distance, id). Hand-built
+    # reservoir of point 0: dists 3.0 (0x4040), 1.0 (0x3F80), 2.0 (0x4000), 1.0 (0x3F80) for ids 7, 9, 4, 2,
+    # stored in hash order -> (1.0, 2), (1.0, 9), (2.0, 4), (3.0, 7).
+    X = np.zeros((10, 4), dtype=np.uint8)
+    ds = O.Dataset(X)
+    slots = np.full((10, 8), np.iinfo(np.uint64).max, dtype=np.uint64)
+    count = np.zeros(10, dtype=np.uint32)
+    row = [_slot(1, 0x4040, 7), _slot(3, 0x3F80, 9), _slot(5, 0x4000, 4), _slot(9, 0x3F80, 2)]
+    slots[0, :4] = np.array(row, dtype=np.uint64)
+    count[0] = 4
+    for R, want in [(3, [2, 9, 4]), (1, [2]), (8, [2, 9, 4, 7])]:
+        rp, ci, ok = O.final_prune(ds, slots, count, R, final=0)
+        assert ok and rp.tolist() == [0] + [len(want)] * 10 and ci.tolist() == want
+
+
+# MIPS final prune (R22, changed): candidates in the (-<u,c>, id) order, the alpha test on the angular
+# dissimilarity 1 - cos. Hand-computed 2-D example, u = (1, 0):
+#   a = (2, 0)  -<u,a> = -2, angle 0      b = (1, 1)  -<u,b> = -1, 1 - cos = 1 - 1/sqrt2 = 0.2929
+#   c = (0.9, 0.1)  -<u,c> = -0.9, 1 - cos(u,c) = 1 - 0.9/0.90554 = 0.00612   e = (0, 3)  -<u,e> = 0, 1 - cos = 1
+# order a, b, c, e. b: 1.2 (1 - cos(a,b)) = 0.3515 >= 0.2929 -> kept. c: 1.2 * 0.00612 (a is parallel to u)
+# >= 0.00612, and 1 - cos(b,c) = 1 - 1/(sqrt2 * 0.90554) = 0.2191 -> kept. e: 1.2 (1 - cos(b,e)) =
+# 1.2 * 0.2929 = 0.3515 < 1 -> pruned by b. Result [a, b, c]. (The signed rule 6 D(y,c) < 5 D(u,c) on
+# D = -<.,.> prunes b by a: -12 < -5; that is the collapse R22 fixes.)
+def test_robust_prune_mips_angular_hand_example():
+    ds = ds_of([[1, 0], [2, 0], [1, 1], [0.9, 0.1], [0, 3]], metric="mips", mode="exact")
+    for lazy in (True, False):
+        assert O.robust_prune(ds, 0, [4, 3, 2, 1], 64, (6, 5), lazy).tolist() == [1, 2, 3]
+        assert O.robust_prune(ds, 0, [4, 3, 2, 1], 2, (6, 5), lazy).tolist() == [1, 2]
+    # a zero-norm candidate z: cos taken as 0 (1 - cos = 1), so a (1 - cos(a,z) = 1, 1.2 >= 1) cannot prune it
+    dz = ds_of([[1, 0], [2, 0], [0, 0]], metric="mips", mode="exact")
+    assert O.robust_prune(dz, 0, [2, 1], 64, (6, 5)).tolist() == [1, 2]
+
+
+def test_robust_prune_mips_unit_norm_equals_l2():
+    # closed form: for unit vectors ||a - b||^2 = 2 (1 - <a,b>), so the (-<u,.>, id) order is the L2 order and
+    # alpha * (1 - cos) tests are the L2 tests halved: the MIPS prune must equal the (SPEC-pinned) L2 prune.
+    # Entries +-1/4 in d = 16 make every norm exactly 1 and every value exact in fp64 (ties included).
+    rng = np.random.default_rng(11)
+    for trial in range(200):
+        n = int(rng.integers(2, 40))
+        X = (rng.integers(0, 2, size=(n, 16)) * 0.5 - 0.25).astype(np.float32)
+        dm, dl = O.Dataset(X, "mips", "exact"), O.Dataset(X, "l2", "exact")
+        cands = rng.choice(np.arange(1, n), size=int(rng.integers(0, n - 1)), replace=False)
+        R = int(rng.integers(1, 12))
+        for lazy in (True, False):
+            assert O.robust_prune(dm, 0, cands, R, (6, 5), lazy).tolist() == \
+                O.robust_prune(dl, 0, cands, R, (6, 5), lazy).tolist()
+
+
+def test_build_mips_graph_is_navigable():
+    # C4-shaped (Text2Image) sample: the final prune keeps a usable out-degree and the graph reaches the
+    # exact neighbours (P:1044 reports PiPNN's highest maximum recall on the MIPS Text2Image set). Under the
+    # signed-value reading the mean out-degree was 1.09 and recall@10 0.23 at L = 128 on this sample.
+    cfg = synth.C4.scaled(20000, n_queries=300)
+    X, Q = synth.gen_points(cfg), synth.gen_queries(cfg)
+    ds = O.Dataset(X, metric="mips", mode="bf16")
+    r = O.build(ds, cfg.params())
+    assert r.check_failed == 0
+    deg = np.diff(r.row_ptr)
+    assert deg.mean() >= 10 and deg.max() <= cfg.R
+    truth, _ = O.brute_knn(ds, Q, 10)
+    res, _ = O.beam_search(ds, r.row_ptr, r.col_idx, Q, O.entry_point(ds), 128, 10)
+    assert O.recall_at(res, truth).mean() >= 0.9
+
+
 # ---------------------------------------------------------------- pipeline (Alg. 4)
 def test_build_n3():
     # n=3, C_max >= 3, k=2: one leaf, bidirected 2-NN connects all pairs, every out-degree 2
