@@ -3,10 +3,11 @@
 % roofline, recall@10).
 
 A step = one pipnn_build (all §8(a) rows: sketches, partition, leaf distance tiles + pick, HashPrune,
-final prune, CSR) over one synthetic input resident in HBM. Default workload: BASELINE.json configs[1]
-(C2: n=1M, d=128 uint8, L2, BIGANN-shaped mixture). Multi-GPU: one process per GPU (torchrun), each rank
-builds its own independent replica of the workload (the build does not shard),
-value = all ranks' points / max-over-ranks time.
+final prune, CSR) over one synthetic input resident in HBM. Default workload: BASELINE.json configs[4]
+(C5: n=50M, d=128 uint8, L2, BIGANN-shaped 100k-cluster mixture, C_max 2048, l_max 96, R 32 — the largest
+configuration that fits one GPU; configs[1..3] run with --config C2/C3/C4). Multi-GPU: one process per GPU
+(torchrun), each rank builds its own independent replica of the workload (the build does not shard;
+DESIGN.md "Multi-GPU"), value = all ranks' points / max-over-ranks time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
 
@@ -95,6 +96,87 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def int8_peak_tops(dev) -> float:
+    """Dense int8 tensor-core rate on this GPU, measured like MEASURED_PEAKS.json's bf16 figure (torch._int_mm
+    8192^3, best of 10 after 3 warm-ups, CUDA events)."""
+    import torch
+
+    N = 8192
+    a = torch.randint(-128, 127, (N, N), dtype=torch.int8, device=dev)
+    b = torch.randint(-128, 127, (N, N), dtype=torch.int8, device=dev).t().contiguous().t()
+    for _ in range(3):
+        torch._int_mm(a, b)
+    best = 1e30
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch._int_mm(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2 * N ** 3 / best / 1e9
+
+
+def exact_knn(Xd, Qd, metric, k=10, qids=None, xchunk=1 << 21, qchunk=2048):
+    """Exact k nearest of every query by a chunked fp32 GEMM over X (exact for uint8: every partial sum is an
+    integer < 2^24); qids: the queries are these base points, themselves excluded. -> ids int64 [nq, k]."""
+    import torch
+
+    torch.backends.cuda.matmul.allow_tf32 = False
+    n, nq = Xd.shape[0], Qd.shape[0]
+    out = torch.empty((nq, k), dtype=torch.int64, device=Xd.device)
+    for q0 in range(0, nq, qchunk):
+        Qf = Qd[q0:q0 + qchunk].float()
+        q2 = (Qf * Qf).sum(1, keepdim=True)
+        bd = torch.full((Qf.shape[0], k), float("inf"), device=Xd.device)
+        bi = torch.full((Qf.shape[0], k), -1, dtype=torch.int64, device=Xd.device)
+        for x0 in range(0, n, xchunk):
+            Xf = Xd[x0:x0 + xchunk].float()
+            D = -(Qf @ Xf.T) if metric == "mips" else q2 + (Xf * Xf).sum(1)[None] - 2 * (Qf @ Xf.T)
+            if qids is not None:
+                own = qids[q0:q0 + qchunk] - x0
+                r = torch.nonzero((own >= 0) & (own < Xf.shape[0])).flatten()
+                D[r, own[r]] = float("inf")
+            d, i = torch.topk(D, k, dim=1, largest=False)
+            cd, ci = torch.cat([bd, d], 1), torch.cat([bi, i + x0], 1)
+            bd, sel = torch.topk(cd, k, dim=1, largest=False)
+            bi = torch.gather(ci, 1, sel)
+            del D, Xf
+        out[q0:q0 + qchunk] = bi
+    return out
+
+
+def entry_point(Xd, metric, chunk=1 << 21) -> int:
+    """The point nearest the dataset mean by (D, id) (R25; MIPS: argmax <x, mean>), fp64, chunked."""
+    import torch
+
+    n = Xd.shape[0]
+    mean = torch.zeros(Xd.shape[1], dtype=torch.float64, device=Xd.device)
+    for x0 in range(0, n, chunk):
+        mean += Xd[x0:x0 + chunk].double().sum(0)
+    mean /= n
+    best, arg = None, 0
+    for x0 in range(0, n, chunk):
+        Xe = Xd[x0:x0 + chunk].double()
+        v = -(Xe @ mean) if metric == "mips" else ((Xe - mean) ** 2).sum(1)
+        j = int(torch.argmin(v).item())
+        if best is None or float(v[j]) < best:
+            best, arg = float(v[j]), x0 + j
+    return arg
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -129,7 +211,7 @@ def run_reference(args, cfg):
     import oracle as O
 
     n_s = args.ref_sample
-    sub = cfg.scaled(n_s) if n_s < cfg.n else cfg
+    sub = cfg.scaled(n_s, n_centres=cfg.n_centres) if n_s < cfg.n else cfg  # the workload's first n_s points
     X = synth.gen_points(sub)
     ds = O.Dataset(X, metric=cfg.metric, mode="bf16")
     times = []
@@ -146,56 +228,70 @@ def run_reference(args, cfg):
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64" if cfg.dtype != "u8" else "int64", "data": "synthetic",
             "config": workload_desc(cfg),
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu": cpu_model(),
                              "sample": f"oracle build (partition, leaf pick, HashPrune, final prune) of the first "
-                                       f"{sub.n:,} points of the {cfg.name} generator with the same parameters"},
+                                       f"{sub.n:,} points of the {cfg.name} workload with the same parameters"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(cfg, n_sample):
-    import oracle as O
+def cpu_baseline(cfg, n_sample, dev):
+    """The oracle, as it stands, on the workload's first n_sample points (same parameters) on the host cores;
+    the GPU builds the same sample and the two graphs are compared (identical CSR for uint8) and searched with
+    the same queries and entry point (paired recall@10)."""
+    import torch
 
-    sub = cfg.scaled(n_sample)
+    import oracle as O
+    import paper_2602_21247_b200 as P
+
+    sub = cfg.scaled(n_sample, n_centres=cfg.n_centres) if n_sample < cfg.n else cfg
     X = synth.gen_points(sub)
     ds = O.Dataset(X, metric=cfg.metric, mode="bf16")
     t0 = time.perf_counter()
-    O.build(ds, sub.params())
+    ref = O.build(ds, sub.params())
     dt = time.perf_counter() - t0
-    return {"value": sub.n / dt, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle",
-            "sample": f"oracle build of the first {sub.n:,} points of the {cfg.name} generator, same parameters "
+    base = {"value": sub.n / dt, "unit": UNIT, "cores": O.num_threads(), "kind": "oracle", "cpu": cpu_model(),
+            "sample": f"oracle build of the first {sub.n:,} points of the {cfg.name} workload, same parameters "
                       f"({dt:.1f} s)"}
+    Xd = torch.from_numpy(X).to(dev)
+    out = P.pipnn_build(Xd, P.build_params_from(sub.params()), metric=cfg.metric)
+    rp, ci = out.row_ptr.cpu().numpy(), out.col_idx.cpu().numpy().view(np.uint32)
+    same = bool(np.array_equal(rp, ref.row_ptr) and np.array_equal(ci, ref.col_idx))
+    Qd = torch.from_numpy(synth.gen_queries(cfg, n_queries=1000)).to(dev)
+    truth = exact_knn(Xd, Qd, cfg.metric)
+    e = entry_point(Xd, cfg.metric)
+    rows = {}
+    rpo = torch.from_numpy(ref.row_ptr.astype(np.int64)).to(dev)
+    cio = torch.from_numpy(ref.col_idx.view(np.int32)).to(dev)
+    for L in (10, 32, 64, 128):
+        a, _, _ = P.pipnn_search(Xd, out.row_ptr, out.col_idx, Qd, e, L, 10, cfg.metric)
+        b, _, _ = P.pipnn_search(Xd, rpo, cio, Qd, e, L, 10, cfg.metric)
+        ra = (a.long().unsqueeze(2) == truth.unsqueeze(1)).any(2).sum(1).double() / 10
+        rb = (b.long().unsqueeze(2) == truth.unsqueeze(1)).any(2).sum(1).double() / 10
+        d = ra - rb
+        rows[str(L)] = {"gpu": round(float(ra.mean()), 4), "oracle": round(float(rb.mean()), 4),
+                        "paired_diff": round(float(d.mean()), 5), "se": round(float(d.std() / len(d) ** 0.5), 5)}
+    parity = {"n": sub.n, "csr_identical": same, "gpu_edges": int(rp[-1]), "oracle_edges": int(ref.row_ptr[-1]),
+              "recall_at_10_paired": rows, "queries": 1000}
+    return base, parity
 
 
-def recall_eval(Xd, cfg, row_ptr, col_idx, n_queries):
+def recall_eval(Xd, cfg, row_ptr, col_idx, n_queries, knn_queries=1_000_000):
     """recall@10 of the GPU graph over the L sweep (evaluation harness, not the method): queries from the
-    config's generator, exact ground truth by a fp32 torch GEMM (exact for uint8 data), entry point = the point
-    nearest the dataset mean (R25), search by the library's batched beam search (pipnn_search,
-    Alg. 1); plus the search's throughput (queries/s, CUDA events) at each L."""
+    config's generator, exact ground truth by a chunked fp32 torch GEMM over X (exact for uint8 data), entry
+    point = the point nearest the dataset mean (R25), search by the library's batched beam search
+    (pipnn_search, Alg. 1); plus the search's throughput (queries/s, CUDA events) at each L. Then the k-NN-graph
+    task: base points queried on their own index, themselves excluded, over an L sweep up to the first
+    L reaching recall@10 >= 0.95 (or 256, the kernel's limit): points/s on the first knn_queries base points and
+    recall on 1,000 of them."""
     import torch
 
     import paper_2602_21247_b200 as P
 
     Q = synth.gen_queries(cfg, n_queries=n_queries)
     Qd = torch.from_numpy(Q).to(Xd.device)
-    torch.backends.cuda.matmul.allow_tf32 = False
-    Xf = Xd.float()
-    x2 = (Xf * Xf).sum(1)
-    truth = []
-    for s0 in range(0, len(Q), 1000):
-        Qf = Qd[s0:s0 + 1000].float()
-        if cfg.metric == "mips":
-            D = -(Qf @ Xf.T)
-        else:
-            D = (Qf * Qf).sum(1, keepdim=True) + x2[None] - 2 * (Qf @ Xf.T)
-        truth.append(torch.topk(D, 10, dim=1, largest=False).indices)
-    truth = torch.cat(truth)
-    Xe = Xd.double()
-    if cfg.metric == "mips":
-        entry = int(torch.argmax(Xe @ Xe.mean(0)).item())
-    else:
-        entry = int(torch.argmin(((Xe - Xe.mean(0)) ** 2).sum(1)).item())
-    del Xf, Xe
+    truth = exact_knn(Xd, Qd, cfg.metric)
+    entry = entry_point(Xd, cfg.metric)
     recall, qps = {}, {}
     for L in (10, 32, 64, 128):
         P.pipnn_search(Xd, row_ptr, col_idx, Qd[:100], entry, L, 10, cfg.metric)  # warm-up
@@ -207,26 +303,23 @@ def recall_eval(Xd, cfg, row_ptr, col_idx, n_queries):
         qps[str(L)] = round(len(Q) / (e0.elapsed_time(e1) / 1e3))
         hit = (ids.long().unsqueeze(2) == truth.unsqueeze(1)).any(2).sum(1).float() / 10.0
         recall[str(L)] = round(float(hit.mean().item()), 4)
-    # the k-NN-graph task: every base point queried on the index (itself excluded), L = 64;
-    # recall@10 on 1,000 sampled points against their exact 10 nearest other points
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    gids, _ = P.knn_graph(Xd, row_ptr, col_idx, entry, 10, 64, cfg.metric)
-    e1.record()
-    torch.cuda.synchronize()
-    knn_pps = Xd.shape[0] / (e0.elapsed_time(e1) / 1e3)
+    nk = min(Xd.shape[0], knn_queries)
     g = torch.Generator(device="cpu").manual_seed(5)
-    smp = torch.randperm(Xd.shape[0], generator=g)[:1000].to(Xd.device)
-    Xf = Xd.float()
-    Sf = Xf[smp]
-    if cfg.metric == "mips":
-        D = -(Sf @ Xf.T)
-    else:
-        D = (Sf * Sf).sum(1, keepdim=True) + (Xf * Xf).sum(1)[None] - 2 * (Sf @ Xf.T)
-    D[torch.arange(len(smp), device=D.device), smp] = float("inf")
-    gt = torch.topk(D, 10, dim=1, largest=False).indices
-    knn_rec = float(((gids[smp].long().unsqueeze(2) == gt.unsqueeze(1)).any(2).sum(1).float() / 10.0).mean().item())
-    return recall, qps, {"points_per_s": round(knn_pps), "L": 64, "k": 10, "recall_at_10_sample1000": round(knn_rec, 4)}
+    smp = torch.randperm(nk, generator=g)[:1000].to(Xd.device)
+    gt = exact_knn(Xd, Xd[smp], cfg.metric, qids=smp)
+    sweep = {}
+    for L in (64, 128, 256):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        gids, _, _ = P.pipnn_search(Xd, row_ptr, col_idx, Xd[:nk], entry, L, 10, cfg.metric, exclude_self=True)
+        e1.record()
+        torch.cuda.synchronize()
+        rec = float(((gids[smp].long().unsqueeze(2) == gt.unsqueeze(1)).any(2).sum(1).float() / 10.0).mean())
+        sweep[str(L)] = {"points_per_s": round(nk / (e0.elapsed_time(e1) / 1e3)), "recall_at_10_sample1000": round(rec, 4)}
+        if rec >= 0.95:
+            break
+    first = next((int(L) for L, v in sweep.items() if v["recall_at_10_sample1000"] >= 0.95), None)
+    return recall, qps, {"k": 10, "queried_points": nk, "L_sweep": sweep, "first_L_recall_ge_0.95": first}
 
 
 def main():
@@ -234,10 +327,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-sample", type=int, default=100_000)
     ap.add_argument("--cpu-sample", type=int, default=200_000)
+    ap.add_argument("--no-int8-peak", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--recall-queries", type=int, default=10000)
     args = ap.parse_args()
@@ -371,9 +465,18 @@ def main():
         st = stats[-1]
         tile_ms = statistics.mean(s["ms_leaf_tiles"] for s in stats)
         leaf_ops = 2.0 * st["leaf_pairs"] * cfg.d  # algorithmic: 2 s^2 d per leaf
+        int8_meas = None
         if cfg.dtype == "u8":
-            peak = 2.0 * peaks["bf16_tflops"]  # int8 dense = 2x bf16 (nominal ratio) x measured bf16 burst
-            peak_note = f"int8 = 2 x bf16 burst ({src} MEASURED_PEAKS.json), nominal ratio 4.5/2.25 PF"
+            proxy = 2.0 * peaks["bf16_tflops"]  # nominal ratio 4.5/2.25 PF x measured bf16 burst
+            if not args.no_int8_peak:
+                try:
+                    int8_meas = int8_peak_tops(dev)
+                except Exception:
+                    int8_meas = None
+            # the larger of the measured int8 GEMM rate and the nominal-ratio proxy (the conservative peak)
+            peak = max(proxy, int8_meas or 0.0)
+            peak_note = (f"int8: max(measured torch._int_mm 8192^3 = {int8_meas and round(int8_meas, 1)} TOP/s, "
+                         f"2 x bf16 burst {peaks['bf16_tflops']} ({src} MEASURED_PEAKS.json) = {proxy:.1f})")
         else:
             peak = peaks["bf16_tflops"]
             peak_note = f"bf16 burst ({src} MEASURED_PEAKS.json)"
@@ -386,6 +489,36 @@ def main():
                     traffic = json.load(f).get(cfg.name)
             except Exception:
                 traffic = None
+        # per-pass HBM: algorithmic bytes / the stage's device time, against the measured copy
+        # bandwidth. Occupied reservoir slots and degrees of the last build.
+        bb = builder.debug_buffers(Xd, st)
+        occ = int(bb["count"].long().sum().item())
+        E = st["n_edges"]
+        I = st["n_instances"]
+        ebytes = 1 if cfg.dtype == "u8" else 2  # the path's row precision (bf16 for float data)
+        row_b = cfg.d * ebytes
+        kb = -(-cfg.d // 32) * 32 if cfg.dtype == "u8" else -(-cfg.d // 16) * 32 + 32
+        ne = out.n_edges
+        stg = {k: statistics.mean(s[k] for s in stats) for k in ("ms_prep", "ms_partition", "ms_leaf",
+                                                               "ms_leaf_tiles", "ms_hashprune", "ms_final",
+                                                               "ms_total")}
+        hbm = peaks["hbm_gbs"]
+
+        def pas(nbytes, ms, what):
+            gbs = nbytes / (ms / 1e3) / 1e9 if ms > 0 else None
+            return {"algorithmic_bytes": int(nbytes), "ms": round(ms, 4), "achieved_gbs": gbs and round(gbs, 1),
+                    "peak_gbs": hbm, "frac": gbs and round(gbs / hbm, 4), "bytes": what}
+
+        hbm_passes = {
+            "leaf_gather": pas(I * (row_b + kb), stg["ms_leaf"] - stg["ms_leaf_tiles"],
+                               "X rows gathered (d x elem) + tiled rows written (Kb) per instance"),
+            "hashprune": pas(16 * E + 8 * occ + 4 * cfg.n, stg["ms_hashprune"],
+                             "8-B edge key written by the emit and read by the merge per streamed edge + 8 B per "
+                             "occupied slot written + count"),
+            "final_prune": pas(occ * (row_b + 8) + ne * 4 * 3 + cfg.n * 16, stg["ms_final"],
+                               "candidate rows gathered + reservoir slots read per occupied slot; admitted ids "
+                               "written, re-read and copied into the CSR; degree + row_ptr per point"),
+        }
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
@@ -395,11 +528,12 @@ def main():
             "roofline": {"bound": "tensor", "kernel": "dist_topk_kernel (leaf distance tiles + fused pick)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s" if cfg.dtype != "u8" else "TOP/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_note,
-                         "algorithmic_ops_per_launch": leaf_ops, "ms_per_launch": tile_ms},
-            "stages_ms": {k: round(statistics.mean(s[k] for s in stats), 4) for k in
-                          ("ms_prep", "ms_partition", "ms_leaf", "ms_leaf_tiles", "ms_hashprune", "ms_final",
-                           "ms_total")},
-            "counts": {k: st[k] for k in ("n_leaves", "n_instances", "n_edges", "max_leaf", "depth")},
+                         "algorithmic_ops_per_launch": leaf_ops, "ms_per_launch": tile_ms,
+                         "int8_measured_tops": int8_meas},
+            "hbm_passes": hbm_passes,
+            "stages_ms": {k: round(v, 4) for k, v in stg.items()},
+            "counts": {**{k: st[k] for k in ("n_leaves", "n_instances", "n_edges", "max_leaf", "depth")},
+                       "occupied_slots": occ, "graph_edges": int(ne)},
             "leaf_tflops": achieved,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(X.nbytes), "d2h_bytes_per_step": int(d2h),
                     "mode": e2e_mode, "serial_value": e2e_serial},
@@ -416,7 +550,12 @@ def main():
             except Exception as ex:  # evaluation is reported, never gates the timing
                 line["recall_at_10"] = f"failed: {ex}"
         if not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_sample)
+            try:
+                del builder
+                torch.cuda.empty_cache()
+                line["cpu_baseline"], line["sample_parity"] = cpu_baseline(cfg, args.cpu_sample, dev)
+            except Exception as ex:
+                line["cpu_baseline"] = f"failed: {ex}"
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()

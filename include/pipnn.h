@@ -76,7 +76,7 @@ typedef struct {
   uint64_t seed;
 } pipnn_partition_params;
 
-/* Leaf pick: bidirected k-NN inside every leaf. 1 <= k <= 32. */
+/* Leaf pick: bidirected k-NN inside every leaf. 1 <= k <= 15. */
 typedef struct {
   int32_t k;
 } pipnn_pick_params;
@@ -89,7 +89,8 @@ typedef struct {
 } pipnn_hashprune_params;
 
 /* Final prune: RobustPrune (Alg. 2) with alpha = alpha_num/alpha_den (1 <= terms <= 127, so
- * uint8 alpha tests stay exact in 32-bit integers) on the dissimilarity values, max degree R (1..256). final_prune = 0 keeps the R nearest reservoir entries instead. */
+ * uint8 alpha tests stay exact in 32-bit integers), max degree R (1..256). final_prune = 0 keeps the R
+ * nearest reservoir entries instead. */
 typedef struct {
   int32_t R;
   int32_t alpha_num, alpha_den;
@@ -168,8 +169,9 @@ PIPNN_API pipnn_status hashprune_insert(const pipnn_hashprune_params* p, int64_t
 
 /* Final prune (lazy form P:938-942): per point u, candidates = its reservoir, D(u,v)
  * recomputed at path precision, ascending by (D, v); admit c unless an admitted y has
- * alpha_num*D(y,c) < alpha_den*D(u,c); stop at R. Output CSR: row_ptr[n+1], col_idx (capacity n*R) in
- * admission order. */
+ * alpha_num*D'(y,c) < alpha_den*D'(u,c); stop at R. D' = D for L2; for MIPS the angular dissimilarity
+ * 1 - <a,b>/(||a|| ||b||) (R22: alpha >= 1 relaxes the test only on non-negative values). Output
+ * CSR: row_ptr[n+1], col_idx (capacity n*R) in admission order. */
 PIPNN_API pipnn_status pipnn_final_prune(const pipnn_points* X, const pipnn_hashprune_params* hp, const uint64_t* slots,
                                const uint32_t* count, const pipnn_prune_params* p, uint64_t* row_ptr,
                                uint32_t* col_idx, void* ws, size_t ws_bytes, void* stream);
@@ -179,6 +181,28 @@ PIPNN_API pipnn_status pipnn_final_prune(const pipnn_points* X, const pipnn_hash
  * Synchronises `stream`. */
 PIPNN_API pipnn_status pipnn_build(const pipnn_points* X, const pipnn_build_params* p, void* ws, size_t ws_bytes,
                          uint64_t* row_ptr, uint32_t* col_idx, int64_t* n_edges_h, pipnn_stats* stats_h, void* stream);
+
+/* Diagnostic (the stage-parity tests of the build path): device pointers to the intermediate artefacts the
+ * last pipnn_build with the same X and p left in its workspace `ws` — valid until `ws` is used again:
+ *   leaf_off [n_leaves+1] i64, leaf_ids [n_instances] u32 (the LeafSet, as pipnn_partition writes it);
+ *   cols [n_instances*k] u16: the picks of instance i as local columns of its leaf (0xFFFF = none), in
+ *     (D, id) order; dist [n_instances*k] f32: their D (n_leaves, n_instances from pipnn_stats);
+ *   sketch [n*m] (int32 for uint8, float32 otherwise); slots [n*l_max] u64 / count [n] u32: the HashPrune
+ *     reservoirs before the final prune, slot layout above; inside pipnn_build a reservoir is a set (the
+ *     final prune re-sorts it): its first count[u] slots are in hash order except for owners merged through
+ *     a sized hash table (more keys than one warp merges), and slots at or beyond count[u] are unspecified.
+ * Host-only: nothing is launched. */
+typedef struct {
+  int64_t* leaf_off;
+  uint32_t* leaf_ids;
+  uint16_t* cols;
+  float* dist;
+  void* sketch;
+  uint64_t* slots;
+  uint32_t* count;
+} pipnn_build_buffers;
+PIPNN_API pipnn_status pipnn_debug_build_buffers(const pipnn_points* X, const pipnn_build_params* p, void* ws,
+                                                 size_t ws_bytes, pipnn_build_buffers* out_h);
 
 /* Batched greedy beam search over a built graph (Alg. 1 BeamSearch), the
  * query side of the k-NN-graph / ANN tasks. Per query: beam of the L best (D, id) seen, start

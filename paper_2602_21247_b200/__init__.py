@@ -63,6 +63,11 @@ class SearchParams(C.Structure):
     _fields_ = [("L", C.c_int32), ("k", C.c_int32), ("exclude_self", C.c_int32)]
 
 
+class BuildBuffers(C.Structure):
+    _fields_ = [("leaf_off", C.c_void_p), ("leaf_ids", C.c_void_p), ("cols", C.c_void_p), ("dist", C.c_void_p),
+                ("sketch", C.c_void_p), ("slots", C.c_void_p), ("count", C.c_void_p)]
+
+
 class BuildParams(C.Structure):
     _fields_ = [("part", PartitionParams), ("pick", PickParams), ("hp", HashPruneParams), ("prune", PruneParams)]
 
@@ -97,13 +102,14 @@ _lib.pipnn_final_prune.argtypes = [_P(Points), _P(HashPruneParams), _vp, _vp, _P
 _lib.pipnn_build.argtypes = [_P(Points), _P(BuildParams), _vp, C.c_size_t, _vp, _vp, _P(C.c_int64), _P(Stats), _vp]
 _lib.pipnn_search.argtypes = [_P(Points), _vp, _vp, _vp, C.c_int64, C.c_int64, C.c_uint32, _P(SearchParams), _vp, _vp,
                               _vp, _vp, C.c_size_t, _vp]
-for _f in ("pipnn_workspace_size", "pipnn_partition", "pipnn_leaf_pick", "pipnn_sketch", "pipnn_device_error",
+_lib.pipnn_debug_build_buffers.argtypes = [_P(Points), _P(BuildParams), _vp, C.c_size_t, _P(BuildBuffers)]
+for _f in ("pipnn_debug_build_buffers", "pipnn_workspace_size", "pipnn_partition", "pipnn_leaf_pick", "pipnn_sketch", "pipnn_device_error",
            "hashprune_insert", "pipnn_final_prune", "pipnn_build", "pipnn_search"):
     getattr(_lib, _f).restype = C.c_int
 
 EXPORTS = ("pipnn_last_error", "pipnn_abi_version", "pipnn_required_workspace", "pipnn_launch_count", "pipnn_workspace_size",
            "pipnn_partition", "pipnn_leaf_pick", "pipnn_sketch", "pipnn_device_error", "hashprune_insert",
-           "pipnn_final_prune", "pipnn_build")
+           "pipnn_final_prune", "pipnn_build", "pipnn_search", "pipnn_debug_build_buffers")
 
 
 def lib():
@@ -358,6 +364,31 @@ class Builder:
         _check(_lib.pipnn_build(C.byref(pts), C.byref(self.params), _ptr(self.ws), self.ws_bytes, _ptr(self.row_ptr),
                                 _ptr(self.col_idx), C.byref(ne), C.byref(stats), _stream(stream)))
         return BuildOut(self.row_ptr, self.col_idx[: ne.value], ne.value, stats.as_dict())
+
+
+    def debug_buffers(self, X: torch.Tensor, stats: dict) -> dict:
+        """The last build's intermediate artefacts (pipnn_debug_build_buffers) as tensor views of the workspace:
+        leaf_off, leaf_ids, cols (int16 bits of u16 local columns, [I, k]), dist [I, k], sketch [n, m],
+        slots (int64 bits of u64) [n, l_max], count [n]."""
+        pts = points(X, self.metric)
+        b = BuildBuffers()
+        _check(_lib.pipnn_debug_build_buffers(C.byref(pts), C.byref(self.params), _ptr(self.ws), self.ws_bytes,
+                                              C.byref(b)))
+        base = self.ws.data_ptr()
+        n, k = X.shape[0], self.params.pick.k
+        nl, ni = stats["n_leaves"], stats["n_instances"]
+        m, lm = self.params.hp.m, self.params.hp.l_max
+
+        def view(ptr, count, dtype):
+            esz = torch.empty(0, dtype=dtype).element_size()
+            off = ptr - base
+            return self.ws[off: off + count * esz].view(dtype)
+
+        skd = torch.int32 if X.dtype == torch.uint8 else torch.float32
+        return {"leaf_off": view(b.leaf_off, nl + 1, torch.int64), "leaf_ids": view(b.leaf_ids, ni, torch.int32),
+                "cols": view(b.cols, ni * k, torch.int16).view(ni, k), "dist": view(b.dist, ni * k, torch.float32).view(ni, k),
+                "sketch": view(b.sketch, n * m, skd).view(n, m), "slots": view(b.slots, n * lm, torch.int64).view(n, lm),
+                "count": view(b.count, n, torch.int32)}
 
 
 def pipnn_build(X: torch.Tensor, params: BuildParams, metric="l2", stream=None) -> BuildOut:

@@ -36,6 +36,8 @@ pipnn_status validate_points(const pipnn_points* X) {
   if (X->n > 0xFFFFFFFEll) return fail(PIPNN_EUNSUPPORTED, "n must fit in 32-bit ids");
   if (X->d < 1 || X->ld < X->d) return fail(PIPNN_EINVAL, "need d >= 1 and ld >= d");
   if (!X->data) return fail(PIPNN_EINVAL, "X->data is NULL");
+  // the row loads are 16-B vectors (uint8 rows with 16-B-multiple strides, float4 for float rows)
+  if ((reinterpret_cast<uintptr_t>(X->data) & 15) != 0) return fail(PIPNN_EINVAL, "X->data must be 16-B aligned");
   if (X->dtype != PIPNN_U8 && X->dtype != PIPNN_F32) return fail(PIPNN_EINVAL, "dtype must be PIPNN_U8 or PIPNN_F32");
   if (X->metric != PIPNN_L2 && X->metric != PIPNN_MIPS) return fail(PIPNN_EINVAL, "metric must be L2 or MIPS");
   if (X->dtype == PIPNN_U8 && X->metric == PIPNN_MIPS) return fail(PIPNN_EINVAL, "uint8 + MIPS is not supported (S:27)");
@@ -236,20 +238,47 @@ uint8_t* pinned_scratch(size_t bytes) {
   return s.p;
 }
 
+// The build's long-lived buffers, taken first from its workspace in this order (pipnn_debug_build_buffers
+// replays the same takes to find them after a build).
+struct BuildBufs {
+  int* err;
+  int64_t* leaf_off;
+  uint32_t* leaf_ids;
+  uint16_t* cols;  // picks as local leaf columns [I * k]
+  float* dist;     // their D [I * k]
+  void* sketch;
+  uint64_t* slots;
+  uint32_t* count;
+};
+static BuildBufs take_build_bufs(const pipnn_points* X, const pipnn_build_params* p, Arena& ar) {
+  const BuildPlan bp = plan_of(X, p);
+  BuildBufs b;
+  b.err = err_slot(ar);
+  b.leaf_off = ar.take<int64_t>(bp.leaf_off_cap);
+  b.leaf_ids = ar.take<uint32_t>(bp.leaf_ids_cap);
+  b.cols = ar.take<uint16_t>((size_t)bp.leaf_ids_cap * p->pick.k);
+  b.dist = ar.take<float>((size_t)bp.leaf_ids_cap * p->pick.k);
+  b.sketch = ar.take<int32_t>((size_t)X->n * p->hp.m);
+  b.slots = ar.take<uint64_t>((size_t)X->n * p->hp.l_max);
+  b.count = ar.take<uint32_t>(X->n);
+  return b;
+}
+
 static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* p, Arena& ar, cudaStream_t st,
                                uint64_t* row_ptr, uint32_t* col_idx, int64_t* n_edges_h, pipnn_stats* stats_h) {
   const BuildPlan bp = plan_of(X, p);
-  int* err = err_slot(ar);
+  const BuildBufs B = take_build_bufs(X, p, ar);
+  int* err = B.err;
   Ctx c{st, err};
-  int64_t* leaf_off = ar.take<int64_t>(bp.leaf_off_cap);
-  uint32_t* leaf_ids = ar.take<uint32_t>(bp.leaf_ids_cap);
+  int64_t* leaf_off = B.leaf_off;
+  uint32_t* leaf_ids = B.leaf_ids;
   const int k = p->pick.k;
-  uint16_t* cols = ar.take<uint16_t>((size_t)bp.leaf_ids_cap * k);  // picks as local leaf columns
-  float* dist = ar.take<float>((size_t)bp.leaf_ids_cap * k);
+  uint16_t* cols = B.cols;
+  float* dist = B.dist;
   const bool sk_int = X->dtype == PIPNN_U8;
-  void* sketch = ar.take<int32_t>((size_t)X->n * p->hp.m);
-  uint64_t* slots = ar.take<uint64_t>((size_t)X->n * p->hp.l_max);
-  uint32_t* count = ar.take<uint32_t>(X->n);
+  void* sketch = B.sketch;
+  uint64_t* slots = B.slots;
+  uint32_t* count = B.count;
   int64_t* n_edges_dev = ar.take<int64_t>(1);
   // float data: one bf16 (RNE) copy of X, made in prep; every later stage gathers its rows (R19)
   const bool is_float = X->dtype != PIPNN_U8;
@@ -577,6 +606,24 @@ pipnn_status pipnn_build(const pipnn_points* X, const pipnn_build_params* p, voi
   PIPNN_TRY(pending_cuda());
   Arena ar(ws, ws_bytes);
   return build_impl(X, p, ar, (cudaStream_t)stream, row_ptr, col_idx, n_edges_h, stats_h);
+}
+
+pipnn_status pipnn_debug_build_buffers(const pipnn_points* X, const pipnn_build_params* p, void* ws, size_t ws_bytes,
+                                       pipnn_build_buffers* out_h) {
+  size_t need = 0;
+  PIPNN_TRY(pipnn_workspace_size(X, p, &need));
+  if (!out_h) return fail(PIPNN_EINVAL, "NULL output");
+  PIPNN_TRY(check_ws(ws, ws_bytes, need - 4096));
+  Arena ar(ws, ws_bytes);
+  const BuildBufs b = take_build_bufs(X, p, ar);
+  out_h->leaf_off = b.leaf_off;
+  out_h->leaf_ids = b.leaf_ids;
+  out_h->cols = b.cols;
+  out_h->dist = b.dist;
+  out_h->sketch = b.sketch;
+  out_h->slots = b.slots;
+  out_h->count = b.count;
+  return PIPNN_OK;
 }
 
 pipnn_status pipnn_search(const pipnn_points* X, const uint64_t* row_ptr, const uint32_t* col_idx,

@@ -4,7 +4,8 @@
 //      coordinates of float rows: the path precision of DESIGN.md R19/R24);
 //   2. the (c+1)x(c+1) Gram on the tensor cores with warp-level MMAs (u8 x u8 -> s32, exact; bf16 -> f32);
 //      D(r,s) = G_rr + G_ss - 2 G_rs (L2), -G_rs (MIPS);
-//   3. prune bitmasks (alpha_num*D(y,c) < alpha_den*D(u,c)) and the (D(u,.), id) order (R4);
+//   3. prune bitmasks (alpha_num*D'(y,c) < alpha_den*D'(u,c)) and the (D(u,.), id) order (R4), where
+//      D' = D for L2 and the angular dissimilarity 1 - G_rs / sqrt(G_rr G_ss) for MIPS (R22);
 //   4. the lazy scan: admit c unless an admitted earlier y prunes it; stop at R.
 // Tiers by reservoir occupancy, each a kernel shaped for its size:
 //   <= 31 candidates : one warp per point — fp_gram_kernel (uint8: Gram in SMEM, fixpoint over ballots) or
@@ -12,8 +13,7 @@
 //                      sort, sequential scan over shuffles);
 //   <= 63, <= 127,   : fp_band_kernel (a warp per 16-row Gram band, masks from the fragments and the
 //   <= 191             candidates' ranks in the band warps, a scan warp that resolves 32-candidate batches
-//                      as ballot fixpoints while the band warps start the next point); PIPNN_FP_COOP=1 selects
-//                      the older fp_coop_kernel (a CTA of W warps, Gram in SMEM) for the 63 and 127 tiers;
+//                      as ballot fixpoints while the band warps start the next point);
 //   larger           : the generic final_prune_kernel.
 // final_prune = 0 (keep the R nearest reservoir entries) uses the generic kernel.
 // Then row_ptr = exclusive scan of the degrees and a coalesced copy into col_idx.
@@ -35,6 +35,11 @@ __device__ __forceinline__ uint32_t f_ord(float f) {
 __device__ __forceinline__ float f_unord(uint32_t o) {
   return __uint_as_float(o ^ ((o & 0x80000000u) ? 0x80000000u : 0xFFFFFFFFu));
 }
+
+// MIPS prune dissimilarity (R22): 1 - <a,b> inv(a) inv(b), inv = 1/||.|| (0 for a zero vector, so
+// cos = 0 and the dissimilarity is 1, as in the oracle)
+__device__ __forceinline__ float inv_norm(float nn) { return nn > 0.0f ? 1.0f / sqrtf(nn) : 0.0f; }
+__device__ __forceinline__ float ang_d(float dot, float ia, float ib) { return 1.0f - dot * ia * ib; }
 
 // distance between two staged rows (nw 32-bit words each)
 template <bool U8, bool MIPS>
@@ -88,6 +93,22 @@ __device__ __forceinline__ float warp_row_dist(const void* Xv, int64_t ld, int d
   }
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   return MIPS ? -acc : acc;
+}
+
+// the prune dissimilarity D' of two staged rows (D itself for L2; angular for MIPS, R22)
+template <bool U8, bool MIPS>
+__device__ __forceinline__ float srow_pd(const uint32_t* a, const uint32_t* b, int nw) {
+  if (!MIPS) return srow_dist<U8, MIPS>(a, b, nw);
+  const float ab = -srow_dist<U8, MIPS>(a, b, nw), aa = -srow_dist<U8, MIPS>(a, a, nw),
+              bb = -srow_dist<U8, MIPS>(b, b, nw);
+  return ang_d(ab, inv_norm(aa), inv_norm(bb));
+}
+template <bool U8, bool MIPS>
+__device__ __forceinline__ float warp_row_pd(const void* Xv, int64_t ld, int d, uint32_t a, uint32_t b, int lane) {
+  if (!MIPS) return warp_row_dist<U8, MIPS>(Xv, ld, d, a, b, lane);
+  const float ab = -warp_row_dist<U8, MIPS>(Xv, ld, d, a, b, lane), aa = -warp_row_dist<U8, MIPS>(Xv, ld, d, a, a, lane),
+              bb = -warp_row_dist<U8, MIPS>(Xv, ld, d, b, b, lane);
+  return ang_d(ab, inv_norm(aa), inv_norm(bb));
 }
 
 // stage rows sids[0..c) into rows[r*sw], and sids[cap] (the point itself) into rows[cap*sw];
@@ -293,7 +314,7 @@ __global__ void final_prune_kernel(const void* __restrict__ Xv, int64_t n, int d
       const int npairs = c * (c - 1) / 2;
       for (int p = lane; p < npairs; p += 32) {
         const int i = pairs[2 * p], j = pairs[2 * p + 1];
-        const float D = srow_dist<U8, MIPS>(rows + (size_t)vals[i] * sw, rows + (size_t)vals[j] * sw, nw);
+        const float D = srow_pd<U8, MIPS>(rows + (size_t)vals[i] * sw, rows + (size_t)vals[j] * sw, nw);
         gram[i * kFpStage + j] = D;
         gram[j * kFpStage + i] = D;
       }
@@ -303,7 +324,10 @@ __global__ void final_prune_kernel(const void* __restrict__ Xv, int64_t n, int d
     for (int i = 0; i < c && na < R; ++i) {
       const uint64_t ki = keys[i];
       const uint32_t vi = (uint32_t)(ki & 0xFFFFFFFFu);
-      const float Dui = U8 ? (float)(uint32_t)(ki >> 32) : f_unord((uint32_t)(ki >> 32));
+      float Dui = U8 ? (float)(uint32_t)(ki >> 32) : f_unord((uint32_t)(ki >> 32));
+      if (MIPS)  // the prune test's D'(u, i)
+        Dui = (use_gram || staged) ? srow_pd<U8, MIPS>(urow, rows + (size_t)vals[i] * sw, nw)
+                                   : warp_row_pd<U8, MIPS>(Xv, ld, d, (uint32_t)u, vi, lane);
       bool pr = false;
       if (use_gram) {
         for (int a0 = 0; a0 < na && !pr; a0 += 32) {
@@ -317,12 +341,12 @@ __global__ void final_prune_kernel(const void* __restrict__ Xv, int64_t n, int d
         for (int a0 = 0; a0 < na && !pr; a0 += 32) {
           bool mine = false;
           if (a0 + lane < na)
-            mine = prunes<U8>(srow_dist<U8, MIPS>(rows + (size_t)vals[adm[a0 + lane]] * sw, ri, nw), Dui, an, ad);
+            mine = prunes<U8>(srow_pd<U8, MIPS>(rows + (size_t)vals[adm[a0 + lane]] * sw, ri, nw), Dui, an, ad);
           pr = __any_sync(0xffffffffu, mine);
         }
       } else {
         for (int a = 0; a < na && !pr; ++a) {
-          const float Dyi = warp_row_dist<U8, MIPS>(Xv, ld, d, (uint32_t)(keys[adm[a]] & 0xFFFFFFFFu), vi, lane);
+          const float Dyi = warp_row_pd<U8, MIPS>(Xv, ld, d, (uint32_t)(keys[adm[a]] & 0xFFFFFFFFu), vi, lane);
           pr = prunes<U8>(Dyi, Dui, an, ad);
         }
       }
@@ -494,6 +518,7 @@ __global__ void __launch_bounds__(256, CP == 32 ? 3 : 1) fp_gram_kernel(const vo
                                                       uint32_t* __restrict__ defer, uint32_t* __restrict__ defer_n,
                                                       int src_bf16) {
   using DT = typename std::conditional<U8, int32_t, float>::type;
+  static_assert(U8 && !MIPS, "the Gram-in-SMEM warp tier serves uint8 (L2) only; float uses fp_warp_kernel");
   constexpr int E = CP / 32;  // sorted candidates per lane; also the bitmask words per candidate
   extern __shared__ __align__(16) uint8_t gsm[];
   const GpLayout L = gp_layout(d, U8, CP);
@@ -742,201 +767,6 @@ __device__ __forceinline__ void gp_stage_group(const void* __restrict__ Xv, int6
   }
 }
 
-// One point per CTA of W = CP/32 warps (the larger reservoirs): the warps split the Gram bands, warp w owns
-// candidates 32w .. 32w+31 (one per lane), and the fixpoint of the lazy scan runs over shared admitted /
-// rejected masks with a CTA barrier per round. Same arithmetic and order rules as fp_gram_kernel.
-template <bool U8, bool MIPS, int CP>
-__global__ void __launch_bounds__(CP) fp_coop_kernel(const void* __restrict__ Xv, int64_t n, int d, int64_t ld,
-                                                     int l_max, const uint64_t* __restrict__ slots,
-                                                     const uint32_t* __restrict__ count, int R, int an, int ad,
-                                                     uint32_t* __restrict__ nbr_tmp, uint32_t* __restrict__ deg,
-                                                     const uint32_t* __restrict__ list,
-                                                     const uint32_t* __restrict__ list_n,
-                                                     uint32_t* __restrict__ defer, uint32_t* __restrict__ defer_n,
-                                                     int src_bf16) {
-  using DT = typename std::conditional<U8, int32_t, float>::type;
-  constexpr int W = CP / 32;
-  extern __shared__ __align__(16) uint8_t csm[];
-  __shared__ uint64_t skeys[CP];
-  __shared__ uint32_t sKA[W], sKR[W];
-  __shared__ int s_done;
-  const GpLayout L = gp_layout(d, U8, CP);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint8_t* rows = csm + L.rows_off;
-  DT* G = (DT*)(csm + L.g_off);
-  DT* nrm = (DT*)(csm + L.nrm_off);
-  uint32_t* ids = (uint32_t*)(csm + L.ids_off);
-  const int DS = CP + 1;
-  const int g = lane >> 2, t4 = lane & 3;
-  const int64_t n_iter = list ? (int64_t)*list_n : n;
-  for (int64_t it = blockIdx.x; it < n_iter; it += gridDim.x) {
-    const int64_t u = list ? (int64_t)list[it] : it;
-    const int c = (int)count[u];
-    if (c > CP - 1) {
-      if (tid == 0) defer[atomicAdd(defer_n, 1u)] = (uint32_t)u;
-      continue;
-    }
-    uint32_t* out = nbr_tmp + u * (int64_t)R;
-    if (c == 0) {
-      if (tid == 0) deg[u] = 0;
-      continue;
-    }
-    const uint64_t* res = slots + u * (int64_t)l_max;
-    const int nr = c + 1, nrp = (nr + 15) & ~15;
-    __syncthreads();  // the previous point's SMEM is free
-    for (int t = tid; t < nr; t += CP) ids[t] = t == 0 ? (uint32_t)u : (uint32_t)(res[t - 1] & 0xFFFFFFFFu);
-    __syncthreads();
-    // ---- Gram (bands of 16 rows split over the warps), K in chunks of <= 128 B
-    const int nb16 = nrp >> 4;
-    const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 16;
-    for (int kc0 = 0; kc0 < L.Kb; kc0 += L.Kc) {
-      const int kcn = min(L.Kc, L.Kb - kc0);
-      gp_stage_group<U8>(Xv, ld, d, ids, nr, nrp, rows, L, tid, CP, src_bf16, kc0);
-      __syncthreads();
-      for (int bi = warp; bi < nb16; bi += W) {
-        int32_t acc[CP / 8][4];
-#pragma unroll
-        for (int bj = 0; bj < CP / 8; ++bj) acc[bj][0] = acc[bj][1] = acc[bj][2] = acc[bj][3] = 0;
-        const uint8_t* ra = rows + (size_t)(bi * 16 + lrow) * L.pitch + lcol;
-        for (int kb = 0; kb < kcn; kb += 32) {
-          uint32_t a[4];
-          ldsm_x4(a, ra + kb);
-#pragma unroll
-          for (int bj2 = 0; bj2 < CP / 16; ++bj2) {
-            if (bj2 < nb16) {
-              uint32_t bb[4];
-              ldsm_x4(bb, rows + (size_t)(bj2 * 16 + lrow) * L.pitch + lcol + kb);
-              const uint32_t b0[2] = {bb[0], bb[2]}, b1[2] = {bb[1], bb[3]};
-              mma_16x8<U8>(acc[2 * bj2], a, b0);
-              mma_16x8<U8>(acc[2 * bj2 + 1], a, b1);
-            }
-          }
-        }
-#pragma unroll
-        for (int bj = 0; bj < CP / 8; ++bj) {
-          if (bj < 2 * nb16) {
-            const int r = bi * 16 + g, sc = bj * 8 + 2 * t4;
-            DT* d0 = G + (size_t)r * DS + sc;
-            DT* d1 = G + (size_t)(r + 8) * DS + sc;
-            DT x0, x1, x2, x3;
-            if (U8) {
-              x0 = acc[bj][0]; x1 = acc[bj][1]; x2 = acc[bj][2]; x3 = acc[bj][3];
-            } else {
-              x0 = __int_as_float(acc[bj][0]); x1 = __int_as_float(acc[bj][1]);
-              x2 = __int_as_float(acc[bj][2]); x3 = __int_as_float(acc[bj][3]);
-            }
-            if (kc0 == 0) {
-              d0[0] = x0; d0[1] = x1; d1[0] = x2; d1[1] = x3;
-            } else {
-              d0[0] += x0; d0[1] += x1; d1[0] += x2; d1[1] += x3;
-            }
-          }
-        }
-      }
-      __syncthreads();
-    }
-    for (int r = tid; r < nr; r += CP) nrm[r] = MIPS ? (DT)0 : G[(size_t)r * DS + r];
-    __syncthreads();
-    auto Dof = [&](int r, int sc, DT nr_, DT ns_) -> DT {
-      const DT gg = G[(size_t)r * DS + sc];
-      if (MIPS) return -gg;
-      if (U8) return nr_ + ns_ - 2 * gg;
-      return fmaxf(nr_ + ns_ - 2.0f * gg, 0.0f);
-    };
-    // ---- candidate i = tid (warp w, lane l): key (D(u,v), v), threshold ad * D(u, v)
-    const int i = tid;
-    uint64_t key = ~0ull;
-    DT ni = 0;
-    uint32_t thr_i = 0;
-    float thr_f = 0.0f;
-    if (i < c) {
-      ni = nrm[i + 1];
-      const DT Du = Dof(0, i + 1, nrm[0], ni);
-      key = ((uint64_t)(U8 ? (uint32_t)Du : f_ord((float)Du)) << 32) | ids[i + 1];
-      if (U8) thr_i = (uint32_t)ad * (uint32_t)Du;
-      else thr_f = (float)ad * (float)Du;
-    }
-    skeys[i] = key;
-    __syncthreads();
-    uint32_t Pm[W], M[W];
-#pragma unroll
-    for (int w = 0; w < W; ++w) Pm[w] = M[w] = 0u;
-    for (int y = 0; y < c; ++y) {
-      const uint64_t ky = skeys[y];
-      const DT ny = nrm[y + 1];
-      const bool prec = ky < key;
-      const DT Dyi = Dof(y + 1, i + 1, ny, ni);
-      bool p;
-      if (U8) p = (uint32_t)an * (uint32_t)Dyi < thr_i;
-      else p = (float)an * (float)Dyi < thr_f;
-      const uint32_t bit = 1u << (y & 31);
-#pragma unroll
-      for (int w = 0; w < W; ++w)
-        if (w == (y >> 5) && prec) {
-          Pm[w] |= bit;
-          if (p) M[w] |= bit;
-        }
-    }
-    // ---- fixpoint over shared admitted / rejected masks
-    if (tid < W) {
-      const int valid = min(32, max(0, c - 32 * tid));
-      sKA[tid] = 0u;
-      sKR[tid] = valid == 32 ? 0u : ~((1u << valid) - 1u);
-    }
-    __syncthreads();
-    for (int round = 0; round < c; ++round) {
-      uint32_t KA[W], KR[W];
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        KA[w] = sKA[w];
-        KR[w] = sKR[w];
-      }
-      uint32_t myKA = 0u, myKR = 0u;  // (static register indices: no local-memory arrays)
-#pragma unroll
-      for (int w = 0; w < W; ++w)
-        if (w == warp) {
-          myKA = KA[w];
-          myKR = KR[w];
-        }
-      const bool undecided = !((myKA | myKR) >> lane & 1u);
-      bool hit = false, open = false;
-#pragma unroll
-      for (int w = 0; w < W; ++w) {
-        hit |= (M[w] & KA[w]) != 0u;
-        open |= (M[w] & ~KR[w]) != 0u;
-      }
-      const uint32_t adm = __ballot_sync(0xffffffffu, undecided && !hit && !open);
-      const uint32_t rej = __ballot_sync(0xffffffffu, undecided && hit);
-      __syncthreads();  // everyone has read the masks of this round
-      if (lane == 0) {
-        sKA[warp] = myKA | adm;
-        sKR[warp] = myKR | rej;
-      }
-      if (tid == 0) s_done = 1;
-      __syncthreads();
-      if (lane == 0 && (sKA[warp] | sKR[warp]) != 0xFFFFFFFFu) s_done = 0;
-      __syncthreads();
-      if (s_done) break;
-    }
-    // ---- output
-    uint32_t KA[W], myKA = 0u;
-    int na = 0;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
-      KA[w] = sKA[w];
-      na += __popc(KA[w]);
-      if (w == warp) myKA = KA[w];
-    }
-    if (myKA >> lane & 1u) {
-      int rank = 0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) rank += __popc(KA[w] & Pm[w]);
-      if (rank < R) out[rank] = (uint32_t)(key & 0xFFFFFFFFu);
-    }
-    if (tid == 0) deg[u] = (uint32_t)min(na, R);
-  }
-}
-
 // ------------------------------------------------------------------ warp tier (<= 31 candidates)
 // One warp per point, everything in registers but the staged rows: lane t <-> Gram index t (0 = u, 1..c the
 // candidates). The 32x32 Gram (two 16-row bands x four 8-column blocks of mma.sync fragments) stays in the
@@ -981,10 +811,15 @@ __global__ void __launch_bounds__(256, 3) fp_warp_kernel(const void* __restrict_
   const bool fast = U8 ? ((d & 15) == 0 && (ld & 15) == 0) : (src_bf16 != 0);
   const int64_t rowbytes = U8 ? ld : (src_bf16 ? 2 * ld : 4 * ld);
   const int lim = U8 ? d : (src_bf16 ? (int)(2 * ld) : 2 * d);  // staged bytes that come from the source row
+  // D (the order key) and D' (the prune test); norms are squared norms for L2, inverse norms for MIPS
   auto Dof = [](DT gg, DT na_, DT nb_) -> DT {
     if (MIPS) return -gg;
     if (U8) return na_ + nb_ - 2 * gg;
     return fmaxf(na_ + nb_ - 2.0f * gg, 0.0f);
+  };
+  auto Dpr = [&](DT gg, DT na_, DT nb_) -> DT {
+    if (MIPS) return (DT)ang_d((float)gg, (float)na_, (float)nb_);
+    return Dof(gg, na_, nb_);
   };
   auto val = [](int32_t x) -> DT {
     if (U8) return (DT)x;
@@ -1115,20 +950,20 @@ __global__ void __launch_bounds__(256, 3) fp_warp_kernel(const void* __restrict_
     }
     __syncwarp();
     // ---- lane i: key (D(u,i), id) and threshold ad*D(u,i)
-    const DT n_me = MIPS ? (DT)0 : nrm[lane];
-    const DT n_u = MIPS ? (DT)0 : nrm[0];
+    const DT n_me = MIPS ? (DT)inv_norm((float)nrm[lane]) : nrm[lane];
+    const DT n_u = MIPS ? (DT)inv_norm((float)nrm[0]) : nrm[0];
     const DT Du = Dof(g0[lane], n_u, n_me);
     const bool cand_ok = lane >= 1 && lane <= c;
     const uint64_t key = cand_ok ? (((uint64_t)(U8 ? (uint32_t)Du : f_ord((float)Du)) << 32) | my_id) : ~0ull;
     DT thr_me;
     if (U8) thr_me = (DT)((uint32_t)ad * (uint32_t)Du);
-    else thr_me = (DT)((float)ad * (float)Du);
+    else thr_me = (DT)((float)ad * (float)Dpr(g0[lane], n_u, n_me));
     // ---- prune bits of rows r = 16b + 8h + g, columns y = 8bj + 2t4 + e
     DT nyv[4][2];
 #pragma unroll
     for (int bj = 0; bj < 4; ++bj)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) nyv[bj][e] = MIPS ? (DT)0 : __shfl_sync(0xffffffffu, n_me, 8 * bj + 2 * t4 + e);
+      for (int e = 0; e < 2; ++e) nyv[bj][e] = __shfl_sync(0xffffffffu, n_me, 8 * bj + 2 * t4 + e);
     const uint32_t ymask = ((c >= 31) ? 0xFFFFFFFFu : ((2u << c) - 1u)) & ~1u;  // candidates 1..c
     uint32_t mrow[2][2] = {{0u, 0u}, {0u, 0u}};
 #pragma unroll
@@ -1137,7 +972,7 @@ __global__ void __launch_bounds__(256, 3) fp_warp_kernel(const void* __restrict_
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = 16 * b + 8 * h + g;
-        const DT nr_ = MIPS ? (DT)0 : __shfl_sync(0xffffffffu, n_me, r);
+        const DT nr_ = __shfl_sync(0xffffffffu, n_me, r);
         const DT th = __shfl_sync(0xffffffffu, thr_me, r);
         uint32_t w = 0u;
 #pragma unroll
@@ -1145,7 +980,7 @@ __global__ void __launch_bounds__(256, 3) fp_warp_kernel(const void* __restrict_
           if (bj >= 2 && !two) break;
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const DT D = Dof(val(acc[b][bj][2 * h + e]), nr_, nyv[bj][e]);
+            const DT D = Dpr(val(acc[b][bj][2 * h + e]), nr_, nyv[bj][e]);
             bool pr;
             if (U8) pr = (uint32_t)an * (uint32_t)D < (uint32_t)th;
             else pr = (float)an * (float)D < (float)th;
@@ -1285,10 +1120,15 @@ __global__ void __launch_bounds__(2 * CP + 32, CP <= 64 ? 4 : (CP <= 128 ? 2 : 1
     // ================================================================ band warps
     const int g = lane >> 2, t4 = lane & 3;
     const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lcol = (lane >> 4) * 16;
+    // D (order key) and D' (prune test); nrm holds squared norms (L2) or inverse norms (MIPS)
     auto Dof = [](DT gg, DT na_, DT nb_) -> DT {
       if (MIPS) return -gg;
       if (U8) return na_ + nb_ - 2 * gg;
       return fmaxf(na_ + nb_ - 2.0f * gg, 0.0f);
+    };
+    auto Dpr = [&](DT gg, DT na_, DT nb_) -> DT {
+      if (MIPS) return (DT)ang_d((float)gg, (float)na_, (float)nb_);
+      return Dof(gg, na_, nb_);
     };
     auto val = [](int32_t x) -> DT {
       if (U8) return (DT)x;
@@ -1350,7 +1190,7 @@ __global__ void __launch_bounds__(2 * CP + 32, CP <= 64 ? 4 : (CP <= 128 ? 2 : 1
           g0[bj * 8 + 2 * t4 + 1] = val(acc[bj][1]);
         }
       }
-      if (!MIPS) {
+      {
         for (int r = tid; r < nr; r += NB_T) {
           const uint4* rw = reinterpret_cast<const uint4*>(rows + (size_t)r * L.pitch);
           int32_t si = 0;
@@ -1370,22 +1210,22 @@ __global__ void __launch_bounds__(2 * CP + 32, CP <= 64 ? 4 : (CP <= 128 ? 2 : 1
             }
           }
           if (U8) nrm[r] = (DT)si;
-          else nrm[r] = (DT)sf;
+          else nrm[r] = MIPS ? (DT)inv_norm(sf) : (DT)sf;
         }
       }
       named_sync(kBarBand, NB_T);
       // ---- keys (D(u,y), id) and thresholds ad*D(u,y) of the candidates y = 1..c
       for (int y = tid + 1; y <= c; y += NB_T) {
-        const DT ny = MIPS ? (DT)0 : nrm[y];
-        const DT Du = Dof(g0[y], MIPS ? (DT)0 : nrm[0], ny);
+        const DT ny = nrm[y];
+        const DT Du = Dof(g0[y], nrm[0], ny);
         skey[y] = ((uint64_t)(U8 ? (uint32_t)Du : f_ord((float)Du)) << 32) | ids[y];
         if (U8) thr[y] = (DT)((uint32_t)ad * (uint32_t)Du);
-        else thr[y] = (DT)((float)ad * (float)Du);
+        else thr[y] = (DT)((float)ad * (float)Dpr(g0[y], nrm[0], ny));
       }
       named_sync(kBarBand, NB_T);
       // ---- prune bits of rows r0, r1 (Gram indices; candidates are 1..c), OR-reduced over the quad
       if (act) {
-        const DT n0 = (MIPS || r0 > c) ? (DT)0 : nrm[r0], n1 = (MIPS || r1 > c) ? (DT)0 : nrm[r1];
+        const DT n0 = r0 > c ? (DT)0 : nrm[r0], n1 = r1 > c ? (DT)0 : nrm[r1];
         const DT th0 = (r0 >= 1 && r0 <= c) ? thr[r0] : (DT)0, th1 = (r1 >= 1 && r1 <= c) ? thr[r1] : (DT)0;
         uint32_t w0[W], w1[W];
 #pragma unroll
@@ -1397,8 +1237,8 @@ __global__ void __launch_bounds__(2 * CP + 32, CP <= 64 ? 4 : (CP <= 128 ? 2 : 1
             for (int e = 0; e < 2; ++e) {
               const int y = bj * 8 + 2 * t4 + e;
               if (y >= 1 && y <= c) {
-                const DT ny = MIPS ? (DT)0 : nrm[y];
-                const DT D0 = Dof(val(acc[bj][e]), n0, ny), D1 = Dof(val(acc[bj][2 + e]), n1, ny);
+                const DT ny = nrm[y];
+                const DT D0 = Dpr(val(acc[bj][e]), n0, ny), D1 = Dpr(val(acc[bj][2 + e]), n1, ny);
                 bool p0, p1;
                 if (U8) {
                   p0 = (uint32_t)an * (uint32_t)D0 < (uint32_t)th0;
@@ -1605,8 +1445,6 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
     const uint32_t* in_list = order;  // nullptr: points in id order
     const uint32_t* in_n = order_n;
     bool first_tier = true;
-    static const bool band = std::getenv("PIPNN_FP_COOP") == nullptr;  // experiment hook: old cooperative tiers
-    static const bool gram32 = std::getenv("PIPNN_FP_GRAM32") != nullptr;  // experiment hook: old warp tier
 #define GP_TIER(U, M, CPV, T)                                                                                      \
   do {                                                                                                             \
     const GpLayout GL = gp_layout(X->d, U, CPV);                                                                   \
@@ -1621,20 +1459,6 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
                                                p->alpha_den, nbr_tmp, deg, in_list, in_n, defer + (T) * n,        \
                                                defer_n + (T), src_bf16);                                           \
     PIPNN_LAUNCHED("fp_gram_kernel", c.st);                                                                        \
-    in_list = defer + (T) * n;                                                                                     \
-    in_n = defer_n + (T);                                                                                          \
-  } while (0)
-#define GP_COOP(U, M, CPV, T)                                                                                      \
-  do {                                                                                                             \
-    const GpLayout GL = gp_layout(X->d, U, CPV);                                                                   \
-    const int sm = (int)GL.per_warp;                                                                               \
-    auto* fn = fp_coop_kernel<U, M, CPV>;                                                                          \
-    PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));                         \
-    const int per_sm = std::max(1, std::min(2048 / CPV, (int)((227 * 1024) / (sm + 2048))));                       \
-    fn<<<(unsigned)(num_sms() * per_sm), CPV, sm, c.st>>>(Xg->data, n, X->d, Xg->ld, l_max, slots, count, R,       \
-                                                          p->alpha_num, p->alpha_den, nbr_tmp, deg, in_list, in_n,  \
-                                                          defer + (T) * n, defer_n + (T), src_bf16);                \
-    PIPNN_LAUNCHED("fp_coop_kernel", c.st);                                                                        \
     in_list = defer + (T) * n;                                                                                     \
     in_n = defer_n + (T);                                                                                          \
   } while (0)
@@ -1671,11 +1495,11 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
   } while (0)
 #define GP_ALL(U, M)                                                                                               \
   do {                                                                                                             \
-    if (gram32 || (U)) GP_TIER(U, M, 32, 0); else GP_WARP(U, M);                                                   \
-    if (l_max > 31) { if (band) GP_BAND(U, M, 64, 1); else GP_COOP(U, M, 64, 1); }                                 \
-    if (l_max > 63) { if (band) GP_BAND(U, M, 128, 2); else GP_COOP(U, M, 128, 2); }                               \
-    if (l_max > 127 && band && band_layout(X->d, U, 192).bytes <= 200 * 1024) GP_BAND(U, M, 192, 3);             \
-    if (l_max > (band && band_layout(X->d, U, 192).bytes <= 200 * 1024 ? 191 : 127)) {                            \
+    if (U) GP_TIER(true, false, 32, 0); else GP_WARP(U, M);                                                        \
+    if (l_max > 31) GP_BAND(U, M, 64, 1);                                                                          \
+    if (l_max > 63) GP_BAND(U, M, 128, 2);                                                                         \
+    if (l_max > 127 && band_layout(X->d, U, 192).bytes <= 200 * 1024) GP_BAND(U, M, 192, 3);                       \
+    if (l_max > (band_layout(X->d, U, 192).bytes <= 200 * 1024 ? 191 : 127)) {                                     \
       auto* fn = final_prune_kernel<U, M>;                                                                         \
       PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem1));                    \
       fn<<<(unsigned)(num_sms() * 2), 32, smem1, c.st>>>(X->data, n, X->d, X->ld, l_max, slots, count, R,          \
@@ -1699,7 +1523,6 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
                    (long long)(n - hd[0]), hd[0] - hd[1], hd[1] - hd[2], hd[2]);
     }
 #undef GP_ALL
-#undef GP_COOP
 #undef GP_BAND
 #undef GP_WARP
 #undef GP_TIER

@@ -77,8 +77,9 @@ pipnn_status leaf_order(const uint32_t* leaf_ids, int64_t n_inst, int64_t n, uin
 
 // Device carving of whole subtrees below depth 0 (partition_subtree.cu): which subproblems fit, and the launch.
 bool subtree_fits(const pipnn_points* X, const pipnn_partition_params* p, int64_t size, int depth);
-// Pinned host scratch for small device -> host reads (thread-local, grows as needed; callers copy into it
-// with cudaMemcpyAsync, synchronise the stream, then read it — nothing stays pending across calls).
+// Pinned host scratch for small device <-> host transfers (thread-local, grows as needed). Copy kernels read
+// or write it asynchronously; every user synchronises the stream before the call returns (on error paths
+// too: partition_impl), so nothing is pending when the next call reuses it.
 uint8_t* pinned_scratch(size_t bytes);  // mapped pinned host memory, reused per thread (api.cu)
 // Stream-ordered copy by a kernel (device <-> mapped pinned host or device), not by a copy engine (api.cu).
 cudaError_t kcopy(void* dst, const void* src, size_t bytes, cudaStream_t st);

@@ -383,9 +383,25 @@ static size_t partition_cub_bytes(const PartCaps& cp) {
   return bytes;
 }
 
+static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_params* p, int64_t* leaf_off,
+                                   int64_t leaf_off_cap, uint32_t* leaf_ids, int64_t leaf_ids_cap, int64_t* n_leaves_h,
+                                   int64_t* n_inst_h, int* depth_h, Arena& ar, const Ctx& c);
+
+// The level plans are staged in thread-local mapped pinned buffers (g_pin_level, g_pin_jobs, pinned_scratch)
+// that copy kernels read asynchronously; a successful call ends with its caller's synchronisation, and a
+// failing one synchronises here, so no copy is still reading them when the next call resets them.
 pipnn_status partition_impl(const pipnn_points* X, const pipnn_partition_params* p, int64_t* leaf_off,
                             int64_t leaf_off_cap, uint32_t* leaf_ids, int64_t leaf_ids_cap, int64_t* n_leaves_h,
                             int64_t* n_inst_h, int* depth_h, Arena& ar, const Ctx& c) {
+  const pipnn_status s = partition_body(X, p, leaf_off, leaf_off_cap, leaf_ids, leaf_ids_cap, n_leaves_h, n_inst_h,
+                                        depth_h, ar, c);
+  if (s != PIPNN_OK && !ar.measuring()) cudaStreamSynchronize(c.st);
+  return s;
+}
+
+static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_params* p, int64_t* leaf_off,
+                                   int64_t leaf_off_cap, uint32_t* leaf_ids, int64_t leaf_ids_cap, int64_t* n_leaves_h,
+                                   int64_t* n_inst_h, int* depth_h, Arena& ar, const Ctx& c) {
   const PartCaps cp = caps_of(X, p);
   const int Kb = tiled_row_bytes(X);
   int fmax = 1;

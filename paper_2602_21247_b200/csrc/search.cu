@@ -158,9 +158,13 @@ __global__ void __launch_bounds__(32 * kSrchWarps) search_kernel(const void* __r
       }
       __syncwarp();
       const uint64_t r0 = row_ptr[p], r1 = row_ptr[p + 1];
+      // the row in steps of <= 256 neighbours (S.cand's capacity), each merged into the beam before the next
+      // is read: top-L composes, so this equals one merge of the whole row for any out-degree
+      for (uint64_t q0 = r0; q0 < r1; q0 += 256) {
+      const uint64_t q1 = min(r1, q0 + 256);
       int nc = 0;
-      for (uint64_t e0 = r0; e0 < r1; e0 += 32) {
-        const bool valid = e0 + lane < r1;
+      for (uint64_t e0 = q0; e0 < q1; e0 += 32) {
+        const bool valid = e0 + lane < q1;
         const uint32_t v = valid ? col_idx[e0 + lane] : kEmpty;
         bool add = valid;
         if (add) {  // visited?
@@ -269,6 +273,7 @@ __global__ void __launch_bounds__(32 * kSrchWarps) search_kernel(const void* __r
       __syncwarp();
       cur = nxt;
       nb = nt;
+      }
     }
     // answer: the beam's first k (excluding the query's own id for the k-NN-graph task)
     int pself = nb;

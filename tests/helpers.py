@@ -57,3 +57,108 @@ def check_candidate_lists_float(X, metric, leaf_ids, nbr_g, dist_g, nbr_o, dist_
             t = dist_tol(np.array([kth]), nrm[p], nrm[v])[0] * 2
             assert abs(Dv - kth) <= t, f"row {r}: id {v} differs but D={Dv} is not a near-tie of kth={kth}"
     return ndiff, I
+
+
+def prune_dissim(Xq: np.ndarray, a: np.ndarray, b: np.ndarray, metric: str) -> np.ndarray:
+    """The final prune's alpha-test dissimilarity D' in fp64 (R22): D for L2, 1 - cos for MIPS."""
+    if metric != "mips":
+        return exact_dist(Xq, a, b, metric)
+    dot = (Xq[a] * Xq[b]).sum(-1)
+    na, nb = np.sqrt((Xq[a] ** 2).sum(-1)), np.sqrt((Xq[b] ** 2).sum(-1))
+    den = na * nb
+    return np.where(den > 0, 1.0 - dot / np.where(den > 0, den, 1.0), 1.0)
+
+
+def check_prune_lists_float(X, metric, slots, count, rp_g, ci_g, rp_o, ci_o, alpha=(6, 5), rel=1e-4):
+    """Float parity of the final prune: the GPU's admission lists equal the oracle's (same order)
+    for every point except those whose decision chain holds a near-tie: two candidates whose order keys D(u,.)
+    differ by <= rel (relative, plus a cancellation term), or an alpha test an*D'(y,c) vs ad*D'(u,c) whose two
+    sides differ by <= rel. Returns (n_differing, n)."""
+    Xq = bf16_round(X)
+    nrm = (Xq ** 2).sum(1)
+    an, ad = alpha
+    n = len(rp_g) - 1
+    ndiff = 0
+    for u in range(n):
+        g = ci_g[rp_g[u]:rp_g[u + 1]].tolist()
+        o = ci_o[rp_o[u]:rp_o[u + 1]].tolist()
+        if g == o:
+            continue
+        ndiff += 1
+        c = (slots[u, :count[u]] & 0xFFFFFFFF).astype(np.int64)
+        uu = np.full(len(c), u, dtype=np.int64)
+        Du = exact_dist(Xq, uu, c, metric)
+        scale = (nrm[u] + nrm[c]) if metric != "mips" else np.sqrt(nrm[u] * nrm[c])
+        tolD = rel * np.abs(Du) + 1e-6 * scale
+        Ds = np.sort(Du)
+        order_tie = np.any(np.diff(Ds) <= tolD.max())
+        Pu = prune_dissim(Xq, uu, c, metric)
+        ii, jj = np.meshgrid(np.arange(len(c)), np.arange(len(c)), indexing="ij")
+        Pyc = prune_dissim(Xq, c[ii.ravel()], c[jj.ravel()], metric).reshape(len(c), len(c))
+        # cancellation scale of the fp32 Gram-based values: the norms involved (L2), 1 (angular, in [0, 2])
+        S = 1.0 if metric == "mips" else (nrm[c][:, None] + nrm[c][None, :] + nrm[u])
+        lhs, rhs = an * Pyc, ad * Pu[None, :]
+        tol = rel * (np.abs(lhs) + np.abs(rhs)) + 1e-6 * (an + ad) * S
+        alpha_tie = np.any((np.abs(lhs - rhs) <= tol) & (ii != jj))
+        assert order_tie or alpha_tie, f"point {u}: lists differ without a near-tie ({g} vs {o})"
+    return ndiff, n
+
+
+def leaders_of_root(n: int, num: int, den: int, leader_cap: int, seed: int, replica: int = 0) -> np.ndarray:
+    """Depth-0 leaders of Alg. 5 per docs/DETERMINISM.md: the l ids with the smallest (mix(K0, x), x),
+    K0 = mix(mix(seed, DOM_PART), r), l = min(leader_cap, max(2, ceil(num*n/den)), n); ascending ids."""
+    import oracle as O
+
+    DOM_PART = 0x5041525449544E31
+    K0 = O.mix(O.mix(seed, DOM_PART), replica)
+    l = min(leader_cap, max(2, -(-num * n // den)), n)
+    pri = np.array([O.mix(K0, x) for x in range(n)], dtype=np.uint64)
+    order = np.lexsort((np.arange(n), pri))
+    return np.sort(order[:l])
+
+
+def check_single_level_partition_float(X, metric, leaders, fanout, goff, gids, rel=1e-3):
+    """A one-level partition (every depth-0 group <= C_max, no merging): each point's leaves on the GPU are the
+    groups of its f nearest leaders by (D, leader id); where they differ from the exact fp64 (bf16-input)
+    choice, every differing leader lies within tolerance of the f-th/(f+1)-th nearest leader distance
+    (SURVEY §8(c) "leaf assignment"). Returns the number of points whose leader set differs."""
+    Xq = bf16_round(X)
+    nrm = (Xq ** 2).sum(1)
+    n = len(X)
+    Ld = np.stack([exact_dist(Xq, np.arange(n), np.full(n, l), metric) for l in leaders], 1)  # [n, l]
+    ordr = np.lexsort((np.broadcast_to(leaders, Ld.shape), Ld), axis=1)
+    exact_sets = [set(leaders[ordr[i, :fanout]].tolist()) for i in range(n)]
+    # label the GPU leaves with distinct leaders, greedily by overlap with the exact groups (two leaders of one
+    # tight cluster can have identical groups, so labels must be assigned one-to-one)
+    trip = []
+    for b in range(len(goff) - 1):
+        votes = {}
+        for x in gids[goff[b]:goff[b + 1]].tolist():
+            for l in exact_sets[x]:
+                votes[l] = votes.get(l, 0) + 1
+        trip += [(-v, b, l) for l, v in votes.items()]
+    lab_of, used = {}, set()
+    for _, b, l in sorted(trip):
+        if b not in lab_of and l not in used:
+            lab_of[b] = l
+            used.add(l)
+    assert len(lab_of) == len(goff) - 1, "unlabelled leaves"
+    member_of = {}
+    for b in range(len(goff) - 1):
+        for x in gids[goff[b]:goff[b + 1]].tolist():
+            member_of.setdefault(x, set()).add(lab_of[b])
+    ndiff = 0
+    for x in range(n):
+        g = member_of.get(x, set())
+        if g == exact_sets[x]:
+            continue
+        ndiff += 1
+        assert len(g) == fanout, f"point {x} in {len(g)} leaves"
+        row = Ld[x]
+        srt = np.sort(row)
+        kth = srt[fanout - 1]
+        for l in g ^ exact_sets[x]:
+            Dl = row[np.searchsorted(leaders, l)]
+            tol = 2 * (rel * abs(kth) + 1e-6 * (nrm[x] + nrm[l]))
+            assert abs(Dl - kth) <= tol, f"point {x}: leader {l} D={Dl} is not a near-tie of the f-th {kth}"
+    return ndiff

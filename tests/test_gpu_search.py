@@ -98,3 +98,25 @@ def test_knn_graph_task_u8_bit_exact():
                               torch.from_numpy(ref.col_idx.view(np.int32)).cuda(), e, k, L)
     torch.cuda.synchronize()
     assert np.array_equal(ids.cpu().numpy().view(np.uint32), want)
+
+
+@pytest.mark.parametrize("deg", [300, 1000])
+def test_search_high_degree_rows(deg):
+    # rows longer than the kernel's 256-entry candidate buffer are merged in steps of 256 (top-L composes):
+    # identical result lists to the oracle harness for any out-degree (include/pipnn.h). The distance count can
+    # only grow: a neighbour that was in the beam when the row started but was pushed out by an earlier step of
+    # the same row is evaluated again (the harness still holds it in its untruncated beam).
+    cfg = synth.C2.scaled(3000)
+    X = synth.gen_points(cfg)
+    rng = np.random.default_rng(deg)
+    n = len(X)
+    rows = [np.sort(rng.choice(np.delete(np.arange(n), u), size=deg if u % 3 == 0 else 20, replace=False))
+            for u in range(n)]
+    rp = np.concatenate([[0], np.cumsum([len(r) for r in rows])]).astype(np.int64)
+    ci = np.concatenate(rows).astype(np.uint32)
+    Q = synth.gen_queries(cfg, n_queries=100)
+    ds = O.Dataset(X)
+    for L in (16, 64):
+        oids, ocmps = O.beam_search(ds, rp, ci, Q, 0, L, 10)
+        ids, _, cmps = run(X, rp, ci, Q, 0, L, 10, "l2")
+        assert np.array_equal(ids, oids) and ocmps <= cmps <= 1.01 * ocmps

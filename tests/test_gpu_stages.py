@@ -5,7 +5,8 @@ import pytest
 
 import oracle as O
 import synth
-from tests.helpers import UINT32_MAX
+from tests.helpers import (UINT32_MAX, check_prune_lists_float, check_single_level_partition_float,
+                           leaders_of_root)
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -110,9 +111,12 @@ def test_final_prune_float_close(name):
                                      metric=cfg.metric)
     grp = grp.cpu().numpy()
     gci = u32(gci)
-    same = sum(set(ci[rp[u]:rp[u + 1]]) == set(gci[grp[u]:grp[u + 1]]) for u in range(n))
-    assert same >= 0.99 * n, same  # fp32-vs-fp64 alpha tests may flip at exact near-ties only
     assert np.diff(grp).max() <= cfg.R
+    # admission lists (in order) equal the oracle's except at points whose decisions hold a near-tie
+    nd, _ = check_prune_lists_float(X, cfg.metric, slots, count, grp, gci, rp, ci)
+    assert nd <= 0.01 * n, nd
+    if cfg.metric == "mips":  # the angular reading keeps a navigable degree (R22)
+        assert np.diff(grp).mean() >= 8
 
 
 # ---------------------------------------------------------------- a1/a2 partition
@@ -178,4 +182,31 @@ def test_partition_float_invariants_and_overlap(name):
     mult = np.bincount(gids, minlength=len(X))
     assert mult.min() >= 1 and mult.max() <= int(np.prod(cfg.fanout))
     a, b = set(canon(goff, gids)), set(canon(off, ids))
-    assert len(a & b) >= 0.9 * max(len(a), len(b)), (len(a & b), len(a), len(b))  # near-tie assignments only
+    # multi-level: a near-tie at one depth changes a subproblem's size, hence its leaders and every leaf below
+    # it, so leaves are only compared in bulk here; the per-assignment check is the single-level test below
+    assert len(a & b) >= 0.8 * max(len(a), len(b)), (len(a & b), len(a), len(b))
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
+def test_partition_float_single_level_near_ties(name):
+    # one level of Alg. 5 (100 leaders, every group <= C_max = 4096, c_min = 1: no merge, no recursion): every
+    # point's leaves are the groups of its f nearest leaders, except where the f-th and (f+1)-th leader
+    # distances are within the float tolerance
+    cfg = synth.CONFIGS[name]
+    n = 20000 if cfg.n != 10000 else 10000
+    cfg = cfg.scaled(n) if cfg.n != n else cfg
+    X = synth.gen_points(cfg)
+    num, den, c_max = 100, n, 4096
+    p = cfg.params()
+    p.update(c_max=c_max, c_min=1, p_num=num, p_den=den)
+    off, ids, depth = O.partition(O.Dataset(X, metric=cfg.metric, mode="bf16"), p)
+    assert np.diff(off).max() <= c_max and depth <= 1
+    pp = P().partition_params(c_max=c_max, c_min=1, p_samp=(num, den), fanout=cfg.fanout, seed=cfg.seed)
+    goff, gids = P().pipnn_partition(cuda(X), pp, metric=cfg.metric)
+    goff, gids = goff.cpu().numpy(), u32(gids)
+    leaders = leaders_of_root(n, num, den, cfg.leader_cap, cfg.seed)
+    f = cfg.fanout[0]
+    # the oracle itself is the exact choice (sanity of the checker), the GPU differs only at near-ties
+    assert check_single_level_partition_float(X, cfg.metric, leaders, f, off, ids) == 0
+    nd = check_single_level_partition_float(X, cfg.metric, leaders, f, goff, gids)
+    assert nd <= 0.01 * n, nd
