@@ -330,7 +330,7 @@ def main():
     ap.add_argument("--config", default="C5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--ref-sample", type=int, default=100_000)
-    ap.add_argument("--cpu-sample", type=int, default=200_000)
+    ap.add_argument("--cpu-sample", type=int, default=1_000_000)
     ap.add_argument("--no-int8-peak", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--recall-queries", type=int, default=10000)
@@ -540,9 +540,13 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
+        # the evaluation needs memory: keep the graph, release the builder's workspace
+        g_rp, g_ci = out.row_ptr.clone(), out.col_idx.clone()
+        del out, bb, builder
+        torch.cuda.empty_cache()
         if args.recall_queries > 0:
             try:
-                rec, qps, knn = recall_eval(Xd, cfg, out.row_ptr, out.col_idx, args.recall_queries)
+                rec, qps, knn = recall_eval(Xd, cfg, g_rp, g_ci, args.recall_queries)
                 line["recall_at_10"] = rec
                 line["search_qps"] = qps
                 line["knn_graph_task"] = knn
@@ -551,7 +555,7 @@ def main():
                 line["recall_at_10"] = f"failed: {ex}"
         if not args.no_cpu_baseline:
             try:
-                del builder
+                del g_rp, g_ci
                 torch.cuda.empty_cache()
                 line["cpu_baseline"], line["sample_parity"] = cpu_baseline(cfg, args.cpu_sample, dev)
             except Exception as ex:

@@ -6,32 +6,59 @@
 
 namespace pipnn {
 
-template <bool U8, bool MIPS, int KMAX>
+// Experiment hooks, read once per process (environment): PIPNN_DEBUG_EPI (epilogue skips / wait profile),
+// PIPNN_P1 / PIPNN_P1_PART (threshold-pass tiles), PIPNN_GEOM ("NA,planes per chunk").
+struct DtKnobs {
+  int dbg = 0, p1 = 0, p1_part = 0, geo = 0;
+  DtKnobs() {
+    if (const char* e = std::getenv("PIPNN_DEBUG_EPI")) dbg = std::atoi(e);
+    if (const char* e = std::getenv("PIPNN_P1")) p1 = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("PIPNN_P1_PART")) p1_part = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("PIPNN_GEOM")) {
+      int na = 0, pc = 0;
+      if (std::sscanf(e, "%d,%d", &na, &pc) == 2 && na >= 1 && na <= 2 && pc >= 2 && pc <= 14) geo = 16 * na + pc;
+    }
+  }
+};
+static const DtKnobs& knobs() {
+  static const DtKnobs k;
+  return k;
+}
+
+template <bool U8, bool MIPS, int KMAX, bool UF = false>
 static pipnn_status launch_one(const DistTopkArgs& a0, cudaStream_t st) {
   DistTopkArgs a = a0;
-  const char* dbg_env = std::getenv("PIPNN_DEBUG_EPI");  // experiment hook (read per launch)
-  a.dbg = dbg_env ? std::atoi(dbg_env) : 0;
-  // threshold-pass tiles: any column subset gives a valid bound; fewer tiles trade pass-1 work for a few more
-  // pass-2 candidates (measured: 3 tiles for leaves — C2 u8, and C3/C4 float, whose leaf kernel is bound by
-  // the producer/MMA pipeline, so every pass-1 tile costs a B-tile load: C4 leaf tiles 2.70 -> 2.40 ms with 3
-  // instead of all; 2 for the partition's K <= 4)
-  const char* p1_env = std::getenv(KMAX <= 4 ? "PIPNN_P1_PART" : "PIPNN_P1");
-  a.p1cap = p1_env ? std::max(1, std::atoi(p1_env)) : (KMAX <= 4 ? 2 : 3);
+  const DtKnobs& kn = knobs();
+  a.dbg = kn.dbg;
+  // threshold-pass tiles: any column subset gives a valid bound; fewer tiles trade pass-1 work for more pass-2
+  // candidates (measured: 3 tiles for the plain uint8 and float leaves — C3/C4 are bound by the producer/MMA
+  // pipeline, so every pass-1 tile costs a B-tile load; 6 for the folded uint8 leaves, C5 leaf pick 88.8 ->
+  // 86.1 ms vs 3, whose epilogue pays more for pass-2 candidates than for threshold tiles; 2 for the
+  // partition's K <= 4)
+  const int p1_req = KMAX <= 4 ? kn.p1_part : kn.p1;
+  a.p1cap = p1_req ? p1_req : (KMAX <= 4 ? 2 : (UF ? 6 : 3));
+  // folded uint8 leaves: one A slot and a whole tile per ring stage (one copy and one ring commit per tile:
+  // C5 leaf pick 91.8 -> 88.8 ms)
+  a.geo = kn.geo ? kn.geo : (UF && a.Kb / 16 <= 14 ? 16 + a.Kb / 16 : 0);
   if (a.packed && !(KMAX == 2 && U8)) return fail(PIPNN_EUNSUPPORTED, "dist_topk: packed pass needs uint8, K <= 2");
   if (a.packed) a.p1cap = 0;  // no threshold pass
-  const char* geo_env = std::getenv("PIPNN_GEOM");  // experiment hook: "NA,planes per chunk"
-  a.geo = 0;
-  if (geo_env) {
-    int na = 0, pc = 0;
-    if (std::sscanf(geo_env, "%d,%d", &na, &pc) == 2 && na >= 1 && na <= 2 && pc >= 2 && pc <= 14) a.geo = 16 * na + pc;
-  }
-  const DtGeom g = dt_geom(a.Kb, !U8, a.geo);
+  if (UF != (a.uf_aug > 0)) return fail(PIPNN_EUNSUPPORTED, "dist_topk: folded layout mismatch");
+  const DtGeom g = dt_geom(a.Kb, !U8 ? 2 : a.uf_aug, a.geo);
   if (g.stages < 2) return fail(PIPNN_EUNSUPPORTED, "dist_topk: row too long for the SMEM pipeline");
-  auto* fn = dist_topk_kernel<U8, MIPS, KMAX>;
+  auto* fn = dist_topk_kernel<U8, MIPS, KMAX, UF>;
   PIPNN_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, g.smem));
   fn<<<num_sms(), kDtThreads, g.smem, st>>>(a);
   PIPNN_LAUNCHED("dist_topk_kernel", st);
   return PIPNN_OK;
+}
+
+// folded uint8 leaves (DistTopkArgs::uf_aug > 0)
+static pipnn_status launch_uf(const DistTopkArgs& a, int kmax, cudaStream_t st) {
+  if (kmax <= 2) return launch_one<true, false, 2, true>(a, st);
+  if (kmax <= 4) return launch_one<true, false, 4, true>(a, st);
+  if (kmax <= 8) return launch_one<true, false, 8, true>(a, st);
+  if (kmax <= 12) return launch_one<true, false, 12, true>(a, st);
+  return launch_one<true, false, 16, true>(a, st);
 }
 
 template <bool U8, bool MIPS>
@@ -49,6 +76,7 @@ pipnn_status launch_dist_topk(const DistTopkArgs& a, bool u8, bool mips, int kma
     return fail(PIPNN_EUNSUPPORTED, "dist_topk: row bytes must be a multiple of 32 and <= 512");
   if (kmax > kTopkMax) return fail(PIPNN_EUNSUPPORTED, "dist_topk: k too large (<= 16)");
   if (u8 && mips) return fail(PIPNN_EINVAL, "uint8 + MIPS unsupported");
+  if (u8 && a.uf_aug > 0) return launch_uf(a, kmax, st);
   if (u8) return launch_k<true, false>(a, kmax, st);
   if (mips) return launch_k<false, true>(a, kmax, st);
   return launch_k<false, false>(a, kmax, st);

@@ -81,11 +81,20 @@ struct DistTopkArgs {
   int geo;                 // pipeline geometry request: 0 = default (dt_geom), else 16 * NA + planes per chunk
   int packed;              // uint8, K <= 2, no self exclusion (the partition): nb holds 32 ||y||^2 + (pos mod 32)
                            // and every tile goes through one packed pass (no threshold pass)
+  int uf_aug;              // folded uint8 leaves (kernel template UF): augment planes per row (2 per 32-B K-step);
+                           // na = per-position row base ||x||^2 + 2 R_x (int32), nb = parity bits of ||y||^2 (u32
+                           // words, bit p & 31 of word p >> 5); see leaf.cu "folded uint8 rows"
   int dbg;                 // experiment hook (PIPNN_DEBUG_EPI): low bits 1 = epilogue skips all tile processing,
                            // 2 = skips pass 2; bit 64 = wait profile (pipnn_debug_dt_prof)
   int* err;
+  // nullable: dynamic item scheduling — each pipeline's producer claims the next item with an atomicAdd on this
+  // device counter (zeroed before the launch) and hands it to its MMA warp and epilogue warpgroup through an
+  // SMEM ring; nullptr: the static round-robin order (item = CTA + (2 j + pipeline) * grid)
+  unsigned long long* work;
 };
 
+constexpr int kDtItemRing = 8;  // claimed items in flight per pipeline (dynamic scheduling)
+constexpr int kDtCopyLanes = 4;  // producer lanes issuing B-tile copies
 constexpr int kDtMaxStages = 16;                    // B ring stages (both pipelines)
 constexpr int kDtTileN = 128;                       // columns per tile (one TMEM accumulator)
 constexpr int kDtThreads = 384;
@@ -107,10 +116,12 @@ constexpr int kDtSmemBudget = 227 * 1024 - 1024;
 struct DtGeom {
   int KCs, KCm, KCuse, nchunks, ppc, stage_bytes, KCa, NA, stages, smem;
 };
-__host__ __device__ inline DtGeom dt_geom(int Kb, bool fold, int geo = 0) {
+// augp: augment planes at the end of every row (float: 2 = one bf16 K-step; folded uint8: 2 per 32-B K-step), whose
+// A side comes from a constant SMEM tile instead of the A block.
+__host__ __device__ inline DtGeom dt_geom(int Kb, int augp, int geo = 0) {
   DtGeom g;
   g.KCs = Kb / 16;
-  g.KCm = fold ? g.KCs - 2 : g.KCs;
+  g.KCm = g.KCs - augp;
   g.KCuse = g.KCs;
   const int ppc_req = geo & 15, na_req = geo >> 4;
   g.nchunks = ppc_req ? (g.KCuse + ppc_req - 1) / ppc_req
@@ -118,7 +129,7 @@ __host__ __device__ inline DtGeom dt_geom(int Kb, bool fold, int geo = 0) {
   g.ppc = ((g.KCuse + g.nchunks - 1) / g.nchunks + 1) & ~1;
   g.stage_bytes = g.ppc * 2048;
   g.KCa = g.KCm;
-  const int rest = 2 * kDtStgBytes + 2 * kDtQBytes + 4096;
+  const int rest = 2 * kDtStgBytes + 2 * kDtQBytes + (augp > 2 ? augp : 2) * 2048;
   // 2 A slots per warpgroup (the next item's A block loads while the current item runs) when that still
   // leaves room for 4 B stages, else 1
   g.NA = 2 * 2 * g.KCa * 2048 + rest + 4 * g.stage_bytes <= kDtSmemBudget ? 2 : 1;
@@ -180,18 +191,26 @@ __device__ __forceinline__ void topk_drain(KT (&kk)[KMAX], uint16_t (&ii)[KMAX],
 // summed over the grid; read and cleared by pipnn_debug_dt_prof (dist_topk.cu).
 static __device__ unsigned long long g_dt_prof[16];
 
-template <bool U8, bool MIPS, int KMAX>
+// UF (uint8 leaves, L2): the "folded" uint8 rows of leaf.cu — s8 coordinates y - 128 and augment K-steps whose
+// s8 digits against constant A-side weights add E_y = 128 sum(y) - ceil(||y||^2/2) (offset), so the int32
+// accumulator is acc = x.y - ceil(||y||^2/2) + R_x (R_x per row): larger is nearer, no per-element norm term.
+template <bool U8, bool MIPS, int KMAX, bool UF = false>
 __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopkArgs args) {
   using KT = typename std::conditional<U8, int32_t, float>::type;
   constexpr bool kFold = !U8;  // float paths fold the column term into an augmented MMA K-step
+  constexpr bool kAug = kFold || UF;
+  static_assert(!UF || (U8 && !MIPS), "the folded path is uint8 L2");
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t bar_full[2][kDtMaxStages / 2], bar_empty[2][kDtMaxStages / 2];
   __shared__ __align__(8) uint64_t bar_a_full[2][2], bar_a_empty[2][2];  // [warpgroup][slot]
   __shared__ __align__(8) uint64_t bar_acc_full[4], bar_acc_empty[4];
+  __shared__ __align__(8) uint64_t bar_it_full[2][kDtItemRing], bar_it_empty[2][kDtItemRing];
+  __shared__ int64_t item_ring[2][kDtItemRing];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const DtGeom GM = dt_geom(args.Kb, kFold, args.geo);
+  const int augp = kFold ? 2 : (UF ? args.uf_aug : 0);
+  const DtGeom GM = dt_geom(args.Kb, augp, args.geo);
   const int KCs = GM.KCs;                // planes per 128-row block of the tiled buffers (block stride)
   const int KCm = GM.KCm;                // planes of the coordinates themselves
   const int KCu = GM.KCuse;              // planes multiplied per tile (incl. the augment step when folded)
@@ -205,7 +224,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
   uint8_t* ring = sA + 2 * NA * KCa * 2048;  // [2 warpgroups][NS][SB]
   uint8_t* stg_base = ring + GM.stages * SB;
   uint8_t* q_base = stg_base + 2 * kDtStgBytes;
-  uint8_t* sOnes = q_base + 2 * kDtQBytes;  // [2 planes][128 rows][16 B] A-side augment
+  uint8_t* sOnes = q_base + 2 * kDtQBytes;  // [augp planes][128 rows][16 B] A-side augment
 
   if (kFold) {
     // constant A-side augment tile: row = (1, 1, 1, 0, ...) in bf16
@@ -213,6 +232,15 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
       const int plane = e >> 9, w = e & 3;
       reinterpret_cast<uint32_t*>(sOnes)[e] =
           (plane == 0 && w == 0) ? 0x3F803F80u : ((plane == 0 && w == 1) ? 0x00003F80u : 0u);
+    }
+    ptx::fence_proxy_async_smem();
+  }
+  if (UF) {
+    // constant A-side augment rows of the folded uint8 layout: s8 weights 127 for every entry but the last
+    // (weight 1) of the last plane
+    for (int e = threadIdx.x; e < augp * 512; e += blockDim.x) {
+      const bool last = (e >> 9) == augp - 1 && (e & 3) == 3;
+      reinterpret_cast<uint32_t*>(sOnes)[e] = last ? 0x017F7F7Fu : 0x7F7F7F7Fu;
     }
     ptx::fence_proxy_async_smem();
   }
@@ -231,6 +259,11 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
       ptx::mbar_init(&bar_acc_full[b], 1);
       ptx::mbar_init(&bar_acc_empty[b], 4);
     }
+    for (int g = 0; g < 2; ++g)
+      for (int e = 0; e < kDtItemRing; ++e) {
+        ptx::mbar_init(&bar_it_full[g][e], 1);
+        ptx::mbar_init(&bar_it_empty[g][e], 5);  // the MMA warp + the 4 epilogue warps of the pipeline
+      }
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc(&tmem_base_sh, 512);
@@ -240,6 +273,34 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
   const uint32_t tmem = tmem_base_sh;
   const int64_t n_items = *args.n_items;
   const bool prof = (args.dbg & 64) != 0;
+  const bool dyn = args.work != nullptr;
+  // Item sequence of pipeline g: j-th item. Static: CTA + (2 j + g) * grid. Dynamic: claimed by the producer
+  // (claim_item), read by the MMA warp and the epilogue warps (take_item); -1 ends the sequence.
+  auto claim_item = [&](int g, uint32_t j) -> int64_t {  // producer (one lane)
+    if (!dyn) {
+      const int64_t it = (int64_t)blockIdx.x + (2 * (int64_t)j + g) * gridDim.x;
+      return it < n_items ? it : -1;
+    }
+    const int e = (int)(j % kDtItemRing);
+    if (!ptx::mbar_wait_hint(&bar_it_empty[g][e], ((j / kDtItemRing) & 1) ^ 1u, args.err, DERR_WAIT_TIMEOUT, 1000000u))
+      return -1;
+    const int64_t it = (int64_t)atomicAdd(args.work, 1ull);
+    item_ring[g][e] = it < n_items ? it : -1;
+    ptx::mbar_arrive(&bar_it_full[g][e]);  // (release: the ring entry is visible to the waiters)
+    return it < n_items ? it : -1;
+  };
+  auto take_item = [&](int g, uint32_t j, bool arrive) -> int64_t {  // MMA warp / epilogue warps
+    if (!dyn) {
+      const int64_t it = (int64_t)blockIdx.x + (2 * (int64_t)j + g) * gridDim.x;
+      return it < n_items ? it : -1;
+    }
+    const int e = (int)(j % kDtItemRing);
+    if (!ptx::mbar_wait(&bar_it_full[g][e], (j / kDtItemRing) & 1, args.err, DERR_WAIT_TIMEOUT)) return -1;
+    const int64_t it = *(volatile int64_t*)&item_ring[g][e];
+    __syncwarp();
+    if (arrive) ptx::mbar_arrive(&bar_it_empty[g][e]);
+    return it;
+  };
   unsigned long long pw[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   const unsigned long long t_start = clock64();
   // Producer and MMA waits (slots < 8) park in hardware on a try_wait suspend-time hint instead of re-issuing
@@ -258,42 +319,58 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
   // it = blockIdx.x + (2 j + g) * gridDim.x; every item's column tiles are computed twice (pass 1: threshold,
   // pass 2: exact picks).
   if (warp < 2) {
-    // ------------------------------------------------------------ producer of pipeline g (one lane)
+    // ------------------------------------------------------------ producer of pipeline g
+    // Lane 0 claims items and loads A blocks; the B-chunk copies are spread over kDtCopyLanes lanes (ring stage
+    // s belongs to lane s % kDtCopyLanes): one thread's bulk copies complete one after another (~0.3-0.4 us each
+    // on B200, tools/micro/l2_bulk_bw.cu), several lanes overlap them.
     const int g = warp;
-    if (lane == 0) [&]() {
+    [&]() {
       uint32_t sg = 0, ia = 0;
       uint8_t* my_ring = ring + g * NS * SB;
-      for (int64_t it = (int64_t)blockIdx.x + (int64_t)g * gridDim.x; it < n_items; it += 2 * (int64_t)gridDim.x) {
+      for (uint32_t jj = 0;; ++jj) {
+        int64_t it = 0;
+        if (lane == 0) it = claim_item(g, jj);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it < 0) break;
         const WorkItem w = args.items[it];
         const DistSeg S = args.segs[w.seg];
         const int T = (S.b.rows + kDtTileN - 1) / kDtTileN;
+        bool ok = true;
         // the item's A block stays in SMEM for all of its tiles (both passes); block-major tiled layout:
         // 128-row block j of a segment = KC planes x 2 KB, contiguous
         {
           const int slot = (int)(ia % NA);
           const uint32_t ph = (ia / NA) & 1;
           ++ia;
-          if (!PWAIT(0, &bar_a_empty[g][slot], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
-          ptx::mbar_arrive_expect_tx(&bar_a_full[g][slot], (uint32_t)(KCa * 2048));
-          ptx::bulk_g2s(sA + (g * NA + slot) * KCa * 2048, args.Ta + (S.a.pos / 128 + w.rb) * (int64_t)KCs * 2048,
-                        KCa * 2048, &bar_a_full[g][slot]);
+          if (lane == 0) {
+            ok = PWAIT(0, &bar_a_empty[g][slot], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT);
+            if (ok) {
+              ptx::mbar_arrive_expect_tx(&bar_a_full[g][slot], (uint32_t)(KCa * 2048));
+              ptx::bulk_g2s(sA + (g * NA + slot) * KCa * 2048,
+                            args.Ta + (S.a.pos / 128 + w.rb) * (int64_t)KCs * 2048, KCa * 2048, &bar_a_full[g][slot]);
+            }
+          }
         }
         const int p1 = dt_p1(S.k, S.b.rows, S.self, args.p1cap);
         for (int t = 0; t < p1 + T; ++t) {
           const int c0 = (t < p1 ? t : t - p1) * kDtTileN;
           const uint8_t* srcB = args.Tb + (S.b.pos / 128 + c0 / 128) * (int64_t)KCs * 2048;
           for (int ch = 0; ch < nchunks; ++ch, ++sg) {
+            // stage s is always filled by lane s % kDtCopyLanes, so each lane waits on its stages in order
+            // (a parity wait can never be two phases behind)
             const int s = sg % NS;
+            if (s % kDtCopyLanes != lane || !ok) continue;
             const uint32_t ph = (sg / NS) & 1;
-            if (!PWAIT(1, &bar_empty[g][s], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT)) return;
+            ok = PWAIT(1, &bar_empty[g][s], ph ^ 1u, args.err, DERR_WAIT_TIMEOUT);
+            if (!ok) continue;
             const int kc0 = ch * ppc, kc1 = min(KCu, kc0 + ppc);
             ptx::mbar_arrive_expect_tx(&bar_full[g][s], (uint32_t)((kc1 - kc0) * 2048));
-            ptx::bulk_g2s(my_ring + s * SB, srcB + (int64_t)kc0 * 2048, (kc1 - kc0) * 2048,
-                          &bar_full[g][s]);
+            ptx::bulk_g2s(my_ring + s * SB, srcB + (int64_t)kc0 * 2048, (kc1 - kc0) * 2048, &bar_full[g][s]);
           }
         }
+        if (!__all_sync(0xffffffffu, ok)) return;
       }
-      if (prof) {
+      if (prof && lane == 0) {
         atomicAdd(&g_dt_prof[0], pw[0]);
         atomicAdd(&g_dt_prof[1], pw[1]);
         atomicAdd(&g_dt_prof[2], clock64() - t_start);
@@ -309,7 +386,9 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
       uint32_t sg = 0, ia = 0, tc = 0;
       const uint32_t ring_u32 = ptx::smem_u32(ring + g * NS * SB);
       const uint64_t ones_desc = ptx::smem_desc_kmajor_noswz(ptx::smem_u32(sOnes), 2048, 128);
-      for (int64_t it = (int64_t)blockIdx.x + (int64_t)g * gridDim.x; it < n_items; it += 2 * (int64_t)gridDim.x) {
+      for (uint32_t jj = 0;; ++jj) {
+        const int64_t it = take_item(g, jj, lane == 0);
+        if (it < 0) break;
         const unsigned long long ti0 = prof ? clock64() : 0ull;
         const WorkItem w = args.items[it];
         const DistSeg Sg = args.segs[w.seg];
@@ -331,7 +410,9 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
           const unsigned long long w6 = pw[6];
           ptx::tc_fence_after();
           // float: negate B (bit 14), so the accumulator is -x.y + (column term)
-          const uint32_t idesc = U8 ? ptx::idesc_u8_s32(128, Nt) : (ptx::idesc_bf16_f32(128, Nt) | (1u << 14));
+          // folded uint8: A and B signed (s8, bits 7 and 10)
+          const uint32_t idesc = UF ? (ptx::idesc_u8_s32(128, Nt) | (1u << 7) | (1u << 10))
+                                    : (U8 ? ptx::idesc_u8_s32(128, Nt) : (ptx::idesc_bf16_f32(128, Nt) | (1u << 14)));
           const uint32_t dtm = tmem + buf * kDtTileN;
           for (int ch = 0; ch < nchunks; ++ch, ++sg) {
             const int s = sg % NS;
@@ -342,7 +423,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
             const unsigned long long tm0 = prof ? clock64() : 0ull;
             if (ptx::elect_one()) {
               for (int kc = kc0; kc < kc1; kc += 2) {
-                const bool augk = kFold && kc >= KCm;
+                const bool augk = kAug && kc >= KCm;
                 const uint64_t ad = augk ? ones_desc + (uint64_t)((kc - KCm) * 128) : a_desc + (uint64_t)(kc * 128);
                 const uint64_t bd = b_desc + (uint64_t)((kc - kc0) * 128);
                 const uint32_t acc = (ch > 0 || kc > kc0) ? 1u : 0u;
@@ -393,7 +474,9 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
       KT* my_qk = reinterpret_cast<KT*>(q_base + wg * kDtQBytes) + tid;
       uint16_t* my_qc = reinterpret_cast<uint16_t*>(q_base + wg * kDtQBytes + kQCap * 128 * 4) + tid;
       uint32_t tcount = 0;
-      for (int64_t it = (int64_t)blockIdx.x + (int64_t)wg * gridDim.x; it < n_items; it += 2 * (int64_t)gridDim.x) {
+      for (uint32_t jj = 0;; ++jj) {
+        const int64_t it = take_item(wg, jj, lane == 0);
+        if (it < 0) break;
         const WorkItem w = args.items[it];
         const DistSeg S = args.segs[w.seg];
         const int r0 = w.rb * 128;
@@ -434,10 +517,89 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
           const uint32_t taddr = tmem + buf * kDtTileN + ((uint32_t)(q * 32) << 16);
           if (t2 == P1 && P1 > 0) {
             U = vk[VK - 1];
-            if (U8 && U != kInf) U = U + 1;  // key <= U  <=>  key < U + 1
-            if (!U8) U = (KT)nextafterf((float)U, __int_as_float(0x7F800000));
+            if (UF) {
+              // vk holds negated group maxima of acc: -U is the K1-th largest, so acc >= -U passes (key_l <=
+              // -2 (-U) exactly); no bound yet (fewer than K1 groups): everything passes
+              U = U == kInf ? (KT)(1 << 30) : U;
+            } else {
+              if (U8 && U != kInf) U = U + 1;  // key <= U  <=>  key < U + 1
+              if (!U8) U = (KT)nextafterf((float)U, __int_as_float(0x7F800000));
+            }
           }
           if ((args.dbg & 15) == 1 || ((args.dbg & 15) == 2 && pass2)) {
+          } else if (UF && !pass2) {
+            // ---- folded uint8, pass 1: maxima of acc over groups of 16 columns (3-input max), negated into
+            // the value list; padding columns (beyond ncols) never win
+            for (int j0 = 0; j0 < Nt; j0 += 32) {
+              const int valid = min(32, ncols - (c0 + j0));
+              uint32_t v[32];
+              ptx::tmem_ld32(taddr + j0, v);
+              ptx::tmem_ld_wait();
+              if (valid < 32) {
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj)
+                  if (jj >= valid) v[jj] = 0x80000000u;
+              }
+#pragma unroll
+              for (int gq = 0; gq < 2; ++gq) {
+                const int32_t* w = reinterpret_cast<const int32_t*>(v) + 16 * gq;
+                int32_t g = __vimax3_s32(w[0], w[1], w[2]);
+                g = __vimax3_s32(g, w[3], w[4]);
+                g = __vimax3_s32(g, w[5], w[6]);
+                g = __vimax3_s32(g, w[7], w[8]);
+                g = __vimax3_s32(g, w[9], w[10]);
+                g = __vimax3_s32(g, w[11], w[12]);
+                g = __vimax3_s32(g, w[13], w[14]);
+                g = max(g, w[15]);
+                const KT gm = (16 * gq < valid) ? (KT)(-g) : kInf;
+#pragma unroll
+                for (int t = VK - 1; t > 0; --t) vk[t] = max(vk[t - 1], min(vk[t], gm));
+                vk[0] = min(vk[0], gm);
+              }
+            }
+          } else if (UF) {
+            // ---- folded uint8, pass 2: acc >= tau passes, tau = -U until the exact list is full, then
+            // ceil((-kk - 1) / 2) for its K-th key kk (key_l = -2 acc - parity <= kk requires it: conservative,
+            // the drain compares exactly); the funnel collects sign(acc - tau) (one IADD each), inverted per chunk
+            for (int j0 = 0; j0 < Nt; j0 += 32) {
+              const int col0 = c0 + j0;
+              const int valid = min(32, ncols - col0);
+              uint32_t v[32];
+              ptx::tmem_ld32(taddr + j0, v);
+              const int32_t kk8 = (int32_t)kk[KMAX - 1];
+              const int32_t tau = kk8 != (int32_t)kInf ? ((-kk8) >> 1) : -(int32_t)U;
+              ptx::tmem_ld_wait();
+              uint32_t m8[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+              for (int jj = 7; jj >= 0; --jj) {
+#pragma unroll
+                for (int qd = 0; qd < 4; ++qd) {
+                  const int j = 8 * qd + jj;
+                  m8[qd] = __funnelshift_l((uint32_t)((int32_t)v[j] - tau), m8[qd], 1);  // 1: acc < tau
+                }
+              }
+              uint32_t mask = ~(m8[0] | (m8[1] << 8) | (m8[2] << 16) | (m8[3] << 24));
+              if (valid < 32) mask &= (1u << valid) - 1u;
+              if (col0 == diag_chunk) mask &= ~(1u << lane);  // self exclusion (by id: the diagonal element)
+              if (__any_sync(0xffffffffu, mask != 0)) {
+                if (__any_sync(0xffffffffu, qlen + __popc(mask) > kQCap)) topk_drain<KT, KMAX>(kk, ii, qlen, my_qk, my_qc);
+                const uint32_t pbits = reinterpret_cast<const uint32_t*>(args.nb)[(S.b.pos + col0) >> 5];  // parities
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                  *reinterpret_cast<uint4*>(stg + 4 * u) = make_uint4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+                __syncwarp();
+                while (mask) {
+                  const int jj = __ffs(mask) - 1;
+                  mask &= mask - 1;
+                  if (qlen == kQCap) topk_drain<KT, KMAX>(kk, ii, qlen, my_qk, my_qc);
+                  my_qk[qlen * 128] = (KT)(-2 * reinterpret_cast<const int32_t*>(stg)[jj] - (int32_t)((pbits >> jj) & 1u));
+                  my_qc[qlen * 128] = (uint16_t)(col0 + jj);
+                  ++qlen;
+                  if (prof) ++pw[2];
+                }
+                __syncwarp();
+              }
+            }
           } else if (packedm) {
             for (int j0 = 0; j0 < Nt; j0 += 32) {
               const int col0 = c0 + j0;

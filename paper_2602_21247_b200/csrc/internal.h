@@ -33,7 +33,12 @@ pipnn_status validate_points(const pipnn_points* X);
 pipnn_status gather_tiled(const pipnn_points* X, const uint32_t* ids, const TileSeg* segs, const WorkItem* items,
                           const int64_t* n_items, int64_t max_items, uint8_t* T, void* nrm, const Ctx& c,
                           int Kb = 0 /* 0: tiled_row_bytes(X) */,
-                          int packed = 0 /* u8: norms as 32 ||y||^2 + (position mod 32), see DistTopkArgs::packed */);
+                          int packed = 0 /* u8: norms as 32 ||y||^2 + (position mod 32), see DistTopkArgs::packed */,
+                          int augp = 0 /* > 0: folded uint8 rows (leaf.cu) with this many augment planes */,
+                          uint32_t* par = nullptr /* folded rows: parity bit array */);
+// Folded uint8 rows (leaf.cu): augment planes for dimension d, and the row bytes (0 = not available for d).
+int fold_aug_planes(int d);
+int fold_row_bytes(int d);
 
 // Build TileSegs/items for CSR segments (off[0..ns]) with pad = round_up(rows, 128): writes segs
 // (DistSeg with a == b, self = 1, out_row = off[s], k) and the (segment, row-block) items.

@@ -12,6 +12,30 @@ int tiled_row_bytes(const pipnn_points* X) {
   return (int)round_up(X->d, 16) * 2 + 32;  // bf16 coordinates + one augmented K-step (dist_topk.cuh)
 }
 
+// ------------------------------------------------------------------ folded uint8 rows (leaf self-join, L2)
+// For uint8 L2 leaves the row is stored as s8 coordinates b = y - 128 (y ^ 0x80; zero beyond d) followed by
+// augment K-steps of s8 digits g_e(y) that the MMA multiplies with constant A-side weights w_e (127 for every
+// entry but the last, whose weight is 1; dist_topk.cuh UF), so that with A = B = the same rows
+//   acc = sum_i (x_i - 128)(y_i - 128) + sum_e w_e g_e(y)
+//       = x.y - 128 sum(x) - 128 sum(y) + 16384 d + (E_y - OFF),      E_y = 128 sum(y) - ceil(||y||^2 / 2)
+//       = x.y - ceil(||y||^2 / 2) + R_x,                               R_x = 16384 d - 128 sum(x) - OFF.
+// E_y = sum_i y_i (128 - y_i / 2) (+1/2 if ||y||^2 is odd) lies in [0, 8192 d]; OFF = 127 floor(8192 d / 254)
+// centres it. With p_y = ||y||^2 mod 2, the key ||y||^2 - 2 x.y = 2 R_x - (2 acc + p_y): larger acc is nearer,
+// exactly, and D(x, y) = (||x||^2 + 2 R_x) + key_l with key_l = -2 acc - p_y. Every partial sum is an exact
+// integer (|acc| < 2^24). Per position the gather also writes base = ||x||^2 + 2 R_x (int32) and the parity
+// bit p (u32 bit array).
+int fold_aug_planes(int d) {
+  const int F = 8192 * d / 254;
+  for (int st = 1; st <= 8; ++st)
+    if ((32 * st - 1) * 126 >= F + 2) return 2 * st;  // digits stay within [-128, 127]
+  return 0;
+}
+int fold_row_bytes(int d) {
+  const int ap = fold_aug_planes(d);
+  const int kb = (int)round_up(d, 32) + 16 * ap;
+  return (ap > 0 && kb <= 512) ? kb : 0;  // 0: no folded layout (the plain uint8 rows are used)
+}
+
 // ------------------------------------------------------------------ gather
 // One CTA of 4 warps per (segment, 128-row block); lane = row (warp w: rows 32w..32w+31 of the block). Each
 // lane walks its row in 16-B chunks (fp32 -> bf16 RNE for float data; consecutive chunks of a row share L1
@@ -21,14 +45,16 @@ int tiled_row_bytes(const pipnn_points* X) {
 // Float rows end with the 16-element augment K-step of dist_topk.cuh: (t_hi, t_mid, t_lo, 0...) with
 // t = -||y||^2/2 (L2) or 0 (MIPS), split over three bf16 values; padding rows get t = -1e30 (u8 padding
 // rows get the norm kPadNormU8 instead), so padded columns never enter a top-k.
-template <int SRC>  // 0: uint8, 1: float32, 2: bf16 (kDtypeBf16)
+template <int SRC>  // 0: uint8, 1: float32, 2: bf16 (kDtypeBf16), 3: uint8 folded (nrm = base, par = parity bits)
 __global__ void __launch_bounds__(128) gather_tiled_kernel(const void* __restrict__ Xv, int64_t ld, int d, int Kb,
                                                            int mips, const uint32_t* __restrict__ ids,
                                                            const TileSeg* __restrict__ segs,
                                                            const WorkItem* __restrict__ items,
                                                            const int64_t* __restrict__ n_items, uint8_t* __restrict__ T,
-                                                           void* __restrict__ nrm, int* err, int packed) {
-  constexpr bool U8 = SRC == 0;
+                                                           void* __restrict__ nrm, int* err, int packed,
+                                                           int augp, uint32_t* __restrict__ par) {
+  constexpr bool U8 = SRC == 0 || SRC == 3;
+  constexpr bool UF = SRC == 3;
   if ((int64_t)blockIdx.x >= *n_items) return;
   const WorkItem w = items[blockIdx.x];
   const TileSeg S = segs[w.seg];
@@ -36,11 +62,11 @@ __global__ void __launch_bounds__(128) gather_tiled_kernel(const void* __restric
   const int local = w.rb * 128 + r;
   const bool valid = local < S.rows;
   const int KC = Kb >> 4;
-  const int ldm = U8 ? Kb : (Kb - 32) / 2;      // elements of the coordinate part (float: bf16 elements)
-  const int ncc = U8 ? KC : (ldm >> 3);          // 16-B chunks holding coordinates
+  const int ldm = U8 ? Kb - 16 * augp : (Kb - 32) / 2;  // elements of the coordinate part (float: bf16 elements)
+  const int ncc = U8 ? (ldm >> 4) : (ldm >> 3);          // 16-B chunks holding coordinates
   uint8_t* dst = T + (S.pos / 128 + w.rb) * (int64_t)KC * 2048 + r * 16;
   const int64_t id = valid ? (ids ? (int64_t)ids[S.id_off + local] : (S.id_off + local)) : 0;
-  int32_t ni = 0;
+  int32_t ni = 0, sy = 0;
   float nf = 0.0f;
   bool bad = false;
   const bool vec = U8 ? ((d & 15) == 0 && (ld & 15) == 0) : ((d & 3) == 0 && (ld & 3) == 0);
@@ -62,6 +88,21 @@ __global__ void __launch_bounds__(128) gather_tiled_kernel(const void* __restric
         ni = (int32_t)__dp4a(out.y, out.y, (uint32_t)ni);
         ni = (int32_t)__dp4a(out.z, out.z, (uint32_t)ni);
         ni = (int32_t)__dp4a(out.w, out.w, (uint32_t)ni);
+        if (UF) {
+          sy = (int32_t)__dp4a(out.x, 0x01010101u, (uint32_t)sy);
+          sy = (int32_t)__dp4a(out.y, 0x01010101u, (uint32_t)sy);
+          sy = (int32_t)__dp4a(out.z, 0x01010101u, (uint32_t)sy);
+          sy = (int32_t)__dp4a(out.w, 0x01010101u, (uint32_t)sy);
+          // s8 coordinates y - 128 for the bytes inside the row, 0 beyond d
+          const int nb = d - kc * 16;
+          uint32_t xm[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int b = nb - 4 * t;
+            xm[t] = b >= 4 ? 0x80808080u : (b <= 0 ? 0u : (0x80808080u >> (8 * (4 - b))));
+          }
+          out = make_uint4(out.x ^ xm[0], out.y ^ xm[1], out.z ^ xm[2], out.w ^ xm[3]);
+        }
       } else if (SRC == 2) {
         // bf16 rows zero padded to ld (a multiple of 8): 16-B chunks, norm of the bf16 values
         if (kc * 8 < ld) out = __ldg((const uint4*)((const uint16_t*)Xv + id * ld) + kc);
@@ -99,7 +140,36 @@ __global__ void __launch_bounds__(128) gather_tiled_kernel(const void* __restric
     *(uint4*)(dst + (int64_t)kc * 2048) = out;
   }
   if (bad) atomicExch(err, DERR_NONFINITE);
-  if (U8) {
+  if (UF) {
+    // augment digits of E_y - OFF = 127 q + r: q split over the NE - 1 weight-127 entries, r on the weight-1 one
+    const int NE = 16 * augp;
+    const int32_t OFF = 127 * ((8192 * d) / 254);
+    const int32_t E = 128 * sy - ((ni + 1) >> 1);
+    const int32_t aug = E - OFF;
+    const int32_t q = aug >= 0 ? aug / 127 : -((-aug + 126) / 127);  // floor division
+    const int32_t rr = aug - 127 * q;
+    const int32_t bq = q >= 0 ? q / (NE - 1) : -((-q + NE - 2) / (NE - 1));
+    const int32_t rem = q - bq * (NE - 1);  // in [0, NE - 2]: the first rem digits get bq + 1
+    for (int pl = 0; pl < augp; ++pl) {
+      uint32_t wv[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int by = 0; by < 4; ++by) {
+          const int e = pl * 16 + 4 * t + by;
+          const int32_t g = !valid ? 0 : (e == NE - 1 ? rr : bq + (e < rem ? 1 : 0));
+          w |= ((uint32_t)g & 0xFFu) << (8 * by);
+        }
+        wv[t] = w;
+      }
+      *(uint4*)(dst + (int64_t)(ncc + pl) * 2048) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+    }
+    const int32_t Rx = 16384 * d - 128 * sy - OFF;
+    ((int32_t*)nrm)[S.pos + local] = valid ? ni + 2 * Rx : 0;
+    const uint32_t pb = __ballot_sync(0xffffffffu, valid && (ni & 1));
+    if ((threadIdx.x & 31) == 0) par[(S.pos + local) >> 5] = pb;  // rows 32w .. 32w + 31 of the block
+  } else if (U8) {
     // packed (the partition's K <= 2 single pass, dist_topk.cuh): 32 ||y||^2 + (position mod 32)
     ((int32_t*)nrm)[S.pos + local] = valid ? (packed ? 32 * ni + ((S.pos + local) & 31) : ni) : kPadNormU8;
   } else {
@@ -117,14 +187,16 @@ __global__ void __launch_bounds__(128) gather_tiled_kernel(const void* __restric
 
 pipnn_status gather_tiled(const pipnn_points* X, const uint32_t* ids, const TileSeg* segs, const WorkItem* items,
                           const int64_t* n_items, int64_t max_items, uint8_t* T, void* nrm, const Ctx& c, int Kb,
-                          int packed) {
+                          int packed, int augp, uint32_t* par) {
   if (max_items <= 0) return PIPNN_OK;
   if (Kb <= 0) Kb = tiled_row_bytes(X);
   const int64_t ld = X->ld;
 #define GT_LAUNCH(SRC)                                                                                             \
   gather_tiled_kernel<SRC><<<(unsigned)max_items, 128, 0, c.st>>>(X->data, ld, X->d, Kb, X->metric == PIPNN_MIPS,   \
-                                                                  ids, segs, items, n_items, T, nrm, c.err, packed)
-  if (X->dtype == PIPNN_U8) GT_LAUNCH(0);
+                                                                  ids, segs, items, n_items, T, nrm, c.err, packed, \
+                                                                  augp, par)
+  if (X->dtype == PIPNN_U8 && augp > 0) GT_LAUNCH(3);
+  else if (X->dtype == PIPNN_U8) GT_LAUNCH(0);
   else if (X->dtype == kDtypeBf16) GT_LAUNCH(2);
   else GT_LAUNCH(1);
 #undef GT_LAUNCH
@@ -196,15 +268,20 @@ int64_t leaf_items_bound(int64_t n_leaves, int64_t n_inst) { return n_inst / 128
 pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, const uint32_t* leaf_ids, int64_t n_leaves,
                             int64_t n_inst, int k, uint32_t* nbr, float* dist, Arena& ar, const Ctx& c,
                             int64_t max_items, uint16_t* cols) {
-  const int Kb = tiled_row_bytes(X);
+  // uint8 L2 leaves: the folded rows (exact int8 MMA that yields the ranking key directly); others: tiled rows
+  const bool fold = X->dtype == PIPNN_U8 && X->metric == PIPNN_L2 && fold_row_bytes(X->d) > 0;
+  const int Kb = fold ? fold_row_bytes(X->d) : tiled_row_bytes(X);
+  const int augp = fold ? fold_aug_planes(X->d) : 0;
   if (max_items <= 0) max_items = leaf_items_bound(n_leaves, n_inst);
   const int64_t seg_cap = std::min<int64_t>(n_leaves, max_items);
   const int64_t max_rows = max_items * 128;
   uint8_t* T = ar.take<uint8_t>((size_t)max_rows * Kb);
   void* nrm = ar.take<int32_t>(max_rows);
+  uint32_t* par = fold ? ar.take<uint32_t>(max_rows / 32 + 1) : nullptr;
   DistSeg* segs = ar.take<DistSeg>(seg_cap);
   WorkItem* items = ar.take<WorkItem>(max_items);
   int64_t* n_items = ar.take<int64_t>(1);
+  unsigned long long* work = ar.take<unsigned long long>(1);  // dynamic item counter of the distance kernel
   TileSeg* tsegs = ar.take<TileSeg>(seg_cap);  // compact TileSeg view (seg.a) for the gather kernel
   PIPNN_TRY(csr_dist_segs(leaf_off, seg_cap, k, 1, segs, items, n_items, ar, c));
   if (ar.measuring()) return PIPNN_OK;
@@ -212,12 +289,15 @@ pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, cons
   if (n_leaves == 0 || n_inst == 0) return PIPNN_OK;
   tileseg_view_kernel<<<(unsigned)ceil_div(n_leaves, 256), 256, 0, c.st>>>(segs, n_leaves, tsegs);
   PIPNN_LAUNCHED("tileseg_view_kernel", c.st);
-  PIPNN_TRY(gather_tiled(X, leaf_ids, tsegs, items, n_items, max_items, T, nrm, c, Kb));
+  PIPNN_TRY(gather_tiled(X, leaf_ids, tsegs, items, n_items, max_items, T, nrm, c, Kb, 0, augp, par));
   DistTopkArgs a{};
   a.Ta = T;
   a.Tb = T;
   a.na = nrm;
-  a.nb = nrm;
+  a.nb = fold ? (const void*)par : nrm;
+  a.uf_aug = augp;
+  a.work = work;
+  PIPNN_CUDA(kmemset(work, 0, sizeof(unsigned long long), c.st));
   a.Kb = Kb;
   a.segs = segs;
   a.items = items;

@@ -462,13 +462,13 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
   init_ctr_kernel<<<1, 32, 0, st>>>(dev_ctr, (unsigned long long)cp.L, dev_work + 1);
   PIPNN_LAUNCHED("init_ctr_kernel", st);
   // subproblems below depth 0 that one CTA can carve completely go to the device subtree kernel
-  const bool use_subtree = [] {
+  static const bool use_subtree = [] {
     const char* e = std::getenv("PIPNN_NO_SUBTREE");
     return !(e && e[0] == '1');
   }();
   // from depth 1 on, one CTA carves a whole subtree (no host round trip per depth); C2: 3.01 vs 3.11 ms,
   // C3: 1.82 vs 3.34 ms partition (B200). PIPNN_SUBTREE_DEPTH moves the first device depth (experiments).
-  const int subtree_min_depth = [] {
+  static const int subtree_min_depth = [] {
     const char* e = std::getenv("PIPNN_SUBTREE_DEPTH");
     return e ? std::max(1, std::atoi(e)) : 1;
   }();
