@@ -405,7 +405,8 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   // order, so the candidate rows of consecutive points overlap (L2 reuse); uint8 rows fit L2 at C2 and
   // id order measured slightly faster there.
   // uint8 rows: id order (measured: leaf order made C5's final prune slower, 126 -> 135 ms, and C2's too)
-  const bool by_leaf = is_float;
+  static const bool u8_leaf_order = std::getenv("PIPNN_U8_LEAF_ORDER") != nullptr;  // experiment hook
+  const bool by_leaf = is_float || u8_leaf_order;
   uint32_t* order = by_leaf ? ar.take<uint32_t>(X->n) : nullptr;
   uint32_t* order_n = by_leaf ? ar.take<uint32_t>(1) : nullptr;
   if (by_leaf) {

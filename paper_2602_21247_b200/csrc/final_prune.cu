@@ -1445,6 +1445,7 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
     const uint32_t* in_list = order;  // nullptr: points in id order
     const uint32_t* in_n = order_n;
     bool first_tier = true;
+    static const bool warp_u8 = std::getenv("PIPNN_FP_WARP_U8") != nullptr;  // experiment hook, read once
 #define GP_TIER(U, M, CPV, T)                                                                                      \
   do {                                                                                                             \
     const GpLayout GL = gp_layout(X->d, U, CPV);                                                                   \
@@ -1495,7 +1496,7 @@ pipnn_status final_prune_impl(const pipnn_points* X, int l_max, const uint64_t* 
   } while (0)
 #define GP_ALL(U, M)                                                                                               \
   do {                                                                                                             \
-    if (U) GP_TIER(true, false, 32, 0); else GP_WARP(U, M);                                                        \
+    if (U && !warp_u8) GP_TIER(true, false, 32, 0); else GP_WARP(U, M);                                            \
     if (l_max > 31) GP_BAND(U, M, 64, 1);                                                                          \
     if (l_max > 63) GP_BAND(U, M, 128, 2);                                                                         \
     if (l_max > 127 && band_layout(X->d, U, 192).bytes <= 200 * 1024) GP_BAND(U, M, 192, 3);                       \

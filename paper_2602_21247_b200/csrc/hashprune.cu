@@ -226,8 +226,8 @@ __device__ __forceinline__ int32_t bitcast_st<int32_t>(int x) { return x; }
 template <>
 __device__ __forceinline__ float bitcast_st<float>(int x) { return __int_as_float(x); }
 
-template <typename ST>
-__global__ void __launch_bounds__(256) hp_emit_kernel(const int64_t* __restrict__ leaf_off, const uint32_t* __restrict__ leaf_ids,
+template <typename ST, int NT>
+__global__ void __launch_bounds__(NT) hp_emit_kernel(const int64_t* __restrict__ leaf_off, const uint32_t* __restrict__ leaf_ids,
                                                       int k, const uint16_t* __restrict__ cols,
                                                       const float* __restrict__ dist, const ST* __restrict__ S, int m,
                                                       int stage_sk, uint64_t* __restrict__ fwd, uint64_t* __restrict__ rev,
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(256) hp_emit_kernel(const int64_t* __restrict_
                                                       int64_t* __restrict__ n_edges) {
   extern __shared__ __align__(16) uint8_t esm[];
   __shared__ uint32_t tot_sh;
-  __shared__ uint32_t part[256];
+  __shared__ uint32_t part[NT];
   const int64_t b = blockIdx.x;
   const int64_t o0 = leaf_off[b];
   const int s = (int)(leaf_off[b + 1] - o0);
@@ -853,22 +853,26 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
   if (P >= ((int64_t)1 << 32)) return fail(PIPNN_EUNSUPPORTED, "hashprune: more than 2^32 picks in one wave");
   PIPNN_CUDA(kmemset(n_edges_dev, 0, sizeof(int64_t), c.st));
   if (n_inst == 0 || n_leaves == 0) return PIPNN_OK;
-  // (1) leaf-local emission of both edge directions
+  // (1) leaf-local emission of both edge directions; members' sketches staged in SMEM (C5's 2048-member leaves:
+  // 106 KB of sketches, so a CTA of 1024 threads per leaf there instead of 256)
   max_leaf = std::max(1, std::min(max_leaf, 4096));
   const size_t sk_bytes = (size_t)max_leaf * (m | 1) * 4;
-  const int stage_sk = sk_bytes <= 96 * 1024 ? 1 : 0;
+  const int stage_sk = (size_t)max_leaf * 14 + sk_bytes <= 200 * 1024 ? 1 : 0;
   const int smem = (int)((size_t)max_leaf * 14 + (stage_sk ? sk_bytes : 0));
+  const bool big = max_leaf > 1024;
+#define HP_EMIT(ST, NTH)                                                                                          \
+  do {                                                                                                            \
+    PIPNN_CUDA(cudaFuncSetAttribute(hp_emit_kernel<ST, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
+    hp_emit_kernel<ST, NTH><<<(unsigned)n_leaves, NTH, smem, c.st>>>(leaf_off, leaf_ids, k, cols, dist,           \
+                                                                   (const ST*)sketch, m, stage_sk, fwd, rev,       \
+                                                                   rev_start, rev_cnt, n_edges_dev);              \
+  } while (0)
   if (sk_int) {
-    PIPNN_CUDA(cudaFuncSetAttribute(hp_emit_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    hp_emit_kernel<int32_t><<<(unsigned)n_leaves, 256, smem, c.st>>>(leaf_off, leaf_ids, k, cols, dist,
-                                                                      (const int32_t*)sketch, m, stage_sk, fwd, rev,
-                                                                      rev_start, rev_cnt, n_edges_dev);
+    if (big) HP_EMIT(int32_t, 1024); else HP_EMIT(int32_t, 256);
   } else {
-    PIPNN_CUDA(cudaFuncSetAttribute(hp_emit_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    hp_emit_kernel<float><<<(unsigned)n_leaves, 256, smem, c.st>>>(leaf_off, leaf_ids, k, cols, dist,
-                                                                    (const float*)sketch, m, stage_sk, fwd, rev,
-                                                                    rev_start, rev_cnt, n_edges_dev);
+    if (big) HP_EMIT(float, 1024); else HP_EMIT(float, 256);
   }
+#undef HP_EMIT
   PIPNN_LAUNCHED("hp_emit_kernel", c.st);
   // (2) point -> instances
   PIPNN_CUDA(kmemset(g.cnt, 0, (n + 1) * sizeof(uint32_t), c.st));
@@ -881,6 +885,8 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
   // (3) merge per owner (register path), deferred owners through the generic chunked path
   PIPNN_CUDA(kmemset(defer_n, 0, sizeof(uint32_t), c.st));
   const int64_t blocks = std::min<int64_t>(ceil_div(n, 8), (int64_t)num_sms() * 32);
+  // (measured: the sort-free set merge below, match_any / SMEM-table buckets, was slower than the register
+  // bitonic merge: C5 44.0 vs 31.9 ms, C2 0.90 vs 0.55 ms — the merge is bound by its dependent gathers)
   hp_merge_inst_kernel<<<(unsigned)blocks, 256, 0, c.st>>>(n, l_max, k, g.start, inv, fwd, rev, rev_start, rev_cnt,
                                                                slots, count, defer, defer_n);
   PIPNN_LAUNCHED("hp_merge_inst_kernel", c.st);
