@@ -322,6 +322,86 @@ def recall_eval(Xd, cfg, row_ptr, col_idx, n_queries, knn_queries=1_000_000):
     return recall, qps, {"k": 10, "queried_points": nk, "L_sweep": sweep, "first_L_recall_ge_0.95": first}
 
 
+def run_sharded(args, cfg):
+    """--shard: ONE build of the workload sharded over the N ranks (paper_2602_21247_b200.sharded): rank 0
+    partitions and broadcasts the LeafSet, each rank picks in its leaf range, one all_to_all routes the edges to the
+    owners' ranks, each rank runs HashPrune + the final prune of its owners. value = n / max-over-ranks step time
+    (strong scaling: the total work is fixed). e2e: each rank copies X in (pinned) and its CSR rows out."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2602_21247_b200 as P
+    from paper_2602_21247_b200 import sharded as SH
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % (29500 + os.getpid() % 1000), rank=0,
+                                world_size=1)
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+    X = synth.gen_points(cfg)  # every rank holds the same X (replicated, §8(e))
+    Xh = torch.from_numpy(X).pin_memory()
+    Xd = Xh.to(dev)
+    params = P.build_params_from(cfg.params())
+
+    def step():
+        return SH.sharded_build(Xd, params, cfg.metric) if ws > 1 else SH.virtual_sharded_build(Xd, params, 1,
+                                                                                                  cfg.metric)[0]
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = P.pipnn_launch_count()
+    times = []
+    with ClockSampler(dev.index) as clk:
+        for _ in range(args.steps):
+            if ws > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = step()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    launches = P.pipnn_launch_count() - launches0
+    ms = statistics.mean(times)
+    ms_max = rank_max(ms, ws, dev)
+    rows_h = torch.empty(out.row_ptr.numel(), dtype=torch.int64).pin_memory()
+    cols_h = torch.empty(max(1, out.col_idx.numel()), dtype=torch.int32).pin_memory()
+    e2e = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        Xd.copy_(Xh, non_blocking=True)
+        o = step()
+        rows_h.copy_(o.row_ptr, non_blocking=True)
+        cols_h[: o.col_idx.numel()].copy_(o.col_idx, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        e2e.append(e0.elapsed_time(e1))
+    e2e_max = rank_max(statistics.mean(e2e), ws, dev)
+    edges = torch.tensor([float(out.col_idx.numel())], device=dev)
+    if ws > 1:
+        dist.all_reduce(edges)
+    if rank == 0:
+        line = {"metric": METRIC, "value": cfg.n / (ms_max / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "u8" if cfg.dtype == "u8" else "bf16", "data": "synthetic",
+                "config": {**workload_desc(cfg), "parallelism": f"sharded x{ws}: leaf ranges + owner ranges, one "
+                                                                f"all_to_all of edges (SURVEY 8(e))"},
+                "e2e": {"value": cfg.n / (e2e_max / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(X.nbytes),
+                        "d2h_bytes_per_step": int(rows_h.numel() * 8 + out.col_idx.numel() * 4),
+                        "mode": "serial per rank: X H2D, sharded build, own CSR rows D2H"},
+                "gpu_launches": int(launches), "graph_edges": int(edges.item()), "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -334,10 +414,15 @@ def main():
     ap.add_argument("--no-int8-peak", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--recall-queries", type=int, default=10000)
+    ap.add_argument("--shard", action="store_true",
+                    help="one build sharded over the ranks (SURVEY §8(e), NEXT-4; strong scaling) instead of replicas")
     args = ap.parse_args()
     cfg = synth.CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)
+        return
+    if args.shard:
+        run_sharded(args, cfg)
         return
 
     import torch
