@@ -414,6 +414,8 @@ def main():
     ap.add_argument("--no-int8-peak", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--recall-queries", type=int, default=10000)
+    ap.add_argument("--quant", action="store_true",
+                    help="NEXT-2: float L2 leaves picked by per-leaf int8-quantised distances, re-ranked exactly")
     ap.add_argument("--shard", action="store_true",
                     help="one build sharded over the ranks (SURVEY §8(e), NEXT-4; strong scaling) instead of replicas")
     args = ap.parse_args()
@@ -440,7 +442,9 @@ def main():
     X = synth.gen_points(cfg, seed=rank)  # each rank: an independent replica of the workload
     Xh = torch.from_numpy(X).pin_memory()
     Xd = Xh.to(dev)
-    params = P.build_params_from(cfg.params())
+    pd = cfg.params()
+    pd["quant"] = 1 if args.quant else 0
+    params = P.build_params_from(pd)
     builder = P.Builder(Xd, params, metric=cfg.metric)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream()
@@ -609,7 +613,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u8" if cfg.dtype == "u8" else "bf16", "data": "synthetic",
             "config": {**workload_desc(cfg), "parallelism": f"replicas x{ws} (independent builds)",
-                       "l2": "flushed between timed steps (512 MB write)"},
+                       "l2": "flushed between timed steps (512 MB write)",
+                       "leaf_pick": "int8-quantised + exact re-rank (NEXT-2)" if args.quant else "exact"},
             "roofline": {"bound": "tensor", "kernel": "dist_topk_kernel (leaf distance tiles + fused pick)",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s" if cfg.dtype != "u8" else "TOP/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_note,

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define PIPNN_ABI_VERSION 1
+#define PIPNN_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define PIPNN_API __attribute__((visibility("default")))
@@ -76,9 +76,15 @@ typedef struct {
   uint64_t seed;
 } pipnn_partition_params;
 
-/* Leaf pick: bidirected k-NN inside every leaf. 1 <= k <= 15. */
+/* Leaf pick: bidirected k-NN inside every leaf. 1 <= k <= 15.
+ * quant ("quantized GEMM operations"): 0 = the exact path (uint8: exact int8 MMA; float:
+ * bf16 MMA). 1 = float L2 data only: every leaf is scalar-quantised (per-leaf centre and one scale, int8 codes), the
+ * int8 tensor-core kernel keeps the min(16, k + 8) nearest by the quantised distance and they are re-ranked with
+ * the exact bf16-input distances (the k nearest by (D, id) among them are returned). uint8 data ignores it;
+ * float MIPS with quant = 1 is PIPNN_EUNSUPPORTED. */
 typedef struct {
   int32_t k;
+  int32_t quant;
 } pipnn_pick_params;
 
 /* HashPrune (Alg. 3): m hash bits (1..16, default 12 per P:636), l_max reservoir slots

@@ -48,7 +48,7 @@ class PartitionParams(C.Structure):
 
 
 class PickParams(C.Structure):
-    _fields_ = [("k", C.c_int32)]
+    _fields_ = [("k", C.c_int32), ("quant", C.c_int32)]
 
 
 class HashPruneParams(C.Structure):
@@ -163,10 +163,11 @@ def partition_params(c_max=1024, c_min=100, p_samp=None, leader_cap=1000, fanout
 
 
 def build_params(c_max=1024, c_min=100, p_samp=None, leader_cap=1000, fanout=(2,), replicas=1, k=8, m=12, l_max=128,
-                 R=64, alpha=(6, 5), final_prune=1, seed=0x5EED) -> BuildParams:
+                 R=64, alpha=(6, 5), final_prune=1, seed=0x5EED, quant=0) -> BuildParams:
     bp = BuildParams()
     bp.part = partition_params(c_max, c_min, p_samp, leader_cap, fanout, replicas, seed)
     bp.pick.k = k
+    bp.pick.quant = quant
     bp.hp.m, bp.hp.l_max, bp.hp.seed = m, l_max, seed
     bp.prune.R, bp.prune.alpha_num, bp.prune.alpha_den, bp.prune.final_prune = R, alpha[0], alpha[1], final_prune
     return bp
@@ -177,7 +178,7 @@ def build_params_from(p: dict) -> BuildParams:
     return build_params(c_max=p["c_max"], c_min=p["c_min"], p_samp=(p["p_num"], p["p_den"]),
                         leader_cap=p["leader_cap"], fanout=p["fanout"], replicas=p["replicas"], k=p["k"], m=p["m"],
                         l_max=p["l_max"], R=p["R"], alpha=(p["alpha_num"], p["alpha_den"]),
-                        final_prune=p["final_prune"], seed=p["seed"])
+                        final_prune=p["final_prune"], seed=p["seed"], quant=p.get("quant", 0))
 
 
 def _workspace(call, device) -> torch.Tensor:
@@ -224,14 +225,14 @@ def pipnn_partition(X: torch.Tensor, params: PartitionParams, metric="l2", strea
 
 
 def pipnn_leaf_pick(X: torch.Tensor, leaf_off: torch.Tensor, leaf_ids: torch.Tensor, k: int, metric="l2",
-                    stream=None, check=True):
+                    stream=None, check=True, quant=0):
     """Leaf building -> (nbr int32[I, k] (uint32 ids, -1 = none), dist float32[I, k])."""
     pts = points(X, metric)
     nl = leaf_off.numel() - 1
     I = leaf_ids.numel()
     nbr = torch.empty((I, k), dtype=torch.int32, device=X.device)
     dist = torch.empty((I, k), dtype=torch.float32, device=X.device)
-    pp = PickParams(k)
+    pp = PickParams(k, quant)
     st = _stream(stream)
 
     def call(ws, nbytes):

@@ -359,7 +359,8 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   const int64_t budget = std::min<int64_t>(bp.leaf_ids_cap / 64 + 1024, (int64_t)1 << 16);
   int max_leaf_h = p->part.c_max;
   if (ar.measuring()) {
-    s = leaf_pick_impl(XS, nullptr, nullptr, budget, budget * 128, k, nullptr, dist, ar, c, budget, cols);
+    s = leaf_pick_impl(XS, nullptr, nullptr, budget, budget * 128, k, nullptr, dist, ar, c, budget, cols,
+                       p->pick.quant);
     if (s != PIPNN_OK) { cleanup(); return s; }
   } else if (n_leaves > 0) {
     std::vector<int64_t> off(n_leaves + 1);
@@ -383,7 +384,8 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
         ++b1;
       }
       if (b1 == b0) { cleanup(); return fail(PIPNN_EUNSUPPORTED, "leaf larger than the wave budget"); }
-      s = leaf_pick_impl(XS, leaf_off + b0, leaf_ids, b1 - b0, off[b1] - off[b0], k, nullptr, dist, ar, c, budget, cols);
+      s = leaf_pick_impl(XS, leaf_off + b0, leaf_ids, b1 - b0, off[b1] - off[b0], k, nullptr, dist, ar, c, budget, cols,
+                         p->pick.quant);
       if (s != PIPNN_OK) { cleanup(); return s; }
       ar.release(mark);
       b0 = b1;
@@ -480,6 +482,9 @@ pipnn_status pipnn_workspace_size(const pipnn_points* X, const pipnn_build_param
   PIPNN_TRY(validate_hp(&p->hp));
   PIPNN_TRY(validate_prune(&p->prune));
   if (p->pick.k < 1 || p->pick.k > 15) return fail(PIPNN_EINVAL, "k must be in [1, 15]");
+  if (p->pick.quant < 0 || p->pick.quant > 1) return fail(PIPNN_EINVAL, "pick.quant must be 0 or 1");
+  if (p->pick.quant && X->dtype == PIPNN_F32 && X->metric == PIPNN_MIPS)
+    return fail(PIPNN_EUNSUPPORTED, "quantised leaf pick: float L2 only");
   Arena ar;  // measuring
   PIPNN_TRY(build_impl(X, p, ar, nullptr, nullptr, nullptr, nullptr, nullptr));
   *bytes_h = ar.peak + 4096;
@@ -527,18 +532,21 @@ pipnn_status pipnn_leaf_pick(const pipnn_points* X, const int64_t* leaf_off, con
                              float* dist, void* ws, size_t ws_bytes, void* stream) {
   PIPNN_TRY(validate_points(X));
   if (!p || p->k < 1 || p->k > 15) return fail(PIPNN_EINVAL, "k must be in [1, 15]");
+  if (p->quant < 0 || p->quant > 1) return fail(PIPNN_EINVAL, "quant must be 0 or 1");
   if (n_leaves < 0 || n_instances < 0) return fail(PIPNN_EINVAL, "negative sizes");
   if (n_leaves > 0 && (!leaf_off || !leaf_ids || !nbr)) return fail(PIPNN_EINVAL, "NULL argument");
   cudaStream_t st = (cudaStream_t)stream;
   Arena m;
   m.take<int>(64);
-  PIPNN_TRY(leaf_pick_impl(X, leaf_off, leaf_ids, n_leaves, n_instances, p->k, nbr, dist, m, Ctx{st, nullptr}));
+  PIPNN_TRY(leaf_pick_impl(X, leaf_off, leaf_ids, n_leaves, n_instances, p->k, nbr, dist, m, Ctx{st, nullptr}, 0,
+                           nullptr, p->quant));
   PIPNN_TRY(check_ws(ws, ws_bytes, m.peak));
   PIPNN_TRY(pending_cuda());
   Arena ar(ws, ws_bytes);
   int* err = err_slot(ar);
   PIPNN_CUDA(kmemset(err, 0, 256, st));
-  return leaf_pick_impl(X, leaf_off, leaf_ids, n_leaves, n_instances, p->k, nbr, dist, ar, Ctx{st, err});
+  return leaf_pick_impl(X, leaf_off, leaf_ids, n_leaves, n_instances, p->k, nbr, dist, ar, Ctx{st, err}, 0, nullptr,
+                        p->quant);
 }
 
 pipnn_status pipnn_sketch(const pipnn_points* X, const pipnn_hashprune_params* p, void* sketch, void* ws,

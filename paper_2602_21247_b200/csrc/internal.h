@@ -35,7 +35,8 @@ pipnn_status gather_tiled(const pipnn_points* X, const uint32_t* ids, const Tile
                           int Kb = 0 /* 0: tiled_row_bytes(X) */,
                           int packed = 0 /* u8: norms as 32 ||y||^2 + (position mod 32), see DistTopkArgs::packed */,
                           int augp = 0 /* > 0: folded uint8 rows (leaf.cu) with this many augment planes */,
-                          uint32_t* par = nullptr /* folded rows: parity bit array */);
+                          uint32_t* par = nullptr /* folded rows: parity bit array */,
+                          const float* qstats = nullptr /* NEXT-2: per-segment (centre[d], 1/scale) of bf16 rows X */);
 // Folded uint8 rows (leaf.cu): augment planes for dimension d, and the row bytes (0 = not available for d).
 int fold_aug_planes(int d);
 int fold_row_bytes(int d);
@@ -43,14 +44,15 @@ int fold_row_bytes(int d);
 // Build TileSegs/items for CSR segments (off[0..ns]) with pad = round_up(rows, 128): writes segs
 // (DistSeg with a == b, self = 1, out_row = off[s], k) and the (segment, row-block) items.
 pipnn_status csr_dist_segs(const int64_t* off, int64_t ns, int k, int self, DistSeg* segs, WorkItem* items,
-                           int64_t* n_items, Arena& ar, const Ctx& c);
+                           int64_t* n_items, Arena& ar, const Ctx& c, int rebase = 0 /* out_off relative to off[0] */);
 
 // max_items: capacity in 128-row work items (0 = exact bound for these leaves); with an explicit capacity
 // the caller guarantees sum_b ceil(|b|/128) <= max_items (pipnn_build forms waves of leaves that fit).
 int64_t leaf_items_bound(int64_t n_leaves, int64_t n_inst);
+// quant (NEXT-2, float L2): pick by per-leaf scalar-quantised int8 distances, then re-rank exactly (leaf.cu)
 pipnn_status leaf_pick_impl(const pipnn_points* X, const int64_t* leaf_off, const uint32_t* leaf_ids, int64_t n_leaves,
                             int64_t n_inst, int k, uint32_t* nbr, float* dist, Arena& ar, const Ctx& c,
-                            int64_t max_items = 0, uint16_t* cols = nullptr);
+                            int64_t max_items = 0, uint16_t* cols = nullptr, int quant = 0);
 
 // fp32 -> bf16 copy of float points (kDtypeBf16 rows of ldb = round_up(d, 8) elements).
 pipnn_status to_bf16(const pipnn_points* X, uint16_t* Xb, int ldb, const Ctx& c);

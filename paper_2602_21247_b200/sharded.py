@@ -123,7 +123,7 @@ def shard_edges(X: torch.Tensor, params: BuildParams, leaf_off: torch.Tensor, le
         return e, e, torch.empty(0, dtype=torch.float32, device=X.device), {"leaves": 0, "instances": 0}
     my_off = (leaf_off[b0:b1 + 1] - i0).contiguous()
     my_ids = leaf_ids[i0:i1]
-    nbr, dist = pipnn_leaf_pick(X, my_off, my_ids, params.pick.k, metric)
+    nbr, dist = pipnn_leaf_pick(X, my_off, my_ids, params.pick.k, metric, quant=params.pick.quant)
     owner, cand, d = bidirected_edges(my_ids, nbr, dist)
     return owner, cand, d, {"leaves": b1 - b0, "instances": i1 - i0}
 
