@@ -801,7 +801,8 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
               if (MIPS) D = (float)key;
               else if (U8) D = (float)(na + key);
               else D = fmaxf(fmaf(2.0f, (float)key, (float)na), 0.0f);
-              const uint32_t pid = args.col_ids ? args.col_ids[S.b.id_off + col] : col;
+              // (the pick's id is needed only for out_idx / out_cnt: the build path writes local columns)
+              const uint32_t pid = (args.out_idx || args.out_cnt) && args.col_ids ? args.col_ids[S.b.id_off + col] : col;
               if (args.out_idx) args.out_idx[obase + o] = pid;
               if (args.out_col) args.out_col[obase + o] = (uint16_t)col;
               if (args.out_dist) args.out_dist[obase + o] = D;
