@@ -628,7 +628,7 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
                   const int32_t a = min(qv[jj], qv[jj + 1]), b = max(qv[jj], qv[jj + 1]);
                   const int32_t t = max(m1, a);
                   m1 = min(m1, a);
-                  m2 = min(min(t, m2), b);  // second smallest of {m1, m2} u {a, b}
+                  m2 = __vimin3_s32(t, m2, b);  // second smallest of {m1, m2} u {a, b} (3-input min)
                 }
               }
               // decode (key = q >> 5, exact: arithmetic shift) and insert; columns grow with the chunks, so
