@@ -1,5 +1,5 @@
-"""Leaf-kernel experiment: time pipnn_leaf_pick on the C2 leaves for each PIPNN_DEBUG_EPI value given on the
-command line (default 0 1 2 0). Bits 0-3: 1 = epilogue skips all tile processing, 2 = skips pass 2;
+"""Leaf-kernel experiment: time pipnn_leaf_pick on a config's leaves under PIPNN_DEBUG_EPI (set in the environment;
+the library reads it once per process). Bits 0-3: 1 = epilogue skips all tile processing, 2 = skips pass 2;
 bit 64: wait profile. CFG=C3|C4|... selects the config (L2 metric)."""
 import os, sys, numpy as np, torch
 sys.path.insert(0, '/root/repo')
@@ -7,11 +7,21 @@ import synth
 import paper_2602_21247_b200 as P
 cfg = getattr(synth, os.environ.get("CFG", "C2"))
 X = torch.from_numpy(synth.gen_points(cfg)).cuda()
-pp = P.partition_params(c_max=cfg.c_max, fanout=cfg.fanout, seed=cfg.seed)
-off, ids = P.pipnn_partition(X, pp)
+# the partition is computed without the debug knobs (read once per process by the library) and cached on disk
+cache = f"/tmp/leafexp_{cfg.name}.pt"
+if os.path.exists(cache):
+    off, ids = (t.cuda() for t in torch.load(cache))
+else:
+    import subprocess
+    subprocess.check_call([sys.executable, "-c", f"""
+import sys, torch; sys.path.insert(0, '/root/repo'); import synth, paper_2602_21247_b200 as P
+cfg = synth.{cfg.name}; X = torch.from_numpy(synth.gen_points(cfg)).cuda()
+pp = P.partition_params(c_max=cfg.c_max, c_min=cfg.c_min, p_samp=cfg.p_samp, fanout=cfg.fanout, seed=cfg.seed)
+off, ids = P.pipnn_partition(X, pp); torch.save((off.cpu(), ids.cpu()), '{cache}')"""],
+                          env={k: v for k, v in os.environ.items() if not k.startswith("PIPNN_")})
+    off, ids = (t.cuda() for t in torch.load(cache))
 ref = None
-for dbg in (sys.argv[1:] or ["0", "1", "2", "0"]):
-    os.environ["PIPNN_DEBUG_EPI"] = dbg
+for dbg in (sys.argv[1:] or [os.environ.get("PIPNN_DEBUG_EPI", "0")]):  # (the knob is read once: one value per run)
     ts = []
     for rep in range(5):
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
