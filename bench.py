@@ -547,7 +547,7 @@ def main():
         _, e2e_val = job_throughput(t0.elapsed_time(t1) / K, cfg.n, ws, dev)
         e2e_mode = (f"pipelined over {K} steps: H2D of step i+1 and D2H of step i on a copy stream overlap build i "
                     "(first H2D and last D2H exposed)")
-        del builder2, Xd2
+        del builder2, Xd2, bufs, b, xd  # (the builders' workspaces: the evaluation below needs the memory)
 
     if rank == 0:
         peaks, src = measured_peaks()

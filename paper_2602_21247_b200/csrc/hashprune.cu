@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(NT) hp_emit_kernel(const int64_t* __restrict__
                                                       const float* __restrict__ dist, const ST* __restrict__ S, int m,
                                                       int stage_sk, uint64_t* __restrict__ fwd, uint64_t* __restrict__ rev,
                                                       uint32_t* __restrict__ rev_start, uint32_t* __restrict__ rev_cnt,
-                                                      int64_t* __restrict__ n_edges) {
+                                                      uint2* __restrict__ rev_meta, int64_t* __restrict__ n_edges) {
   extern __shared__ __align__(16) uint8_t esm[];
   __shared__ uint32_t tot_sh;
   __shared__ uint32_t part[NT];
@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(NT) hp_emit_kernel(const int64_t* __restrict__
   for (int j = threadIdx.x; j < s; j += blockDim.x) {
     rev_start[o0 + j] = (uint32_t)(rbase + rs[j]);  // absolute offset into rev (I*k < 2^32, checked on the host)
     rev_cnt[o0 + j] = rc[j];
+    rev_meta[o0 + j] = make_uint2((uint32_t)(rbase + rs[j]), rc[j]);  // both in one 8-B load for the merge
     rc[j] = 0;
   }
   __syncthreads();
@@ -483,9 +484,9 @@ struct OwnerKeys {
 // Returns false (nothing written) when more than l_max buckets survive.
 template <int E>
 __device__ __forceinline__ bool merge_owner_regs(int lane, int T, int c, int k, const uint64_t* res_in,
-                                                 const uint32_t* sinst, const uint32_t* sbeg, int ni,
-                                                 const uint64_t* __restrict__ fwd, const uint64_t* __restrict__ rev,
-                                                 const uint32_t* __restrict__ rev_start, int l_max, uint64_t* res,
+                                                 const uint32_t* sinst, const uint32_t* sbeg, const uint32_t* srs,
+                                                 int ni, const uint64_t* __restrict__ fwd,
+                                                 const uint64_t* __restrict__ rev, int l_max, uint64_t* res,
                                                  int& B_out) {
   uint64_t key[E];
 #pragma unroll
@@ -501,7 +502,7 @@ __device__ __forceinline__ bool merge_owner_regs(int lane, int T, int c, int k, 
         while (j + 1 < ni && (int)sbeg[j + 1] <= idx) ++j;  // segment j: k forward then rev keys of instance j
         const int o = idx - (int)sbeg[j];
         const uint32_t i = sinst[j];
-        v = o < k ? fwd[(int64_t)i * k + o] : rev[(uint64_t)rev_start[i] + (o - k)];
+        v = o < k ? fwd[(int64_t)i * k + o] : rev[(uint64_t)srs[j] + (o - k)];
       }
     }
     key[e] = v;
@@ -536,11 +537,10 @@ __device__ __forceinline__ bool merge_owner_regs(int lane, int T, int c, int k, 
 __global__ void __launch_bounds__(256) hp_merge_inst_kernel(int64_t n, int l_max, int k, const uint64_t* __restrict__ inv_start,
                                                             const uint32_t* __restrict__ inv, const uint64_t* __restrict__ fwd,
                                                             const uint64_t* __restrict__ rev,
-                                                            const uint32_t* __restrict__ rev_start,
-                                                            const uint32_t* __restrict__ rev_cnt,
+                                                            const uint2* __restrict__ rev_meta,
                                                             uint64_t* __restrict__ slots, uint32_t* __restrict__ count,
                                                             uint32_t* __restrict__ defer, uint32_t* __restrict__ defer_n) {
-  __shared__ uint32_t s_inst[8][32], s_beg[8][32];
+  __shared__ uint32_t s_inst[8][32], s_beg[8][32], s_rs[8][32];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -554,10 +554,12 @@ __global__ void __launch_bounds__(256) hp_merge_inst_kernel(int64_t n, int l_max
     }
     const int c = (int)count[u];
     int sz = 0;
-    uint32_t inst = 0;
+    uint32_t inst = 0, rs0 = 0;
     if (lane < ni) {
       inst = inv[i0 + lane];
-      sz = k + (int)rev_cnt[inst];
+      const uint2 mt = rev_meta[inst];  // (rev start, rev count) in one load
+      rs0 = mt.x;
+      sz = k + (int)mt.y;
     }
     int x = sz;  // inclusive prefix over the instance segments
 #pragma unroll
@@ -573,13 +575,14 @@ __global__ void __launch_bounds__(256) hp_merge_inst_kernel(int64_t n, int l_max
     __syncwarp();
     s_inst[wl][lane] = inst;
     s_beg[wl][lane] = (uint32_t)(x - sz);
+    s_rs[wl][lane] = rs0;
     __syncwarp();
     uint64_t* res = slots + u * (int64_t)l_max;
     int B = 0;
     bool ok;
-    if (T <= 32) ok = merge_owner_regs<1>(lane, T, c, k, res, s_inst[wl], s_beg[wl], ni, fwd, rev, rev_start, l_max, res, B);
-    else if (T <= 64) ok = merge_owner_regs<2>(lane, T, c, k, res, s_inst[wl], s_beg[wl], ni, fwd, rev, rev_start, l_max, res, B);
-    else ok = merge_owner_regs<4>(lane, T, c, k, res, s_inst[wl], s_beg[wl], ni, fwd, rev, rev_start, l_max, res, B);
+    if (T <= 32) ok = merge_owner_regs<1>(lane, T, c, k, res, s_inst[wl], s_beg[wl], s_rs[wl], ni, fwd, rev, l_max, res, B);
+    else if (T <= 64) ok = merge_owner_regs<2>(lane, T, c, k, res, s_inst[wl], s_beg[wl], s_rs[wl], ni, fwd, rev, l_max, res, B);
+    else ok = merge_owner_regs<4>(lane, T, c, k, res, s_inst[wl], s_beg[wl], s_rs[wl], ni, fwd, rev, l_max, res, B);
     if (!ok) {
       if (lane == 0) defer[atomicAdd(defer_n, 1u)] = (uint32_t)u;
       continue;
@@ -844,6 +847,7 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
   uint64_t* rev = ar.take<uint64_t>(P);
   uint32_t* rev_start = ar.take<uint32_t>(std::max<int64_t>(1, n_inst));
   uint32_t* rev_cnt = ar.take<uint32_t>(std::max<int64_t>(1, n_inst));
+  uint2* rev_meta = ar.take<uint2>(std::max<int64_t>(1, n_inst));
   Grouping g = take_grouping(n, ar);  // point -> instances
   uint32_t* inv = ar.take<uint32_t>(std::max<int64_t>(1, n_inst));
   uint32_t* defer = ar.take<uint32_t>(n);
@@ -865,7 +869,7 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
     PIPNN_CUDA(cudaFuncSetAttribute(hp_emit_kernel<ST, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
     hp_emit_kernel<ST, NTH><<<(unsigned)n_leaves, NTH, smem, c.st>>>(leaf_off, leaf_ids, k, cols, dist,           \
                                                                    (const ST*)sketch, m, stage_sk, fwd, rev,       \
-                                                                   rev_start, rev_cnt, n_edges_dev);              \
+                                                                   rev_start, rev_cnt, rev_meta, n_edges_dev);    \
   } while (0)
   if (sk_int) {
     if (big) HP_EMIT(int32_t, 1024); else HP_EMIT(int32_t, 256);
@@ -887,8 +891,8 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
   const int64_t blocks = std::min<int64_t>(ceil_div(n, 8), (int64_t)num_sms() * 32);
   // (measured: the sort-free set merge below, match_any / SMEM-table buckets, was slower than the register
   // bitonic merge: C5 44.0 vs 31.9 ms, C2 0.90 vs 0.55 ms — the merge is bound by its dependent gathers)
-  hp_merge_inst_kernel<<<(unsigned)blocks, 256, 0, c.st>>>(n, l_max, k, g.start, inv, fwd, rev, rev_start, rev_cnt,
-                                                               slots, count, defer, defer_n);
+  hp_merge_inst_kernel<<<(unsigned)blocks, 256, 0, c.st>>>(n, l_max, k, g.start, inv, fwd, rev, rev_meta, slots,
+                                                               count, defer, defer_n);
   PIPNN_LAUNCHED("hp_merge_inst_kernel", c.st);
   if (m <= 12) {
     const int tsm = (int)((size_t)8 << m);

@@ -1,0 +1,16 @@
+# round-2 evidence: GPU tests, smoke, the default bench (C5, full), the reference arm, the other configs,
+# the C5 launch list, an ncu capture of the C5 leaf kernel (traffic) and of the C2 leaf kernel
+set -x
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?; tail -2 gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/r2_bench.json 2> gpurun_out/r2_bench.err; echo bench=$?; tail -c 3000 gpurun_out/r2_bench.json
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r2_bench_ref.json 2> gpurun_out/r2_bench_ref.err; echo ref=$?; cat gpurun_out/r2_bench_ref.json
+for C in C2 C3 C4 C1 C2-f10x3 C2-rep2; do timeout 600 python bench.py --config $C --steps 5 --warmup 3 --no-cpu-baseline --no-int8-peak > gpurun_out/r2_bench_$C.json 2> gpurun_out/r2_bench_$C.err; echo bench_$C=$?; done
+timeout 300 python bench.py --config C2 --shard --steps 3 --warmup 2 > gpurun_out/r2_bench_C2-shard1.json 2> gpurun_out/r2_bench_shard.err; echo shard=$?
+timeout 300 python bench.py --config C3 --quant --steps 5 --warmup 3 --no-cpu-baseline --no-int8-peak --recall-queries 2000 > gpurun_out/r2_bench_C3-quant.json 2> gpurun_out/r2_bench_quant.err; echo quant=$?
+CMD="python tools/build_once.py C5"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_launches_C5.csv $CMD > gpurun_out/r2_ncu_launch.log 2>&1; echo ncu_launch=$?
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:dist_topk_kernelILb1ELb0ELi8ELb1E -s 2 -c 1 -o gpurun_out/r2_leaf_C5 $CMD > gpurun_out/r2_ncu_leaf.log 2>&1; echo ncu_leaf=$?
+ncu -i gpurun_out/r2_leaf_C5.ncu-rep --page raw --csv > gpurun_out/r2_leaf_C5_raw.csv 2>/dev/null
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:dist_topk_kernelILb1ELb0ELi8ELb1E -s 0 -c 1 -o gpurun_out/r2_leaf_C2 python tools/build_once.py C2 > gpurun_out/r2_ncu_leaf2.log 2>&1; echo ncu_leaf2=$?
+ncu -i gpurun_out/r2_leaf_C2.ncu-rep --page raw --csv > gpurun_out/r2_leaf_C2_raw.csv 2>/dev/null
