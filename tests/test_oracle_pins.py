@@ -168,6 +168,65 @@ def test_merge_spec_examples():
     assert g[0] == -1 and g[1] == g[2]
 
 
+def _same(g, a, b):
+    return g[a] == g[b]
+
+
+def test_merge_bins_close_in_key_order():
+    """R15: small groups are taken in (key, id) order and a bin closes once the SUM of its sizes
+    reaches C_min. Hand-derived: sizes [30, 40, 50, 20], C_min 60."""
+    s = [30, 40, 50, 20]
+    # key order 1, 3, 0, 2 -> sizes 40, 20 | 30, 50 -> bins {1, 3} (60) and {0, 2} (80)
+    g, ng = O.merge_plan(s, np.array([3, 1, 4, 2], np.uint64), [0, 1, 2, 3], 60, 1000)
+    assert ng == 2 and _same(g, 1, 3) and _same(g, 0, 2) and not _same(g, 0, 1)
+    # identity order -> 30, 40 | 50, 20 -> bins {0, 1} (70) and {2, 3} (70)
+    g, ng = O.merge_plan(s, np.array([1, 2, 3, 4], np.uint64), [0, 1, 2, 3], 60, 1000)
+    assert ng == 2 and _same(g, 0, 1) and _same(g, 2, 3) and not _same(g, 0, 2)
+    # equal keys: the id breaks the tie (ids 3, 1, 4, 2 reproduce the first order)
+    g, ng = O.merge_plan(s, np.array([7, 7, 7, 7], np.uint64), [3, 1, 4, 2], 60, 1000)
+    assert ng == 2 and _same(g, 1, 3) and _same(g, 0, 2) and not _same(g, 0, 1)
+
+
+def test_merge_leftover_joins_first_closed_bin():
+    """R15: a leftover (the small groups after the last closed bin) joins the FIRST closed bin."""
+    g, ng = O.merge_plan([40, 30, 10], np.array([1, 2, 3], np.uint64), [0, 1, 2], 60, 1000)
+    assert ng == 1 and _same(g, 0, 1) and _same(g, 0, 2)
+    # bins {0, 1} (70) and {2, 3} (65) close; the leftover {4} joins {0, 1}
+    g, ng = O.merge_plan([40, 30, 35, 30, 10], np.array([1, 2, 3, 4, 5], np.uint64), [0, 1, 2, 3, 4], 60, 1000)
+    assert ng == 2 and _same(g, 4, 0) and _same(g, 0, 1) and _same(g, 2, 3) and not _same(g, 4, 2)
+
+
+def test_merge_leftover_without_bins_joins_smallest_fitting_big():
+    """R15: with no closed bin the leftover joins the smallest Big group whose size + leftover sum <= C_max (ties
+    by key), else stands alone (a group below C_min survives only if every merge would exceed C_max)."""
+    sizes = [500, 300, 300, 20, 15]  # Big: 0, 1, 2 (>= C_min 100); small 3, 4 (sum 35 < C_min: no bin closes)
+    keys = np.array([9, 5, 2, 1, 1], np.uint64)
+    g, ng = O.merge_plan(sizes, keys, [0, 1, 2, 3, 4], 100, 400)  # 500 + 35 > 400; 300s fit; key 2 < 5
+    assert ng == 3 and _same(g, 3, 4) and _same(g, 3, 2) and not _same(g, 3, 1) and not _same(g, 3, 0)
+    g, ng = O.merge_plan(sizes, keys, [0, 1, 2, 3, 4], 100, 320)  # 300 + 35 > 320: the leftover stands alone
+    assert ng == 4 and _same(g, 3, 4) and len({g[0], g[1], g[2], g[3]}) == 4
+    g, ng = O.merge_plan([300, 200, 20], np.array([1, 2, 3], np.uint64), [0, 1, 2], 100, 400)  # smallest fitting Big
+    assert ng == 2 and _same(g, 2, 1) and not _same(g, 2, 0)
+
+
+def test_merge_survival_invariant_fuzz():
+    """an output group below C_min survives only if it is the only group or merging it with any other
+    output group would exceed C_max; every merged group is a union of whole input groups with at most one Big."""
+    rng = np.random.default_rng(1)
+    for _ in range(300):
+        c_max = int(rng.integers(30, 3000))
+        c_min = int(rng.integers(1, max(2, (c_max - 1) // 3)))
+        ng = int(rng.integers(1, 40))
+        sizes = np.where(rng.random(ng) < 0.6, rng.integers(1, c_min + 1, ng), rng.integers(c_min, 2 * c_max, ng))
+        keys = rng.integers(0, 2 ** 63, ng, dtype=np.uint64)
+        g, n_out = O.merge_plan(sizes, keys, np.arange(ng), c_min, c_max)
+        tot = np.array([sizes[g == t].sum() for t in range(n_out)])
+        for t in range(n_out):
+            assert (sizes[g == t] >= c_min).sum() <= 1
+            if tot[t] < c_min and n_out > 1:
+                assert all(tot[t] + tot[u] > c_max for u in range(n_out) if u != t)
+
+
 def test_merge_bounds_fuzz():
     rng = np.random.default_rng(0)
     for _ in range(300):
