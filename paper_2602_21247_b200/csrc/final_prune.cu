@@ -641,8 +641,44 @@ __global__ void __launch_bounds__(256, CP == 32 ? 3 : 1) fp_gram_kernel(const vo
     for (int e = 0; e < E; ++e)
 #pragma unroll
       for (int w = 0; w < E; ++w) Pm[e][w] = M[e][w] = 0u;
+    // Fast path (one word per lane, d <= 256): the masks over k32 = 32 D(u, i) + i (D < 2^24), which is the
+    // (D, id) order unless two candidates share D (checked below; then the general loop). y precedes i iff
+    // k32_y - k32_i < 0, and y prunes i iff an (n_y + n_i - 2 G_yi) - ad D(u, i) < 0 (|.| < 2^31 for d <= 256);
+    // both bits enter their masks by a funnel shift of the difference's sign (y descending, so bit y lands at
+    // position y), M = P & (prune bits).
+    bool fast = false;
+    if (E == 1 && U8 && d <= 256) {
+      const bool vi = lane < c;
+      const uint32_t du = (uint32_t)(key[0] >> 32);
+      const int32_t k32 = vi ? (int32_t)((du << 5) | (uint32_t)lane) : 0x7FFFFFFF;
+      const int32_t ani = an * (int32_t)ni[0];
+      const int32_t ci = ani - (int32_t)thr_i[0];
+      const int32_t an2 = -2 * an;
+      const DT* gcol = G + lane + 1;
+      uint32_t P = 0u, Q = 0u;
+      for (int y = c - 1; y >= 0; --y) {
+        const int32_t ky = __shfl_sync(0xffffffffu, k32, y);
+        const int32_t ay = __shfl_sync(0xffffffffu, ani, y);
+        const int32_t gy = (int32_t)gcol[(size_t)(y + 1) * DS];
+        P = __funnelshift_l((uint32_t)(ky - k32), P, 1);
+        Q = __funnelshift_l((uint32_t)(gy * an2 + (ay + ci)), Q, 1);
+      }
+      // D ties: neighbours in the k32 order (rank = popc(P)) with the same D; G row 0 (D(u, .) is in the keys
+      // already) is the scratch
+      uint32_t* sc = reinterpret_cast<uint32_t*>(G);
+      const int rk = __popc(P);
+      __syncwarp();
+      if (vi) sc[rk] = du;
+      __syncwarp();
+      const bool tie = vi && rk + 1 < c && sc[rk + 1] == du;
+      fast = __ballot_sync(0xffffffffu, tie) == 0u;
+      if (fast) {
+        Pm[0][0] = P;
+        M[0][0] = P & Q;
+      }
+    }
 #pragma unroll
-    for (int wy = 0; wy < E; ++wy) {
+    for (int wy = 0; wy < (fast ? 0 : E); ++wy) {
       const int ylim = min(32, c - 32 * wy);
       for (int b = 0; b < ylim; ++b) {
         const int y = 32 * wy + b;

@@ -1,0 +1,7 @@
+# final-prune iteration: u8 prune/build parity, then C5 (and C2) stage times
+timeout 900 python -m pytest tests/test_gpu_stages.py tests/test_gpu_build.py -q -x --timeout 600 2>&1 | tail -3
+for C in ${CFGS:-C5 C2}; do
+timeout 600 python bench.py --config $C --steps ${STEPS:-3} --warmup 3 --no-cpu-baseline --recall-queries 0 --no-int8-peak > gpurun_out/b_$C.json 2>gpurun_out/b_$C.err
+python -c "
+import json; d=json.loads(open('gpurun_out/b_$C.json').read().strip().splitlines()[-1]); print('$C', round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['stages_ms'].items()})" || tail -3 gpurun_out/b_$C.err
+done
