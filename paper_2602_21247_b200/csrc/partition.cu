@@ -114,6 +114,170 @@ __global__ void iota_kernel(uint32_t* __restrict__ out, int64_t n) {
     out[e] = (uint32_t)e;
 }
 
+// The level's work items (one per 128-row block of every group's members, resp. leaders): CTA g writes
+// its group's items at its offsets (host prefix sums over the groups; the item lists themselves never pass the host).
+__global__ void level_items_kernel(const int64_t* __restrict__ offA, const int64_t* __restrict__ offB, int G,
+                                   WorkItem* __restrict__ itA, WorkItem* __restrict__ itB) {
+  const int g = blockIdx.x;
+  if (g >= G) return;
+  const int64_t a0 = offA[g], a1 = offA[g + 1], b0 = offB[g], b1 = offB[g + 1];
+  for (int64_t i = a0 + threadIdx.x; i < a1; i += blockDim.x) itA[i] = WorkItem{g, (int32_t)(i - a0)};
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) itB[i] = WorkItem{g, (int32_t)(i - b0)};
+}
+
+// Leaders of every group (Alg. 5 line 3, R12): the l_g candidates of smallest priority, then by id. One
+// CTA (1024 threads) per group over its candidate segment (cap entries; unfilled slots hold key ~0; real keys are
+// distinct: mix(K, .) is injective):
+//   * cap <= 2048: the segment bitonic-sorted by key in SMEM, the first l_g ids taken;
+//   * larger: an MSB-first radix select, 12 bits per pass: a SMEM histogram of the digit of every key under the
+//     current prefix, the bin holding the l_g-th key found by a block scan; keys in smaller bins are taken, the
+//     boundary bin becomes the prefix, until it holds <= 2048 keys, which are bitonic-sorted and the rest taken;
+// then the l_g ids are bitonic-sorted ascending and written to lead_sorted.
+constexpr int kLeadSortMax = 1 << 20;  // segments above this use the library sort (redo_unfiltered only)
+constexpr int kLeadSmall = 2048;
+__device__ __forceinline__ int next_pow2_dev(int x) { return x <= 1 ? 1 : 1 << (32 - __clz(x - 1)); }
+template <typename K, typename V>
+__device__ void block_bitonic(K* k, V* v, int N) {  // ascending by k, N a power of two, all threads of the block
+  for (int size = 2; size <= N; size <<= 1)
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < (N >> 1); i += blockDim.x) {
+        const int lo = 2 * stride * (i / stride) + (i % stride), hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const K a = k[lo], b = k[hi];
+        if ((a > b) == up) {
+          k[lo] = b;
+          k[hi] = a;
+          if (v) {
+            const V t = v[lo];
+            v[lo] = v[hi];
+            v[hi] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+}
+// SMEM: keys [kLeadSmall] u64 | ids [kLeadSmall] u32 | hist [4096] u32 | warp sums [32] | sel [l_max] u32 | scalars
+__global__ void __launch_bounds__(1024) leaders_kernel(const PGroup* __restrict__ gs, int G, const uint64_t* __restrict__ ck,
+                                                       const uint32_t* __restrict__ cv, uint32_t* __restrict__ lead_sorted) {
+  extern __shared__ __align__(16) uint64_t lsm[];
+  __shared__ int nsel_sh, bin_sh, below_sh, nb_sh;
+  const int g = blockIdx.x;
+  if (g >= G) return;
+  const PGroup p = gs[g];
+  const int cap = p.cap, l = p.l, tid = threadIdx.x, nt = blockDim.x;
+  uint64_t* k = lsm;
+  uint32_t* v = reinterpret_cast<uint32_t*>(k + kLeadSmall);
+  uint32_t* hist = v + kLeadSmall;
+  uint32_t* wsum = hist + 4096;
+  uint32_t* sel = wsum + 32;  // [next_pow2(l)]
+  const uint64_t* key = ck + p.cand_off;
+  const uint32_t* id = cv + p.cand_off;
+  if (tid == 0) nsel_sh = 0;
+  __syncthreads();
+  int need = l;  // still to select, all from keys under the prefix
+  uint64_t prefix = 0;
+  int pbits = 0;  // bits of the prefix (keys with key >> (64 - pbits) == prefix are "under" it)
+  bool small = cap <= kLeadSmall;
+  while (!small) {
+    const int shift = 64 - pbits - 12;  // digit = bits [shift, shift + 12) (the last pass: 4 bits, shift 0)
+    const int sh = shift < 0 ? 0 : shift;
+    const uint32_t dmask = shift < 0 ? 0xFu : 0xFFFu;
+    for (int i = tid; i < 4096; i += nt) hist[i] = 0;
+    __syncthreads();
+    for (int i = tid; i < cap; i += nt) {
+      const uint64_t x = key[i];
+      if (pbits == 0 || (x >> (64 - pbits)) == prefix) atomicAdd(&hist[(x >> sh) & dmask], 1u);
+    }
+    __syncthreads();
+    // block exclusive scan of the 4096 bins (4 per thread), then the bin b with below(b) < need <= below(b + 1)
+    uint32_t h4[4], s = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      h4[t] = hist[4 * tid + t];
+      s += h4[t];
+    }
+    uint32_t inc = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if ((tid & 31) >= o) inc += y;
+    }
+    if ((tid & 31) == 31) wsum[tid >> 5] = inc;
+    __syncthreads();
+    if (tid < 32) {
+      uint32_t w = wsum[tid], wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+        if (tid >= o) wi += y;
+      }
+      wsum[tid] = wi - w;  // exclusive warp offsets
+    }
+    __syncthreads();
+    uint32_t run = wsum[tid >> 5] + inc - s;  // exclusive prefix of this thread's first bin
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (run < (uint32_t)need && run + h4[t] >= (uint32_t)need) {
+        bin_sh = 4 * tid + t;
+        below_sh = (int)run;
+        nb_sh = (int)h4[t];
+      }
+      run += h4[t];
+    }
+    __syncthreads();
+    const int b = bin_sh, below = below_sh, nb = nb_sh;
+    // take every key under the prefix whose digit is below b
+    for (int i = tid; i < cap; i += nt) {
+      const uint64_t x = key[i];
+      if ((pbits == 0 || (x >> (64 - pbits)) == prefix) && (int)((x >> sh) & dmask) < b)
+        sel[atomicAdd(&nsel_sh, 1)] = id[i];
+    }
+    need -= below;
+    prefix = (prefix << (shift < 0 ? 4 : 12)) | (uint64_t)b;
+    pbits += shift < 0 ? 4 : 12;
+    __syncthreads();
+    if (nb <= kLeadSmall || pbits >= 64) {
+      // the boundary bin: its keys into the small buffer
+      if (tid == 0) bin_sh = 0;
+      __syncthreads();
+      for (int i = tid; i < cap; i += nt) {
+        const uint64_t x = key[i];
+        if ((x >> (64 - pbits)) == prefix || pbits >= 64 && x == prefix) {
+          const int j = atomicAdd(&bin_sh, 1);
+          if (j < kLeadSmall) {
+            k[j] = x;
+            v[j] = id[i];
+          }
+        }
+      }
+      __syncthreads();
+      small = true;
+    }
+  }
+  // sort the small set by key and take its first `need`
+  const int ns = cap <= kLeadSmall ? cap : min(bin_sh, kLeadSmall);
+  const int N = next_pow2_dev(ns < 2 ? 2 : ns);
+  if (cap <= kLeadSmall)
+    for (int i = tid; i < N; i += nt) {
+      k[i] = i < cap ? key[i] : ~0ull;
+      v[i] = i < cap ? id[i] : 0u;
+    }
+  else
+    for (int i = ns + tid; i < N; i += nt) k[i] = ~0ull;
+  __syncthreads();
+  block_bitonic<uint64_t, uint32_t>(k, v, N);
+  const int base = nsel_sh;
+  for (int j = tid; j < need; j += nt) sel[base + j] = v[j];
+  __syncthreads();
+  // the l leaders ascending by id
+  const int N2 = next_pow2_dev(l < 2 ? 2 : l);
+  for (int i = l + tid; i < N2; i += nt) sel[i] = 0xFFFFFFFFu;
+  __syncthreads();
+  block_bitonic<uint32_t, uint32_t>(sel, nullptr, N2);
+  for (int j = tid; j < l; j += nt) lead_sorted[p.lead_off + j] = sel[j];
+}
+
 // first l_g sorted candidates -> leaders (then sorted by id with a segmented sort)
 __global__ void take_leaders_kernel(const PGroup* __restrict__ gs, int G, const uint32_t* __restrict__ cv_sorted,
                                     uint32_t* __restrict__ lead) {
@@ -438,6 +602,7 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
   DistSeg* dsegs = ar.take<DistSeg>(cp.G);
   WorkItem* itA = ar.take<WorkItem>(cp.rowsA / 128 + 1);
   WorkItem* itB = ar.take<WorkItem>(cp.rowsB / 128 + 1);
+  int64_t* d_itoff = ar.take<int64_t>(2 * (cp.G + 1));
   int64_t* n_it = ar.take<int64_t>(2);
   uint32_t* pk = ar.take<uint32_t>(cp.L);
   uint32_t* iota = ar.take<uint32_t>(cp.C);
@@ -608,34 +773,50 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
     PIPNN_LAUNCHED("prio_check_kernel", st);
     const double t_prio = dbg_timing ? wall() : 0.0;
     size_t tb = cub_bytes;
-    if (G == 1) {
+    int max_cap = 0;
+    for (int g = 0; g < G; ++g) max_cap = std::max(max_cap, hg[g].cap);
+    if (max_cap <= kLeadSortMax) {
+      // hand-written: one CTA per group (the common case; no library sort, no host synchronisation)
+      int max_l = 2;
+      for (int g = 0; g < G; ++g) max_l = std::max(max_l, hg[g].l);
+      int np = 2;
+      while (np < max_l) np <<= 1;
+      const int smem = kLeadSmall * 12 + 4096 * 4 + 32 * 4 + np * 4;
+      if (smem > 200 * 1024) return fail(PIPNN_EUNSUPPORTED, "partition: leader count too large");
+      PIPNN_CUDA(cudaFuncSetAttribute(leaders_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      leaders_kernel<<<G, 1024, smem, st>>>(d_groups, G, ck, cv, lead_sorted);
+      PIPNN_LAUNCHED("leaders_kernel", st);
+    } else if (G == 1) {
+      // (a group whose filter was dropped, redo_unfiltered: every member is a candidate)
       PIPNN_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, tb, ck, ck2, cv, cv2, (int)NC, 0, 64, st));
     } else {
       PIPNN_CUDA(cub::DeviceSegmentedSort::SortPairs(cub_tmp, tb, ck, ck2, cv, cv2, (int)NC, G, d_cand_seg,
                                                      d_cand_seg + 1, st));
     }
-    take_leaders_kernel<<<G, 128, 0, st>>>(d_groups, G, cv2, lead);
-    PIPNN_LAUNCHED("take_leaders_kernel", st);
-    tb = cub_bytes;
-    if (G == 1) {
-      PIPNN_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, lead, lead_sorted, (int)C, 0, 32, st));
-    } else {
-      PIPNN_CUDA(cub::DeviceSegmentedSort::SortKeys(cub_tmp, tb, lead, lead_sorted, (int)C, G, d_lead_seg,
-                                                    d_lead_seg + 1, st));
+    if (max_cap > kLeadSortMax) {
+      take_leaders_kernel<<<G, 128, 0, st>>>(d_groups, G, cv2, lead);
+      PIPNN_LAUNCHED("take_leaders_kernel", st);
+      tb = cub_bytes;
+      if (G == 1) {
+        PIPNN_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp, tb, lead, lead_sorted, (int)C, 0, 32, st));
+      } else {
+        PIPNN_CUDA(cub::DeviceSegmentedSort::SortKeys(cub_tmp, tb, lead, lead_sorted, (int)C, G, d_lead_seg,
+                                                      d_lead_seg + 1, st));
+      }
     }
     const double t_leaders = dbg_timing ? wall() : 0.0;
     // ---- 2. nearest f_g leaders of every member (tcgen05 distance tiles + top-f), written directly as
     // (child = lead_off + leader index, member id) pairs with the child histogram
     std::vector<TileSeg> hA(G), hB(G);
     std::vector<DistSeg> hD(G);
-    std::vector<WorkItem> hItA, hItB;
+    std::vector<int64_t> hOffA(G + 1), hOffB(G + 1);  // item offsets: one item per 128-row block
     int64_t posA = 0, posB = 0;
     for (int g = 0; g < G; ++g) {
       const PGroup& q = hg[g];
       TileSeg a{q.off, posA, (int32_t)round_up(q.size, 128), (int32_t)q.size};
       TileSeg b{q.lead_off, posB, (int32_t)round_up(q.l, 128), q.l};
-      for (int32_t rb = 0; rb < a.pad / 128; ++rb) hItA.push_back(WorkItem{g, rb});
-      for (int32_t rb = 0; rb < b.pad / 128; ++rb) hItB.push_back(WorkItem{g, rb});
+      hOffA[g] = posA / 128;
+      hOffB[g] = posB / 128;
       posA += a.pad;
       posB += b.pad;
       hA[g] = a;
@@ -651,15 +832,19 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
       hD[g] = d;
     }
     if (posA > cp.rowsA || posB > cp.rowsB) return fail(PIPNN_ECAPACITY, "partition: tiled capacity");
-    const int64_t nItA = (int64_t)hItA.size(), nItB = (int64_t)hItB.size();
+    const int64_t nItA = posA / 128, nItB = posB / 128;
+    hOffA[G] = nItA;
+    hOffB[G] = nItB;
     const int64_t nits[2] = {nItA, nItB};
     PIPNN_CUDA(g_pin_level.copy(tsA, hA.data(), G * sizeof(TileSeg), st));
     PIPNN_CUDA(g_pin_level.copy(tsB, hB.data(), G * sizeof(TileSeg), st));
     PIPNN_CUDA(g_pin_level.copy(dsegs, hD.data(), G * sizeof(DistSeg), st));
-    PIPNN_CUDA(g_pin_level.copy(itA, hItA.data(), nItA * sizeof(WorkItem), st));
-    PIPNN_CUDA(g_pin_level.copy(itB, hItB.data(), nItB * sizeof(WorkItem), st));
+    PIPNN_CUDA(g_pin_level.copy(d_itoff, hOffA.data(), (G + 1) * sizeof(int64_t), st));
+    PIPNN_CUDA(g_pin_level.copy(d_itoff + (G + 1), hOffB.data(), (G + 1) * sizeof(int64_t), st));
     PIPNN_CUDA(g_pin_level.copy(n_it, nits, 2 * sizeof(int64_t), st));
     PIPNN_CUDA(g_pin_level.flush(st));
+    level_items_kernel<<<G, 256, 0, st>>>(d_itoff, d_itoff + (G + 1), G, itA, itB);
+    PIPNN_LAUNCHED("level_items_kernel", st);
     const double t_plan2 = dbg_timing ? wall() : 0.0;
     PIPNN_TRY(gather_tiled(X, mem, tsA, itA, n_it, nItA, TA, nA, c));
     // uint8 with fanout <= 2 at this level: leader norms in the packed form of the single-pass top-2
@@ -786,7 +971,9 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
       }
     }
     if (staged > cp.L || n_leaves > cp.leaves - 1) return fail(PIPNN_ECAPACITY, "partition: leaf capacity");
+    const double t_merge = dbg_timing ? wall() : 0.0;
     PIPNN_TRY(flush_jobs(nxt));
+    const double t_flush = dbg_timing ? wall() : 0.0;
     if (use_subtree && !next.empty() && depth + 1 >= subtree_min_depth) {
       std::vector<DevGroup> dg;
       std::vector<HGroup> keep;
@@ -807,9 +994,10 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
       }
     }
     if (dbg_timing)
-      std::fprintf(stderr, "[pipnn] depth %d: groups %d members %lld | enqueue %.0f us (prio %.0f leaders %.0f plan %.0f gather %.0f dist %.0f sort %.0f), wait %.0f us, host plan %.0f us\n",
+      std::fprintf(stderr, "[pipnn] depth %d: groups %d members %lld | enqueue %.0f us (prio %.0f leaders %.0f plan %.0f gather %.0f dist %.0f sort %.0f), wait %.0f us, host plan %.0f us (merge %.0f jobs %.0f)\n",
                    depth, G, (long long)M, t_sync0 - t_level0, t_prio - t_level0, t_leaders - t_prio, t_plan2 - t_leaders,
-                   t_gather - t_plan2, t_dist - t_gather, t_sync0 - t_dist, t_sync1 - t_sync0, wall() - t_sync1);
+                   t_gather - t_plan2, t_dist - t_gather, t_sync0 - t_dist, t_sync1 - t_sync0, wall() - t_sync1,
+                   t_merge - t_sync1, t_flush - t_merge);
     // next level: subproblems live in `nxt`; ping-pong the member buffers
     open.swap(next);
     std::swap(mem, nxt);
