@@ -453,6 +453,46 @@ __device__ __forceinline__ void warp_sort_regs(uint64_t (&k)[E], int lane) {
   }
 }
 
+// The same network with the stage loops kept rolled (only the per-register work unrolled): a fraction of the code
+// size, for kernels whose instruction fetch would otherwise thrash (hp_defer_sort_kernel: 84% "no instruction"
+// stalls with the fully unrolled E = 4/8/16 networks).
+template <int E>
+__device__ __forceinline__ void warp_sort_regs_rolled(uint64_t (&k)[E], int lane) {
+#pragma unroll 1
+  for (int kk = 2; kk <= 32 * E; kk <<= 1) {
+#pragma unroll 1
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {
+        const int js = j >> 5;  // register distance (1, 2, 4, 8)
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          // partner e ^ js, handled by the lower of the two
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            if ((1 << b) < E && js == (1 << b) && !(e & (1 << b))) {
+              const int f = e | (1 << b);
+              const bool up = ((e * 32 + lane) & kk) == 0;
+              const uint64_t a = k[e], c = k[f];
+              const bool sw = (a > c) == up;
+              k[e] = sw ? c : a;
+              k[f] = sw ? a : c;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, k[e], j);
+          const bool lower = (lane & j) == 0;
+          const bool up = ((e * 32 + lane) & kk) == 0;
+          const uint64_t mn = o < k[e] ? o : k[e], mx = o < k[e] ? k[e] : o;
+          k[e] = (lower == up) ? mn : mx;
+        }
+      }
+    }
+  }
+}
+
 // The keys streamed to owner u, addressed by a flat index: its reservoir (c keys), then for each of its
 
 // Merge of a row of c <= 32 keys (one per lane, lane < c): keep the minimum of every hash bucket (Alg. 3's
@@ -571,6 +611,88 @@ __device__ __forceinline__ uint32_t row_prefix(uint32_t c, const HpOverflow& ov,
   uint32_t pre = c;
   for (uint32_t r = ov.head[u]; r != ~0u; r = ov.rec_next[r]) pre = min(pre, ov.rec[r].y);
   return pre;
+}
+
+// Sort merge for the deferred owners with at most 32 E_MAX keys (nearly all of them): a warp per owner. Its keys (row
+// front, then the overflow records) are staged in the warp's SMEM buffer and sorted in registers (bitonic, u64
+// hash | okey | id); the first key of every hash run is the bucket minimum. When more than l_max buckets remain, the
+// run heads are rotated to (okey | id | hash), sorted again, and the l_max smallest kept — the eviction rule's end
+// state ((okey, id) is distinct per bucket: a candidate's hash is a function of the pair). Owners with
+// more keys go to `big` for the table kernel.
+template <int E>
+__device__ __forceinline__ void defer_sort_owner(const uint64_t* buf, int total, int l_max, uint64_t* res,
+                                                 uint32_t* cnt_u, int lane) {
+  uint64_t key[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) key[e] = e * 32 + lane < total ? buf[e * 32 + lane] : ~0ull;
+  warp_sort_regs_rolled<E>(key, lane);
+  bool keep[E];
+  int nh = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint64_t up = __shfl_up_sync(0xffffffffu, key[e], 1);
+    const uint64_t last = __shfl_sync(0xffffffffu, key[e > 0 ? e - 1 : 0], 31);  // element 32e - 1
+    const uint64_t prev = lane > 0 ? up : last;
+    const bool first = (e == 0 && lane == 0) || ((prev >> 48) != (key[e] >> 48));
+    keep[e] = key[e] != ~0ull && first;
+    nh += __popc(__ballot_sync(0xffffffffu, keep[e]));
+  }
+  if (nh <= l_max) {
+    int base = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t bal = __ballot_sync(0xffffffffu, keep[e]);
+      if (keep[e]) res[base + __popc(bal & ((1u << lane) - 1u))] = key[e];
+      base += __popc(bal);
+    }
+    if (lane == 0) *cnt_u = (uint32_t)base;
+    return;
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) key[e] = keep[e] ? ((key[e] << 16) | (key[e] >> 48)) : ~0ull;
+  warp_sort_regs_rolled<E>(key, lane);
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (e * 32 + lane < l_max) res[e * 32 + lane] = (key[e] >> 16) | (key[e] << 48);
+  if (lane == 0) *cnt_u = (uint32_t)l_max;
+}
+constexpr int kDeferSortMax = 512;  // keys per owner of the sort merge (E = 16)
+__global__ void __launch_bounds__(128) hp_defer_sort_kernel(int l_max, uint64_t* __restrict__ slots,
+                                                            uint32_t* __restrict__ count, HpOverflow ov,
+                                                            const uint32_t* __restrict__ list,
+                                                            const uint32_t* __restrict__ list_n,
+                                                            uint32_t* __restrict__ big, uint32_t* __restrict__ big_n) {
+  __shared__ uint64_t sbuf[4][kDeferSortMax];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint64_t* buf = sbuf[w];
+  const int64_t nl = *list_n;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nl; it += nw) {
+    const uint32_t u = list[it];
+    uint64_t* res = slots + (int64_t)u * l_max;
+    uint32_t pre = count[u], novf = 0;
+    for (uint32_t r = ov.head[u]; r != ~0u; r = ov.rec_next[r]) {
+      const uint4 rc = ov.rec[r];
+      pre = min(pre, rc.y);
+      novf += rc.w;
+    }
+    const int total = (int)(pre + novf);
+    if (total > kDeferSortMax) {
+      if (lane == 0) big[atomicAdd(big_n, 1u)] = u;
+      continue;
+    }
+    __syncwarp();
+    for (int i = lane; i < (int)pre; i += 32) buf[i] = res[i];
+    int off = (int)pre;
+    for (uint32_t r = ov.head[u]; r != ~0u; r = ov.rec_next[r]) {
+      const uint4 rc = ov.rec[r];
+      for (int t = lane; t < (int)rc.w; t += 32) buf[off + t] = ov.keys[(uint64_t)rc.z + t];
+      off += (int)rc.w;
+    }
+    __syncwarp();
+    if (total <= 128) defer_sort_owner<4>(buf, total, l_max, res, count + u, lane);
+    else defer_sort_owner<16>(buf, total, l_max, res, count + u, lane);
+  }
 }
 
 // Table merge for the deferred owners (hubs, evictions; m <= 12): one CTA per owner, a 2^m-entry SMEM table
@@ -725,8 +847,9 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
   ov.rec_next = ar.take<uint32_t>(std::max<int64_t>(1, n_inst));
   ov.rec_cap = (uint32_t)std::min<int64_t>(std::max<int64_t>(1, n_inst), 0xFFFFFFFFll);
   ov.head = ar.take<uint32_t>(std::max<int64_t>(1, n));
-  uint32_t* counters = ar.take<uint32_t>(6);  // keys_n (u64), rec_n, defer_n
+  uint32_t* counters = ar.take<uint32_t>(6);  // keys_n (u64), rec_n, defer_n, big_n
   uint32_t* defer = ar.take<uint32_t>(std::max<int64_t>(1, n));
+  uint32_t* defer_big = ar.take<uint32_t>(std::max<int64_t>(1, n));
   if (ar.measuring()) return PIPNN_OK;
   if (ar.overflow()) return fail(PIPNN_EWORKSPACE, "workspace too small (hashprune)");
   if (P >= ((int64_t)1 << 32)) return fail(PIPNN_EUNSUPPORTED, "hashprune: more than 2^32 edge keys in one wave");
@@ -764,9 +887,14 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
   hp_merge_rows_kernel<<<(unsigned)std::max<int64_t>(1, blocks), 256, 0, c.st>>>(n, l_max, slots, count, defer, defer_n);
   PIPNN_LAUNCHED("hp_merge_rows_kernel", c.st);
   if (m <= 12) {
+    // most deferred owners by the warp sort merge, the ones with more than kDeferSortMax keys by the table kernel
+    hp_defer_sort_kernel<<<(unsigned)(num_sms() * 8), 128, 0, c.st>>>(l_max, slots, count, ov, defer, defer_n,
+                                                                     defer_big, defer_n + 1);
+    PIPNN_LAUNCHED("hp_defer_sort_kernel", c.st);
     const int tsm = (int)((size_t)8 << m);
     PIPNN_CUDA(cudaFuncSetAttribute(hp_defer_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tsm));
-    hp_defer_table_kernel<<<(unsigned)(num_sms() * 6), 256, tsm, c.st>>>(m, l_max, slots, count, ov, defer, defer_n);
+    hp_defer_table_kernel<<<(unsigned)(num_sms() * 6), 256, tsm, c.st>>>(m, l_max, slots, count, ov, defer_big,
+                                                                       defer_n + 1);
     PIPNN_LAUNCHED("hp_defer_table_kernel", c.st);
   } else {
     const int cap = merge_cap(l_max);
@@ -784,7 +912,7 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
     uint32_t hc[6] = {0, 0, 0, 0, 0, 0};
     PIPNN_CUDA(cudaMemcpyAsync(hc, counters, sizeof(hc), cudaMemcpyDeviceToHost, c.st));
     PIPNN_CUDA(cudaStreamSynchronize(c.st));
-    std::fprintf(stderr, "[pipnn] hashprune: %u owners deferred, %u overflow records, %llu overflow keys\n", hc[3],
+    std::fprintf(stderr, "[pipnn] hashprune: %u owners deferred (%u to the table merge), %u overflow records, %llu overflow keys\n", hc[3], hc[4],
                  hc[2], (unsigned long long)hc[0] | ((unsigned long long)hc[1] << 32));
   }
   return PIPNN_OK;
