@@ -787,7 +787,33 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
         const unsigned long long t_out = prof ? clock64() : 0ull;
         if (prof) ++pw[3];  // items (rows) of this thread
         topk_drain<KT, KMAX>(kk, ii, qlen, my_qk, my_qc);
-        if (row < S.a.rows) {
+        bool vec_done = false;
+        if (KMAX == 8 && row < S.a.rows && K == 8 && S.ostride == 8 && args.out_col && args.out_dist && !args.out_idx &&
+            !args.out_cnt && !args.out_rowid) {
+          // the build path's leaf picks (k = 8, every slot valid): the row's 8 columns (16 B) and distances (32 B) as
+          // vector stores instead of 16 scalar stores at an 8-element stride
+          bool allv = true;
+#pragma unroll
+          for (int t = 0; t < 8; ++t) allv &= ii[t] != 0xFFFFu && ii[t] < (uint32_t)ncols;
+          if (allv) {
+            const int64_t obase = S.out_off + (int64_t)row * 8;
+            float Dv[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+              if (MIPS) Dv[t] = (float)kk[t];
+              else if (U8) Dv[t] = (float)(na_row + kk[t]);
+              else Dv[t] = fmaxf(fmaf(2.0f, (float)kk[t], (float)na_row), 0.0f);
+            }
+            *reinterpret_cast<uint4*>(args.out_col + obase) =
+                make_uint4((uint32_t)ii[0] | ((uint32_t)ii[1] << 16), (uint32_t)ii[2] | ((uint32_t)ii[3] << 16),
+                           (uint32_t)ii[4] | ((uint32_t)ii[5] << 16), (uint32_t)ii[6] | ((uint32_t)ii[7] << 16));
+            float4* dp = reinterpret_cast<float4*>(args.out_dist + obase);
+            dp[0] = make_float4(Dv[0], Dv[1], Dv[2], Dv[3]);
+            dp[1] = make_float4(Dv[4], Dv[5], Dv[6], Dv[7]);
+            vec_done = true;
+          }
+        }
+        if (row < S.a.rows && !vec_done) {
           const int64_t obase = S.out_off + (int64_t)row * S.ostride;
           const KT na = na_row;
           int o = 0;
