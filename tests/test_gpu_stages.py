@@ -99,6 +99,38 @@ def test_final_prune_u8_bit_exact(name, R, final):
     assert np.array_equal(u32(gci)[: grp[-1]], ci)
 
 
+@pytest.mark.parametrize("final", [1, 0])
+def test_final_prune_u8_large_reservoirs(final):
+    # reservoirs of 0..255 candidates (l_max 256): every u8 tier runs — warp (<= 31), band 64 / 128 / 192 and the
+    # generic kernel above 191 — against the oracle's prune of the same reservoirs (Alg. 2 lazy form)
+    cfg = synth.C2.scaled(4000)
+    X = synth.gen_points(cfg)
+    n = len(X)
+    rng = np.random.default_rng(11)
+    own, cand = [], []
+    for u in range(n):
+        c = int(rng.integers(0, 420)) if u % 3 == 0 else int(rng.integers(0, 40))
+        v = rng.choice(n - 1, size=c, replace=False)
+        v = v + (v >= u)  # no self loops
+        own.append(np.full(c, u, np.uint32))
+        cand.append(v.astype(np.uint32))
+    own, cand = np.concatenate(own), np.concatenate(cand)
+    xi = X.astype(np.int64)
+    dist = ((xi[own] - xi[cand]) ** 2).sum(1).astype(np.float64)  # exact for uint8 (< 2^24)
+    S = O.sketch(O.Dataset(X), O.hyperplanes(16, cfg.d, cfg.seed))  # m = 16: few bucket collisions, big reservoirs
+    slots, count, ok = O.hashprune(n, S, 256, own, cand, dist)
+    assert ok
+    for lo, hi in ((32, 63), (64, 127), (128, 191), (192, 256)):
+        assert ((count >= lo) & (count <= hi)).sum() > 20, (lo, hi)  # every tier is populated
+    rp, ci, ok2 = O.final_prune(O.Dataset(X), slots, count, 48, (6, 5), final)
+    assert ok2
+    grp, gci = P().pipnn_final_prune(cuda(X), cuda(slots.view(np.int64)), cuda(count.view(np.int32)), R=48,
+                                     final_prune=final)
+    grp = grp.cpu().numpy()
+    assert np.array_equal(grp, rp)
+    assert np.array_equal(u32(gci)[: grp[-1]], ci)
+
+
 @pytest.mark.parametrize("name", ["C1", "C3", "C4"])
 def test_final_prune_float_close(name):
     cfg = synth.CONFIGS[name].scaled(6000) if synth.CONFIGS[name].n != 6000 else synth.CONFIGS[name]
