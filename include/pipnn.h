@@ -195,8 +195,9 @@ PIPNN_API pipnn_status pipnn_build(const pipnn_points* X, const pipnn_build_para
  *     (D, id) order; dist [n_instances*k] f32: their D (n_leaves, n_instances from pipnn_stats);
  *   sketch [n*m] (int32 for uint8, float32 otherwise); slots [n*l_max] u64 / count [n] u32: the HashPrune
  *     reservoirs before the final prune, slot layout above; inside pipnn_build a reservoir is a set (the
- *     final prune re-sorts it): its first count[u] slots are in hash order except for owners merged through
- *     a sized hash table (more keys than one warp merges), and slots at or beyond count[u] are unspecified.
+ *     final prune re-sorts it): its first count[u] slots are in hash order, except for owners whose merge
+ *     evicted (more buckets than l_max: (dist, id) order) or went through the hash-table kernel (more than 512
+ *     streamed keys), and slots at or beyond count[u] are unspecified.
  * Host-only: nothing is launched. */
 typedef struct {
   int64_t* leaf_off;
@@ -209,6 +210,11 @@ typedef struct {
 } pipnn_build_buffers;
 PIPNN_API pipnn_status pipnn_debug_build_buffers(const pipnn_points* X, const pipnn_build_params* p, void* ws,
                                                  size_t ws_bytes, pipnn_build_buffers* out_h);
+
+/* Experiment hook (tools/leaf_exp.py): copies out and clears the distance kernel's wait profile —
+ * 16 u64 counters of clock64 cycles summed over the grid, filled only when the process runs with
+ * PIPNN_DEBUG_EPI bit 64 set — into out16 (HOST, 16 elements). Returns 0 on success, 1 on a CUDA error. */
+PIPNN_API int pipnn_debug_dt_prof(unsigned long long* out16);
 
 /* Batched greedy beam search over a built graph (Alg. 1 BeamSearch), the
  * query side of the k-NN-graph / ANN tasks. Per query: beam of the L best (D, id) seen, start
