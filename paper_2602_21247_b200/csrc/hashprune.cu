@@ -657,37 +657,45 @@ __device__ __forceinline__ void defer_sort_owner(const uint64_t* buf, int total,
   if (lane == 0) *cnt_u = (uint32_t)l_max;
 }
 constexpr int kDeferSortMax = 512;  // keys per owner of the sort merge (E = 16)
+constexpr int kDeferRecs = 64;      // overflow records per owner of the sort merge
 __global__ void __launch_bounds__(128) hp_defer_sort_kernel(int l_max, uint64_t* __restrict__ slots,
                                                             uint32_t* __restrict__ count, HpOverflow ov,
                                                             const uint32_t* __restrict__ list,
                                                             const uint32_t* __restrict__ list_n,
                                                             uint32_t* __restrict__ big, uint32_t* __restrict__ big_n) {
   __shared__ uint64_t sbuf[4][kDeferSortMax];
+  __shared__ uint2 srec[4][kDeferRecs];  // the owner's overflow records (key offset, key count), in list order
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint64_t* buf = sbuf[w];
+  uint2* recs = srec[w];
   const int64_t nl = *list_n;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t it = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < nl; it += nw) {
     const uint32_t u = list[it];
     uint64_t* res = slots + (int64_t)u * l_max;
+    // one walk of the record list (a dependent chain: overlap-heavy builds link ~20 records per owner), the
+    // records kept in SMEM so that their keys then load in parallel
     uint32_t pre = count[u], novf = 0;
+    int nrec = 0;
     for (uint32_t r = ov.head[u]; r != ~0u; r = ov.rec_next[r]) {
       const uint4 rc = ov.rec[r];
       pre = min(pre, rc.y);
       novf += rc.w;
+      if (lane == 0 && nrec < kDeferRecs) recs[nrec] = make_uint2(rc.z, rc.w);
+      ++nrec;
     }
     const int total = (int)(pre + novf);
-    if (total > kDeferSortMax) {
+    if (total > kDeferSortMax || nrec > kDeferRecs) {
       if (lane == 0) big[atomicAdd(big_n, 1u)] = u;
       continue;
     }
     __syncwarp();
     for (int i = lane; i < (int)pre; i += 32) buf[i] = res[i];
     int off = (int)pre;
-    for (uint32_t r = ov.head[u]; r != ~0u; r = ov.rec_next[r]) {
-      const uint4 rc = ov.rec[r];
-      for (int t = lane; t < (int)rc.w; t += 32) buf[off + t] = ov.keys[(uint64_t)rc.z + t];
-      off += (int)rc.w;
+    for (int q = 0; q < nrec; ++q) {
+      const uint2 rc = recs[q];
+      for (int t = lane; t < (int)rc.y; t += 32) buf[off + t] = ov.keys[(uint64_t)rc.x + t];
+      off += (int)rc.y;
     }
     __syncwarp();
     if (total <= 128) defer_sort_owner<4>(buf, total, l_max, res, count + u, lane);
