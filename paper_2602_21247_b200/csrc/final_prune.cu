@@ -1389,6 +1389,22 @@ __global__ void csr_copy_kernel(int64_t n, int R, const uint32_t* __restrict__ n
     const int64_t ul = u0 + lane;
     const uint32_t dgl = ul < n ? deg[ul] : 0u;
     const uint64_t ol = ul < n ? row_ptr[ul] : 0ull;
+    if (R <= 32) {
+      // one entry per lane and row: all 32 rows' loads in flight, then the 32 stores
+      uint32_t v[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const uint32_t dq = __shfl_sync(0xffffffffu, dgl, q);
+        v[q] = (uint32_t)lane < dq ? nbr_tmp[(u0 + q) * (int64_t)R + lane] : 0u;
+      }
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const uint32_t dq = __shfl_sync(0xffffffffu, dgl, q);
+        const uint64_t oq = __shfl_sync(0xffffffffu, ol, q);
+        if ((uint32_t)lane < dq) col_idx[oq + lane] = v[q];
+      }
+      continue;
+    }
     for (int j0 = 0; j0 < 32; j0 += 4) {
       uint32_t v[4][2];
       uint32_t dgs[4];
