@@ -74,6 +74,15 @@ __global__ void __launch_bounds__(128) gather_tiled_kernel(const void* __restric
   bool bad = false;
   const bool vec = SRC == 4 ? true : (U8 ? ((d & 15) == 0 && (ld & 15) == 0) : ((d & 3) == 0 && (ld & 3) == 0));
   const float* qs = SRC == 4 ? qstats + (int64_t)w.seg * (d + 1) : nullptr;  // centre [d], inverse scale
+  // uint8 rows of <= 128 B: every chunk of the row loaded before any is processed (8 loads in flight per lane)
+  uint4 pre[8];
+  const bool batch = (SRC == 0 || SRC == 3) && vec && ncc <= 8;
+  if (batch) {
+#pragma unroll
+    for (int kc = 0; kc < 8; ++kc)
+      pre[kc] = (valid && kc < ncc && kc * 16 < d) ? __ldg((const uint4*)((const uint8_t*)Xv + id * ld) + kc)
+                                                   : make_uint4(0u, 0u, 0u, 0u);
+  }
 #pragma unroll 4
   for (int kc = 0; kc < ncc; ++kc) {
     uint4 out = make_uint4(0u, 0u, 0u, 0u);
@@ -118,7 +127,11 @@ __global__ void __launch_bounds__(128) gather_tiled_kernel(const void* __restric
         out = make_uint4(out.x ^ xm[0], out.y ^ xm[1], out.z ^ xm[2], out.w ^ xm[3]);
       } else if (U8) {
         const uint8_t* src = (const uint8_t*)Xv + id * ld;
-        if (vec) {
+        if (batch) {
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if (t == kc) out = pre[t];
+        } else if (vec) {
           if (kc * 16 < d) out = __ldg((const uint4*)src + kc);
         } else {
           uint32_t wv[4] = {0u, 0u, 0u, 0u};
