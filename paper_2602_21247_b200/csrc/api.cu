@@ -399,7 +399,8 @@ static pipnn_status build_impl(const pipnn_points* X, const pipnn_build_params* 
   // prune), so the n*l_max arena is not initialised here (it is internal to pipnn_build).
   if (!ar.measuring()) PIPNN_CUDA(kmemset(count, 0, (size_t)X->n * sizeof(uint32_t), st));
   s = hashprune_from_leaves(p->hp.m, p->hp.l_max, X->n, sketch, sk_int, slots, count, leaf_off, n_leaves, leaf_ids,
-                            n_inst, k, cols, dist, max_leaf_h, n_edges_dev, ar, c);
+                            n_inst, k, cols, dist, max_leaf_h, n_edges_dev, ar, c,
+                            (int)std::min<int64_t>(1 << 20, bp.leaf_ids_cap / std::max<int64_t>(1, X->n)));
   if (s != PIPNN_OK) { cleanup(); return s; }
   ar.release(mark);
   if (!ar.measuring()) cudaEventRecord(ev[4], st);

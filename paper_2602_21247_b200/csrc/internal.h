@@ -70,7 +70,8 @@ pipnn_status hashprune_impl(int m, int l_max, int64_t n, const void* sketch, boo
 pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sketch, bool sk_int, uint64_t* slots,
                                    uint32_t* count, const int64_t* leaf_off, int64_t n_leaves, const uint32_t* leaf_ids,
                                    int64_t n_inst, int k, const uint16_t* cols, const float* dist, int max_leaf,
-                                   int64_t* n_edges_dev, Arena& ar, const Ctx& c);
+                                   int64_t* n_edges_dev, Arena& ar, const Ctx& c,
+                                   int inst_per_point);  // leaf instances per point (capacity / n): path choice
 
 // order/order_n (device, nullable): the points to prune, in this order (pipnn_build: leaf order, see
 // leaf_order); without it every point in id order.
