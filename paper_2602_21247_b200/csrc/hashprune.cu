@@ -1592,7 +1592,11 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
                                    int64_t* n_edges_dev, Arena& ar, const Ctx& c, int inst_per_point) {
   // more than 4 leaf instances per point (wide overlap, e.g. fanout [10, 3]: 30): the instance-major path
   // (fanout [10, 3] at 1M points: HashPrune 25.6 vs 44 ms owner-major); C5 (2 per point): owner-major (56 vs 74 ms)
-  if (inst_per_point > 4)
+  static const int im_min = [] {  // experiment hook (read once): instances per point from which im is used
+    const char* e = std::getenv("PIPNN_HP_IM_MIN");
+    return e ? std::atoi(e) : 5;
+  }();
+  if (inst_per_point >= im_min)
     return im::from_leaves(m, l_max, n, sketch, sk_int, slots, count, leaf_off, n_leaves, leaf_ids, n_inst, k, cols,
                            dist, max_leaf, n_edges_dev, ar, c);
   // overflow capacity: every key of the wave (at most 2 k per instance) — never exceeded
