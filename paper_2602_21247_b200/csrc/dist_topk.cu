@@ -3,14 +3,17 @@
 #include <cstdlib>
 
 #include "dist_topk.cuh"
+#include "dist_topk_uf2.cuh"
 
 namespace pipnn {
 
 // Experiment hooks, read once per process (environment): PIPNN_DEBUG_EPI (epilogue skips / wait profile),
-// PIPNN_P1 / PIPNN_P1_PART (threshold-pass tiles), PIPNN_GEOM ("NA,planes per chunk").
+// PIPNN_P1 / PIPNN_P1_PART (threshold-pass tiles), PIPNN_GEOM ("NA,planes per chunk"), PIPNN_UF2=0 (folded uint8
+// leaves on dist_topk_kernel instead of the four-warpgroup dist_topk_uf2_kernel).
 struct DtKnobs {
-  int dbg = 0, p1 = 0, p1_part = 0, geo = 0;
+  int dbg = 0, p1 = 0, p1_part = 0, geo = 0, uf2 = 1;
   DtKnobs() {
+    if (const char* e = std::getenv("PIPNN_UF2")) uf2 = std::atoi(e);
     if (const char* e = std::getenv("PIPNN_DEBUG_EPI")) dbg = std::atoi(e);
     if (const char* e = std::getenv("PIPNN_P1")) p1 = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("PIPNN_P1_PART")) p1_part = std::max(1, std::atoi(e));
@@ -43,6 +46,15 @@ static pipnn_status launch_one(const DistTopkArgs& a0, cudaStream_t st) {
   if (a.packed && !(KMAX == 2 && U8)) return fail(PIPNN_EUNSUPPORTED, "dist_topk: packed pass needs uint8, K <= 2");
   if (a.packed) a.p1cap = 0;  // no threshold pass
   if (UF != (a.uf_aug > 0)) return fail(PIPNN_EUNSUPPORTED, "dist_topk: folded layout mismatch");
+  if (UF && KMAX == 8 && kn.uf2 && !kn.dbg && !a.packed && a.work && uf2_fits(a.Kb, a.uf_aug)) {
+    // folded uint8 leaves, k <= 8: two row blocks per item on four epilogue warpgroups (dist_topk_uf2.cuh)
+    const Uf2Geom g2 = uf2_geom(a.Kb, a.uf_aug);
+    auto* fn2 = dist_topk_uf2_kernel<8>;
+    PIPNN_CUDA(cudaFuncSetAttribute(fn2, cudaFuncAttributeMaxDynamicSharedMemorySize, g2.smem));
+    fn2<<<num_sms(), kUf2Threads, g2.smem, st>>>(a);
+    PIPNN_LAUNCHED("dist_topk_uf2_kernel", st);
+    return PIPNN_OK;
+  }
   const DtGeom g = dt_geom(a.Kb, !U8 ? 2 : a.uf_aug, a.geo);
   if (g.stages < 2) return fail(PIPNN_EUNSUPPORTED, "dist_topk: row too long for the SMEM pipeline");
   auto* fn = dist_topk_kernel<U8, MIPS, KMAX, UF>;
