@@ -48,6 +48,9 @@ static pipnn_status launch_one(const DistTopkArgs& a0, cudaStream_t st) {
   if (UF != (a.uf_aug > 0)) return fail(PIPNN_EUNSUPPORTED, "dist_topk: folded layout mismatch");
   if (UF && KMAX == 8 && kn.uf2 && !kn.dbg && !a.packed && a.work && uf2_fits(a.Kb, a.uf_aug)) {
     // folded uint8 leaves, k <= 8: two row blocks per item on four epilogue warpgroups (dist_topk_uf2.cuh)
+    // threshold pass over 3 tiles (C5 leaf tiles 60.5 ms vs 61.9 at 6, 60.7 at 4: with direct insertion the pass-2
+    // threshold tightens as the list fills, so a looser first bound costs less than in dist_topk_kernel)
+    if (!kn.p1) a.p1cap = 3;
     const Uf2Geom g2 = uf2_geom(a.Kb, a.uf_aug);
     auto* fn2 = dist_topk_uf2_kernel<8>;
     PIPNN_CUDA(cudaFuncSetAttribute(fn2, cudaFuncAttributeMaxDynamicSharedMemorySize, g2.smem));
