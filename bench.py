@@ -615,7 +615,10 @@ def main():
             "config": {**workload_desc(cfg), "parallelism": f"replicas x{ws} (independent builds)",
                        "l2": "flushed between timed steps (512 MB write)",
                        "leaf_pick": "int8-quantised + exact re-rank (NEXT-2)" if args.quant else "exact"},
-            "roofline": {"bound": "tensor", "kernel": "dist_topk_kernel (leaf distance tiles + fused pick)",
+            "roofline": {"bound": "tensor",
+                         "kernel": ("dist_topk_uf2_kernel<8> (folded uint8 leaf tiles + fused pick, four epilogue "
+                                    "warpgroups)" if cfg.dtype == "u8" and cfg.metric == "l2" and cfg.k <= 8
+                                    and not args.quant else "dist_topk_kernel (leaf distance tiles + fused pick)"),
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s" if cfg.dtype != "u8" else "TOP/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_note,
                          "algorithmic_ops_per_launch": leaf_ops, "ms_per_launch": tile_ms,
