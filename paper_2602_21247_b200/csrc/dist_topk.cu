@@ -8,10 +8,10 @@
 namespace pipnn {
 
 // Experiment hooks, read once per process (environment): PIPNN_DEBUG_EPI (epilogue skips / wait profile),
-// PIPNN_P1 / PIPNN_P1_PART (threshold-pass tiles), PIPNN_GEOM ("NA,planes per chunk"), PIPNN_UF2=0 (folded uint8
-// leaves on dist_topk_kernel instead of the four-warpgroup dist_topk_uf2_kernel).
+// PIPNN_P1 / PIPNN_P1_PART (threshold-pass tiles), PIPNN_GEOM ("NA,planes per chunk"), PIPNN_UF2 (bit 0: folded
+// uint8 leaves, bit 1: the partition's packed pass on the four-warpgroup dist_topk_uf2_kernel; default 3).
 struct DtKnobs {
-  int dbg = 0, p1 = 0, p1_part = 0, geo = 0, uf2 = 1;
+  int dbg = 0, p1 = 0, p1_part = 0, geo = 0, uf2 = 3;
   DtKnobs() {
     if (const char* e = std::getenv("PIPNN_UF2")) uf2 = std::atoi(e);
     if (const char* e = std::getenv("PIPNN_DEBUG_EPI")) dbg = std::atoi(e);
@@ -46,13 +46,24 @@ static pipnn_status launch_one(const DistTopkArgs& a0, cudaStream_t st) {
   if (a.packed && !(KMAX == 2 && U8)) return fail(PIPNN_EUNSUPPORTED, "dist_topk: packed pass needs uint8, K <= 2");
   if (a.packed) a.p1cap = 0;  // no threshold pass
   if (UF != (a.uf_aug > 0)) return fail(PIPNN_EUNSUPPORTED, "dist_topk: folded layout mismatch");
-  if (UF && KMAX == 8 && kn.uf2 && !kn.dbg && !a.packed && a.work && uf2_fits(a.Kb, a.uf_aug)) {
+  if (UF && KMAX == 8 && (kn.uf2 & 1) && !kn.dbg && !a.packed && a.work && uf2_fits(a.Kb, a.uf_aug)) {
     // folded uint8 leaves, k <= 8: two row blocks per item on four epilogue warpgroups (dist_topk_uf2.cuh)
     // threshold pass over 3 tiles (C5 leaf tiles 60.5 ms vs 61.9 at 6, 60.7 at 4: with direct insertion the pass-2
     // threshold tightens as the list fills, so a looser first bound costs less than in dist_topk_kernel)
     if (!kn.p1) a.p1cap = 3;
     const Uf2Geom g2 = uf2_geom(a.Kb, a.uf_aug);
     auto* fn2 = dist_topk_uf2_kernel<8>;
+    PIPNN_CUDA(cudaFuncSetAttribute(fn2, cudaFuncAttributeMaxDynamicSharedMemorySize, g2.smem));
+    fn2<<<num_sms(), kUf2Threads, g2.smem, st>>>(a);
+    PIPNN_LAUNCHED("dist_topk_uf2_kernel", st);
+    return PIPNN_OK;
+  }
+  if (a.pairs != (U8 && !UF && !MIPS && KMAX == 2 && a.packed && dt_packed_pairs(a.Kb) ? 1 : 0))
+    return fail(PIPNN_EINVAL, "dist_topk: pair items without the packed uf2 pass (or the reverse)");
+  if (a.pairs) {
+    // the partition's packed top-2 pass on the same four-warpgroup kernel
+    const Uf2Geom g2 = uf2_geom(a.Kb, 0);
+    auto* fn2 = dist_topk_uf2_kernel<2, true>;
     PIPNN_CUDA(cudaFuncSetAttribute(fn2, cudaFuncAttributeMaxDynamicSharedMemorySize, g2.smem));
     fn2<<<num_sms(), kUf2Threads, g2.smem, st>>>(a);
     PIPNN_LAUNCHED("dist_topk_uf2_kernel", st);
@@ -84,6 +95,8 @@ static pipnn_status launch_k(const DistTopkArgs& a, int kmax, cudaStream_t st) {
   if (kmax <= 12) return launch_one<U8, MIPS, 12>(a, st);
   return launch_one<U8, MIPS, 16>(a, st);
 }
+
+bool dt_packed_pairs(int Kb) { return (knobs().uf2 & 2) && !knobs().dbg && uf2_fits(Kb, 0, true); }
 
 // kmax: the largest k any segment asks for (self exclusion does not need an extra slot).
 pipnn_status launch_dist_topk(const DistTopkArgs& a, bool u8, bool mips, int kmax, cudaStream_t st) {

@@ -91,6 +91,8 @@ struct DistTopkArgs {
   // device counter (zeroed before the launch) and hands it to its MMA warp and epilogue warpgroup through an
   // SMEM ring; nullptr: the static round-robin order (item = CTA + (2 j + pipeline) * grid)
   unsigned long long* work;
+  // dist_topk_uf2_kernel only: 1 = items are pair heads (blocks rb, rb + 1), scheduled statically (work == nullptr)
+  int pairs;
 };
 
 constexpr int kDtItemRing = 8;  // claimed items in flight per pipeline (dynamic scheduling)
@@ -869,5 +871,8 @@ __global__ void __launch_bounds__(kDtThreads, 1) dist_topk_kernel(const DistTopk
 
 // Host launcher (dist_topk.cu): picks the instantiation for (dtype, metric, K).
 pipnn_status launch_dist_topk(const DistTopkArgs& a, bool u8, bool mips, int kmax, cudaStream_t st);
+// Whether the packed partition pass (uint8, K <= 2) runs on dist_topk_uf2_kernel, which then takes pair items
+// (DistTopkArgs::pairs = 1) instead of block items.
+bool dt_packed_pairs(int Kb);
 
 }  // namespace pipnn

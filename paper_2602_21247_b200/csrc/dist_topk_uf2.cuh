@@ -18,6 +18,9 @@
 //     threshold tightens with every insertion.
 // The picks are identical to dist_topk_kernel<U8=1, MIPS=0, KMAX, UF=1>: columns arrive in ascending order, the
 // insertion is strict, so equal keys keep the smaller column (= smaller id inside a leaf).
+// PK = the partition's packed single pass instead (uint8 rows against a group's leaders, K <= 2, no threshold pass,
+// plain u8 x u8 MMA; the packed leader norms 32 ||l||^2 + (position mod 32) order a chunk by (key, column) — the
+// packedm branch of dist_topk_kernel), identical to dist_topk_kernel<1, 0, 2, 0> with packed = 1.
 #pragma once
 #include "dist_topk.cuh"
 
@@ -43,13 +46,14 @@ __host__ __device__ inline Uf2Geom uf2_geom(int Kb, int augp) {
   g.smem = fixed + 2 * g.NS * g.stage_bytes;
   return g;
 }
-// The kernel applies when both pipelines get >= 2 stages (d <= 128 at 4 augment planes) and augp <= 8.
-__host__ __device__ inline bool uf2_fits(int Kb, int augp) {
+// The kernel applies when both pipelines get >= 2 stages (folded rows: d <= 128 at 4 augment planes) and augp <= 8
+// (folded rows) or augp == 0 (packed partition pass).
+__host__ __device__ inline bool uf2_fits(int Kb, int augp, bool packed = false) {
   const Uf2Geom g = uf2_geom(Kb, augp);
-  return augp > 0 && augp <= 8 && (g.KCs & 1) == 0 && g.NS >= 2;
+  return (packed ? augp == 0 : (augp > 0 && augp <= 8)) && (g.KCs & 1) == 0 && g.NS >= 2;
 }
 
-template <int KMAX>
+template <int KMAX, bool PK = false>
 __global__ void __launch_bounds__(kUf2Threads, 1) dist_topk_uf2_kernel(const DistTopkArgs args) {
   using KT = int32_t;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -105,7 +109,12 @@ __global__ void __launch_bounds__(kUf2Threads, 1) dist_topk_uf2_kernel(const Dis
   // Item sequence of pipeline p (dynamic): the producer claims block items from the shared counter, skips the
   // odd blocks (each is the second block of its even predecessor's pair) and hands the pair to its MMA warp and
   // epilogue warpgroups through an SMEM ring; -1 ends the sequence.
+  const bool dyn = args.work != nullptr;  // else: static round-robin over pair items (args.pairs)
   auto claim_item = [&](int p, uint32_t j) -> int64_t {  // producer (one lane)
+    if (!dyn) {
+      const int64_t it = (int64_t)blockIdx.x + (2 * (int64_t)j + p) * gridDim.x;
+      return it < n_items ? it : -1;
+    }
     const int e = (int)(j % kDtItemRing);
     if (!ptx::mbar_wait_hint(&bar_it_empty[p][e], ((j / kDtItemRing) & 1) ^ 1u, args.err, DERR_WAIT_TIMEOUT, 1000000u))
       return -1;
@@ -119,6 +128,10 @@ __global__ void __launch_bounds__(kUf2Threads, 1) dist_topk_uf2_kernel(const Dis
     return it < n_items ? it : -1;
   };
   auto take_item = [&](int p, uint32_t j, bool arrive) -> int64_t {  // MMA warp / epilogue warps
+    if (!dyn) {
+      const int64_t it = (int64_t)blockIdx.x + (2 * (int64_t)j + p) * gridDim.x;
+      return it < n_items ? it : -1;
+    }
     const int e = (int)(j % kDtItemRing);
     if (!ptx::mbar_wait(&bar_it_full[p][e], (j / kDtItemRing) & 1, args.err, DERR_WAIT_TIMEOUT)) return -1;
     const int64_t it = *(volatile int64_t*)&item_ring[p][e];
@@ -187,7 +200,8 @@ __global__ void __launch_bounds__(kUf2Threads, 1) dist_topk_uf2_kernel(const Dis
         for (int t = 0; t < p1 + T; ++t, ++sg) {
           const int c0 = (t < p1 ? t : t - p1) * kDtTileN;
           const int Nt = min(kDtTileN, (ncols - c0 + 31) & ~31);
-          const uint32_t idesc = ptx::idesc_u8_s32(128, Nt) | (1u << 7) | (1u << 10);  // A and B signed (s8)
+          // folded rows: A and B signed (s8); packed partition pass: u8 x u8
+          const uint32_t idesc = PK ? ptx::idesc_u8_s32(128, Nt) : (ptx::idesc_u8_s32(128, Nt) | (1u << 7) | (1u << 10));
           const int s = sg % NS;
           if (!ptx::mbar_wait_hint(&bar_full[p][s], (sg / NS) & 1, args.err, DERR_WAIT_TIMEOUT, 1000000u)) return;
           ptx::tc_fence_after();
@@ -267,7 +281,44 @@ __global__ void __launch_bounds__(kUf2Threads, 1) dist_topk_uf2_kernel(const Dis
           U = vk[VK - 1];
           U = U == kInf ? (KT)(1 << 30) : U;  // fewer than K1 groups: everything passes
         }
-        if (!pass2) {
+        if (PK) {
+          // packed single pass (K <= 2): q_j = 32 key_j + (j mod 32) = nbp_j - 64 v_j (one IMAD) orders the chunk's
+          // columns by (key, column) exactly; its two smallest by a min/max network on column pairs, inserted
+          for (int j0 = 0; j0 < Nt; j0 += 32) {
+            const int col0 = c0 + j0;
+            int4 nb4[8];
+            const int4* p4 = reinterpret_cast<const int4*>((const int32_t*)args.nb + S.b.pos + col0);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) nb4[u] = __ldg(p4 + u);
+            uint32_t v[32];
+            ptx::tmem_ld32(tacc + j0, v);
+            ptx::tmem_ld_wait();
+            int32_t qv[32];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              qv[4 * u + 0] = nb4[u].x - 64 * (int32_t)v[4 * u + 0];
+              qv[4 * u + 1] = nb4[u].y - 64 * (int32_t)v[4 * u + 1];
+              qv[4 * u + 2] = nb4[u].z - 64 * (int32_t)v[4 * u + 2];
+              qv[4 * u + 3] = nb4[u].w - 64 * (int32_t)v[4 * u + 3];
+            }
+            int32_t m1 = 0x7FFFFFFF, m2 = 0x7FFFFFFF;
+            if (K == 1) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 2) m1 = min(m1, min(qv[j], qv[j + 1]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; j += 2) {
+                const int32_t lo = min(qv[j], qv[j + 1]), hi = max(qv[j], qv[j + 1]);
+                const int32_t t = max(m1, lo);
+                m1 = min(m1, lo);
+                m2 = __vimin3_s32(t, m2, hi);
+              }
+            }
+            const int32_t k1 = m1 >> 5, k2 = m2 >> 5;
+            if (k1 < kk[KMAX - 1]) topk_insert<KT, KMAX>(kk, ii, (KT)k1, (uint32_t)(col0 + (m1 & 31)));
+            if (K == 2 && k2 < kk[KMAX - 1]) topk_insert<KT, KMAX>(kk, ii, (KT)k2, (uint32_t)(col0 + (m2 & 31)));
+          }
+        } else if (!pass2) {
           // maxima of acc over groups of 16 columns, negated into the value list; padding columns never win
           for (int j0 = 0; j0 < Nt; j0 += 32) {
             const int valid = min(32, ncols - (c0 + j0));

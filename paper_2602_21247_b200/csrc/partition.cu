@@ -117,12 +117,17 @@ __global__ void iota_kernel(uint32_t* __restrict__ out, int64_t n) {
 // The level's work items (one per 128-row block of every group's members, resp. leaders): CTA g writes
 // its group's items at its offsets (host prefix sums over the groups; the item lists themselves never pass the host).
 __global__ void level_items_kernel(const int64_t* __restrict__ offA, const int64_t* __restrict__ offB, int G,
-                                   WorkItem* __restrict__ itA, WorkItem* __restrict__ itB) {
+                                   WorkItem* __restrict__ itA, WorkItem* __restrict__ itB,
+                                   const int64_t* __restrict__ offP, WorkItem* __restrict__ itP) {
   const int g = blockIdx.x;
   if (g >= G) return;
   const int64_t a0 = offA[g], a1 = offA[g + 1], b0 = offB[g], b1 = offB[g + 1];
   for (int64_t i = a0 + threadIdx.x; i < a1; i += blockDim.x) itA[i] = WorkItem{g, (int32_t)(i - a0)};
   for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) itB[i] = WorkItem{g, (int32_t)(i - b0)};
+  if (itP) {  // pair items (blocks 2i, 2i + 1) for dist_topk_uf2_kernel's static schedule
+    const int64_t p0 = offP[g], p1 = offP[g + 1];
+    for (int64_t i = p0 + threadIdx.x; i < p1; i += blockDim.x) itP[i] = WorkItem{g, (int32_t)(2 * (i - p0))};
+  }
 }
 
 // Leaders of every group (Alg. 5 line 3, R12): the l_g candidates of smallest priority, then by id. One
@@ -580,6 +585,9 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
   int64_t* dev_leaf_dst = ar.take<int64_t>(cp.leaves);
   uint8_t* dev_groups = ar.take<uint8_t>((size_t)cp.G * subtree_group_bytes());
   unsigned long long* dev_ctr = ar.take<unsigned long long>(4);  // [0] leaves, [1] staging cursor
+  int64_t* d_poff = ar.take<int64_t>(cp.G + 1);                   // pair-item offsets per group (packed pass)
+  WorkItem* itP = ar.take<WorkItem>(cp.rowsA / 256 + cp.G + 1);    // pair items (packed pass on dist_topk_uf2)
+  int64_t* n_pairs = ar.take<int64_t>(1);
   int* dev_work = ar.take<int>(2);                                 // [0] group counter, [1] max depth
   PGroup* d_groups = ar.take<PGroup>(cp.G);
   int64_t* d_cbase = ar.take<int64_t>(cp.G);
@@ -810,13 +818,16 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
     std::vector<TileSeg> hA(G), hB(G);
     std::vector<DistSeg> hD(G);
     std::vector<int64_t> hOffA(G + 1), hOffB(G + 1);  // item offsets: one item per 128-row block
-    int64_t posA = 0, posB = 0;
+    std::vector<int64_t> hOffP(G + 1);                 // pair-item offsets: one per two 128-row blocks
+    int64_t posA = 0, posB = 0, nP = 0;
     for (int g = 0; g < G; ++g) {
       const PGroup& q = hg[g];
       TileSeg a{q.off, posA, (int32_t)round_up(q.size, 128), (int32_t)q.size};
       TileSeg b{q.lead_off, posB, (int32_t)round_up(q.l, 128), q.l};
       hOffA[g] = posA / 128;
       hOffB[g] = posB / 128;
+      hOffP[g] = nP;
+      nP += (a.pad / 128 + 1) / 2;
       posA += a.pad;
       posB += b.pad;
       hA[g] = a;
@@ -835,6 +846,7 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
     const int64_t nItA = posA / 128, nItB = posB / 128;
     hOffA[G] = nItA;
     hOffB[G] = nItB;
+    hOffP[G] = nP;
     const int64_t nits[2] = {nItA, nItB};
     PIPNN_CUDA(g_pin_level.copy(tsA, hA.data(), G * sizeof(TileSeg), st));
     PIPNN_CUDA(g_pin_level.copy(tsB, hB.data(), G * sizeof(TileSeg), st));
@@ -843,13 +855,20 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
     PIPNN_CUDA(g_pin_level.copy(d_itoff + (G + 1), hOffB.data(), (G + 1) * sizeof(int64_t), st));
     PIPNN_CUDA(g_pin_level.copy(n_it, nits, 2 * sizeof(int64_t), st));
     PIPNN_CUDA(g_pin_level.flush(st));
-    level_items_kernel<<<G, 256, 0, st>>>(d_itoff, d_itoff + (G + 1), G, itA, itB);
-    PIPNN_LAUNCHED("level_items_kernel", st);
-    const double t_plan2 = dbg_timing ? wall() : 0.0;
-    PIPNN_TRY(gather_tiled(X, mem, tsA, itA, n_it, nItA, TA, nA, c));
     // uint8 with fanout <= 2 at this level: leader norms in the packed form of the single-pass top-2
     static const bool no_packed = std::getenv("PIPNN_NO_PACKED") != nullptr;  // experiment hook
     const int packed = X->dtype == PIPNN_U8 && fmax_l <= 2 && !no_packed ? 1 : 0;
+    const bool pairs = packed && dt_packed_pairs(Kb);  // the packed pass runs on dist_topk_uf2_kernel (pair items)
+    if (pairs) {
+      PIPNN_CUDA(g_pin_level.copy(d_poff, hOffP.data(), (G + 1) * sizeof(int64_t), st));
+      PIPNN_CUDA(g_pin_level.copy(n_pairs, &nP, sizeof(int64_t), st));
+      PIPNN_CUDA(g_pin_level.flush(st));
+    }
+    level_items_kernel<<<G, 256, 0, st>>>(d_itoff, d_itoff + (G + 1), G, itA, itB, pairs ? d_poff : nullptr,
+                                          pairs ? itP : nullptr);
+    PIPNN_LAUNCHED("level_items_kernel", st);
+    const double t_plan2 = dbg_timing ? wall() : 0.0;
+    PIPNN_TRY(gather_tiled(X, mem, tsA, itA, n_it, nItA, TA, nA, c));
     PIPNN_TRY(gather_tiled(X, lead_sorted, tsB, itB, n_it + 1, nItB, TB, nB, c, 0, packed));
     const double t_gather = dbg_timing ? wall() : 0.0;
     PIPNN_CUDA(kmemset(ccnt, 0, C * sizeof(uint32_t), st));
@@ -870,6 +889,13 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
     da.out_cnt = ccnt;
     da.packed = packed;
     da.err = c.err;
+    if (pairs) {
+      // dist_topk_uf2_kernel over the pair items, static round-robin schedule (a device claim per item measured
+      // slower here: the packed epilogue is light, so the claim latency is exposed)
+      da.items = itP;
+      da.n_items = n_pairs;
+      da.pairs = 1;
+    }
     PIPNN_TRY(launch_dist_topk(da, X->dtype == PIPNN_U8, X->metric == PIPNN_MIPS, fmax_l, st));
     const double t_dist = dbg_timing ? wall() : 0.0;
     // ---- 3. group-by: stable radix sort of the (child, id) pairs, in member order -> every child ascending
