@@ -10,10 +10,10 @@ timeout 300 python bench.py --config C2 --shard --steps 3 --warmup 2 > gpurun_ou
 timeout 300 python bench.py --config C3 --quant --steps 5 --warmup 3 --no-cpu-baseline --no-int8-peak --recall-queries 2000 > gpurun_out/ev_bench_C3-quant.json 2> gpurun_out/ev_bench_quant.err; echo quant=$?
 CMD="python tools/build_once.py C5"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ev_launches_C5.csv $CMD > gpurun_out/ev_ncu_launch.log 2>&1; echo ncu_launch=$?
-timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:dist_topk_uf2_kernel -s 2 -c 1 -o gpurun_out/ev_leaf_C5 $CMD > gpurun_out/ev_ncu_leaf.log 2>&1; echo ncu_leaf=$?
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:dist_topk_uf2_kernelILi8ELb0E -s 2 -c 1 -o gpurun_out/ev_leaf_C5 $CMD > gpurun_out/ev_ncu_leaf.log 2>&1; echo ncu_leaf=$?
 ncu -i gpurun_out/ev_leaf_C5.ncu-rep --page raw --csv > gpurun_out/ev_leaf_C5_raw.csv 2>/dev/null
-KERNELS="hp_emit_kernel hp_merge_rows_kernel hp_defer_sort_kernel fp_gram_kernel fp_band_kernel dist_topk_kernelILb1ELb0ELi2ELb0E leaders_kernel" bash tools/gpu_prof_kernels.sh
-for K in hp_emit_kernel hp_merge_rows_kernel hp_defer_sort_kernel fp_gram_kernel fp_band_kernel dist_topk_kernelILb1ELb0ELi2ELb0E leaders_kernel; do
+KERNELS="hp_emit_kernel hp_merge_rows_kernel hp_defer_sort_kernel fp_gram_kernel fp_band_kernel dist_topk_uf2_kernelILi2ELb1E leaders_kernel" bash tools/gpu_prof_kernels.sh
+for K in hp_emit_kernel hp_merge_rows_kernel hp_defer_sort_kernel fp_gram_kernel fp_band_kernel dist_topk_uf2_kernelILi2ELb1E leaders_kernel; do
   echo "== $K"; python tools/ncu_raw_summary.py gpurun_out/k_C5_${K}_raw.csv
 done > gpurun_out/ev_kernels_C5_ncu_summary.txt 2>&1
 python tools/ncu_raw_summary.py gpurun_out/ev_leaf_C5_raw.csv > gpurun_out/ev_leaf_C5_ncu_summary.txt 2>&1
