@@ -405,6 +405,9 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t 
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
                "l"(src), "r"(src_bytes));
 }
+__device__ __forceinline__ void cp_async16_s(uint32_t dst_smem, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "r"(src_bytes));
+}
 __device__ __forceinline__ void cp_async_fence() { asm volatile("" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
@@ -451,12 +454,15 @@ __device__ __forceinline__ void gp_stage(const void* __restrict__ Xv, int64_t ld
     const int64_t rb = U8 ? ld : 2 * ld;
     const int lim = U8 ? d : (int)(2 * ld);
     cp_async_fence();
-    if (act)
-      for (int r = rr; r < nrp; r += rpp) {
-        const bool on = r < nr && cb < lim;
-        const uint8_t* src = on ? (const uint8_t*)Xv + (int64_t)ids[r] * rb + cb : (const uint8_t*)Xv;
-        cp_async16(rows + (size_t)r * L.pitch + ch * 16, src, on ? 16u : 0u);
-      }
+    if (act) {
+      // branch-free per row: padding rows (r >= nr) re-address the last real row with a zero-byte source
+      const bool col_on = cb < lim;
+      const uint8_t* xb = (const uint8_t*)Xv + (col_on ? cb : 0);
+      uint32_t dst = (uint32_t)__cvta_generic_to_shared(rows + (size_t)rr * L.pitch + ch * 16);
+      const uint32_t dstep = (uint32_t)(rpp * L.pitch);
+      for (int r = rr; r < nrp; r += rpp, dst += dstep)
+        cp_async16_s(dst, xb + (int64_t)ids[min(r, nr - 1)] * rb, (col_on && r < nr) ? 16u : 0u);
+    }
     cp_async_wait_all();
     return;
   }
@@ -766,12 +772,15 @@ __device__ __forceinline__ void gp_stage_group(const void* __restrict__ Xv, int6
     const int64_t rb = U8 ? ld : 2 * ld;
     const int lim = U8 ? d : (int)(2 * ld);
     cp_async_fence();
-    if (act)
-      for (int r = rr; r < nrp; r += rpp) {
-        const bool on = r < nr && cb < lim;
-        const uint8_t* src = on ? (const uint8_t*)Xv + (int64_t)ids[r] * rb + cb : (const uint8_t*)Xv;
-        cp_async16(rows + (size_t)r * L.pitch + ch * 16, src, on ? 16u : 0u);
-      }
+    if (act) {
+      // branch-free per row: padding rows (r >= nr) re-address the last real row with a zero-byte source
+      const bool col_on = cb < lim;
+      const uint8_t* xb = (const uint8_t*)Xv + (col_on ? cb : 0);
+      uint32_t dst = (uint32_t)__cvta_generic_to_shared(rows + (size_t)rr * L.pitch + ch * 16);
+      const uint32_t dstep = (uint32_t)(rpp * L.pitch);
+      for (int r = rr; r < nrp; r += rpp, dst += dstep)
+        cp_async16_s(dst, xb + (int64_t)ids[min(r, nr - 1)] * rb, (col_on && r < nr) ? 16u : 0u);
+    }
     cp_async_wait_all();
     return;
   }
