@@ -428,7 +428,7 @@ __host__ __device__ inline GpLayout gp_layout(int d, bool u8, int CP) {
   L.rows_off = o;
   o += (size_t)CP * L.pitch;
   L.g_off = o;
-  o += (size_t)CP * (CP + 1) * 4;
+  o += (size_t)CP * (CP + 4) * 4;  // Gram row stride CP + 4 words (see fp_gram_kernel)
   L.nrm_off = o;
   o += (size_t)CP * 4;
   L.ids_off = o;
@@ -532,10 +532,14 @@ __global__ void __launch_bounds__(256, CP == 32 ? 3 : 1) fp_gram_kernel(const vo
   const int wpb = blockDim.x >> 5;
   uint8_t* base = gsm + (size_t)warp * L.per_warp;
   uint8_t* rows = base + L.rows_off;
-  DT* G = (DT*)(base + L.g_off);  // [CP][CP + 1] Gram
+  DT* G = (DT*)(base + L.g_off);  // [CP][CP + 4] Gram
   DT* nrm = (DT*)(base + L.nrm_off);
   uint32_t* ids = (uint32_t*)(base + L.ids_off);
-  const int DS = CP + 1;
+  // Row stride = 4 mod 32 words and the accumulator fragments stored transposed (the Gram is symmetric): element
+  // (r, s) of a fragment goes to G[s][r], word (2 t4 + e) DS + g + const = 8 t4 + g + const mod 32 — all 32 lanes
+  // of a store on distinct banks (stride CP + 1 with the direct store was a 4-way conflict, 25% of the kernel's
+  // shared-memory wavefronts, and the kernel is bound by that pipe: l1tex data-pipe 70% busy).
+  const int DS = CP + 4;
   const int g = lane >> 2, t4 = lane & 3;
   const int64_t n_iter = list ? (int64_t)*list_n : n;
 
@@ -588,21 +592,21 @@ __global__ void __launch_bounds__(256, CP == 32 ? 3 : 1) fp_gram_kernel(const vo
         for (int bj = 0; bj < CP / 8; ++bj) {
           if (bj < 2 * nb16) {
             const int r = bi * 16 + g, s = bj * 8 + 2 * t4;
-            DT* d0 = G + (size_t)r * DS + s;
-            DT* d1 = G + (size_t)(r + 8) * DS + s;
+            DT* d0 = G + (size_t)s * DS + r;  // (r, s), (r + 8, s) -> G[s][r], G[s][r + 8]
+            DT* d1 = d0 + DS;                 // (r, s + 1), (r + 8, s + 1)
             if (U8) {
               if (kc0 == 0) {
-                d0[0] = acc[bj][0]; d0[1] = acc[bj][1]; d1[0] = acc[bj][2]; d1[1] = acc[bj][3];
+                d0[0] = acc[bj][0]; d1[0] = acc[bj][1]; d0[8] = acc[bj][2]; d1[8] = acc[bj][3];
               } else {
-                d0[0] += acc[bj][0]; d0[1] += acc[bj][1]; d1[0] += acc[bj][2]; d1[1] += acc[bj][3];
+                d0[0] += acc[bj][0]; d1[0] += acc[bj][1]; d0[8] += acc[bj][2]; d1[8] += acc[bj][3];
               }
             } else {
               if (kc0 == 0) {
-                d0[0] = __int_as_float(acc[bj][0]); d0[1] = __int_as_float(acc[bj][1]);
-                d1[0] = __int_as_float(acc[bj][2]); d1[1] = __int_as_float(acc[bj][3]);
+                d0[0] = __int_as_float(acc[bj][0]); d1[0] = __int_as_float(acc[bj][1]);
+                d0[8] = __int_as_float(acc[bj][2]); d1[8] = __int_as_float(acc[bj][3]);
               } else {
-                d0[0] += __int_as_float(acc[bj][0]); d0[1] += __int_as_float(acc[bj][1]);
-                d1[0] += __int_as_float(acc[bj][2]); d1[1] += __int_as_float(acc[bj][3]);
+                d0[0] += __int_as_float(acc[bj][0]); d1[0] += __int_as_float(acc[bj][1]);
+                d0[8] += __int_as_float(acc[bj][2]); d1[8] += __int_as_float(acc[bj][3]);
               }
             }
           }

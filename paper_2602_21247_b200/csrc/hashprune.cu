@@ -981,18 +981,20 @@ constexpr uint64_t kDstOvf = 1ull << 63;
 // count / cursor (4), duplicate mask (2), valid picks (1).
 constexpr int kEmitBytesPerMember = 19;
 
-template <typename ST, int NT>
-__global__ void __launch_bounds__(NT) hp_emit_kernel(const int64_t* __restrict__ leaf_off, const uint32_t* __restrict__ leaf_ids,
+template <typename ST, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) hp_emit_kernel(const int64_t* __restrict__ leaf_off, const uint32_t* __restrict__ leaf_ids,
                                                       int k, const uint16_t* __restrict__ cols,
                                                       const float* __restrict__ dist, const ST* __restrict__ S, int m,
                                                       int stage_sk, int l_max, uint64_t* __restrict__ slots,
                                                       uint32_t* __restrict__ count, HpOverflow ov,
-                                                      int64_t* __restrict__ n_edges, int* __restrict__ err) {
+                                                      int64_t* __restrict__ n_edges, int* __restrict__ err,
+                                                      int s_lo, int s_hi) {
   extern __shared__ __align__(16) uint8_t esm[];
   __shared__ uint32_t picks_sh;
   const int64_t b = blockIdx.x;
   const int64_t o0 = leaf_off[b];
   const int s = (int)(leaf_off[b + 1] - o0);
+  if (s <= s_lo || s > s_hi) return;  // size class of this launch: leaves of s_lo < s <= s_hi members
   const int ms = m | 1;                          // SMEM sketch row stride (odd: conflict-free row-per-thread reads)
   uint64_t* dst = (uint64_t*)esm;                // [s] where the instance's keys go (slots index | kDstOvf + offset)
   uint32_t* ids = (uint32_t*)(dst + s);          // [s]
@@ -1629,18 +1631,31 @@ pipnn_status hashprune_from_leaves(int m, int l_max, int64_t n, const void* sket
   const int stage_sk = mem_bytes + sk_bytes <= 200 * 1024 ? 1 : 0;
   const int smem = (int)(mem_bytes + (stage_sk ? sk_bytes : 0));
   const bool big = max_leaf > 1024;
-#define HP_EMIT(ST, NTH)                                                                                          \
+  // Leaves above 1024 members take 1024-thread CTAs (one per SM: 145 KB of SMEM at 2048 members); with such
+  // leaves present the smaller ones go in a launch of their own with 512-thread CTAs and SMEM for 1024 members
+  // (two per SM, so one CTA's barriers and claim latencies overlap the other's work). Both launches span all
+  // leaves; a CTA whose leaf is not of the launch's size class exits at once.
+  const int smem_half = (int)((size_t)1024 * kEmitBytesPerMember + (stage_sk ? (size_t)1024 * (m | 1) * 4 : 0));
+#define HP_EMIT(ST, NTH, MINB, SM, LO, HI)                                                                        \
   do {                                                                                                            \
-    PIPNN_CUDA(cudaFuncSetAttribute(hp_emit_kernel<ST, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
-    hp_emit_kernel<ST, NTH><<<(unsigned)n_leaves, NTH, smem, c.st>>>(leaf_off, leaf_ids, k, cols, dist,           \
-                                                                   (const ST*)sketch, m, stage_sk, l_max, slots,   \
-                                                                   count, ov, n_edges_dev, c.err);                 \
+    PIPNN_CUDA(cudaFuncSetAttribute(hp_emit_kernel<ST, NTH, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, SM)); \
+    hp_emit_kernel<ST, NTH, MINB><<<(unsigned)n_leaves, NTH, SM, c.st>>>(leaf_off, leaf_ids, k, cols, dist,       \
+                                                                 (const ST*)sketch, m, stage_sk, l_max, slots,     \
+                                                                 count, ov, n_edges_dev, c.err, LO, HI);           \
+  } while (0)
+#define HP_EMIT_BIG(ST)                                     \
+  do {                                                      \
+    HP_EMIT(ST, 512, 2, smem_half, 0, 1024);                \
+    HP_EMIT(ST, 1024, 1, smem, 1024, 1 << 30);              \
   } while (0)
   if (sk_int) {
-    if (big) HP_EMIT(int32_t, 1024); else HP_EMIT(int32_t, 256);
+    if (big) HP_EMIT_BIG(int32_t);
+    else HP_EMIT(int32_t, 256, 1, smem, 0, 1 << 30);
   } else {
-    if (big) HP_EMIT(float, 1024); else HP_EMIT(float, 256);
+    if (big) HP_EMIT_BIG(float);
+    else HP_EMIT(float, 256, 1, smem, 0, 1 << 30);
   }
+#undef HP_EMIT_BIG
 #undef HP_EMIT
   PIPNN_LAUNCHED("hp_emit_kernel", c.st);
   // (2) row merge per owner; owners with long rows (hubs, overflow) through the deferred kernels
