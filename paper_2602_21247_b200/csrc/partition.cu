@@ -928,7 +928,12 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
     PIPNN_CUDA(kcopy_batch(hd, 3, st));
     PIPNN_CUDA(cudaEventRecord(ev_sync, st));
     PIPNN_TRY(launch_pending());  // the previous level's device subtrees (see PendingSubtree)
-    if (c.side_work && *c.side_work) {  // the caller's independent work (pipnn_build: sketches), once
+    // the caller's independent work (pipnn_build: sketches), once, behind the read-back of the level with the
+    // longest host plan, so that it fills the GPU's idle time there: depth 0 (<= leader_cap children), or depth 1
+    // when that level is expected to have many more children (C5: ~98k, 2.7 ms of planning with the GPU otherwise
+    // idle; C2: ~4k, where depth 0 measured better). A partition that ends first leaves it to the caller.
+    const bool side_later = depth == 0 && (double)Q * (double)p->p_samp_num / (double)std::max<int64_t>(1, p->p_samp_den) >= 32768.0;
+    if (!side_later && c.side_work && *c.side_work) {
       std::function<pipnn_status()> fn;
       fn.swap(*c.side_work);
       PIPNN_TRY(fn());
