@@ -355,6 +355,9 @@ __global__ void __launch_bounds__(kUf2Threads, 1) dist_topk_uf2_kernel(const Dis
             const int valid = min(32, ncols - col0);
             uint32_t v[32];
             ptx::tmem_ld32(tacc + j0, v);
+            // the chunk's parity word, needed only when a lane passes: loaded here so that its latency overlaps the
+            // TMEM load instead of sitting in the candidate path
+            const uint32_t pbits = __ldg(reinterpret_cast<const uint32_t*>(args.nb) + ((S.b.pos + col0) >> 5));
             const int32_t kk8 = (int32_t)kk[KMAX - 1];
             const int32_t tau = kk8 != (int32_t)kInf ? ((-kk8) >> 1) : -(int32_t)U;
             ptx::tmem_ld_wait();
@@ -368,7 +371,6 @@ __global__ void __launch_bounds__(kUf2Threads, 1) dist_topk_uf2_kernel(const Dis
             if (valid < 32) mask &= (1u << valid) - 1u;
             if (col0 == diag_chunk) mask &= ~(1u << lane);  // self exclusion (the diagonal element)
             if (__any_sync(0xffffffffu, mask != 0)) {
-              const uint32_t pbits = reinterpret_cast<const uint32_t*>(args.nb)[(S.b.pos + col0) >> 5];  // parities
               if (mask) {
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
