@@ -20,6 +20,7 @@
 // At the end, leaf sizes -> exclusive scan -> leaf_off, and the staged leaves are compacted into leaf_ids.
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <chrono>
 #include <cstdlib>
 #include <cub/cub.cuh>
@@ -957,10 +958,11 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
     // leaves, jobs and next-level groups are then emitted in group order as before.
     const double t_copy = dbg_timing ? wall() : 0.0;
     std::vector<HMerge> plans(G);
-    auto plan_groups = [&](int g0, int gstep) {
+    std::atomic<int> next_g{0};
+    auto plan_groups = [&]() {  // groups are claimed from a counter: any number of started threads completes them
       std::vector<int64_t> sz;
       std::vector<std::pair<uint64_t, uint32_t>> mk;
-      for (int g = g0; g < G; g += gstep) {
+      for (int g; (g = next_g.fetch_add(1, std::memory_order_relaxed)) < G;) {
         const PGroup& q = hg[g];
         sz.resize(q.l);
         mk.resize(q.l);
@@ -977,8 +979,14 @@ static pipnn_status partition_body(const pipnn_points* X, const pipnn_partition_
       const int hw = (int)std::thread::hardware_concurrency();
       const int nt = std::max(1, std::min({8, hw > 1 ? hw - 1 : 1, G / 64}));
       std::vector<std::thread> th;
-      for (int t = 1; t < nt; ++t) th.emplace_back(plan_groups, t, nt);
-      plan_groups(0, nt);
+      for (int t = 1; t < nt; ++t) {
+        try {
+          th.emplace_back(plan_groups);
+        } catch (...) {  // no thread available: the calling thread plans the rest
+          break;
+        }
+      }
+      plan_groups();
       for (auto& t : th) t.join();
     }
     const double t_planned = dbg_timing ? wall() : 0.0;
